@@ -1,0 +1,184 @@
+/*
+ * tt_b200.h -- C ABI of libtt_b200.so, the B200 (sm_100a) hot path of the
+ * tensortune cost model (arXiv 2304.05430 reproduction).
+ *
+ * The reference (/root/reference/pkg/src/tensortune) is pure Python; its
+ * "plugin API" for this path is the duck-typed estimator / metric / sampling
+ * functions listed beside each entry point below.  The Python host package
+ * paper_2304_05430_b200 binds these symbols with ctypes and exposes the
+ * reference's own names; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *  - plain pointers + sizes, no C++ or torch types;
+ *  - "d_" pointers are device memory, "h_" pointers host memory;
+ *  - every call is asynchronous on `stream` (a cudaStream_t passed as void*)
+ *    unless stated; buffers are caller-owned; the workspace of a call must
+ *    not be shared with a concurrently running call;
+ *  - return value: TT_OK or an error code; tt_last_error() gives a
+ *    thread-local message.  No exceptions cross the ABI.
+ *  - *_f32 entry points compute in float32 (the production path), *_f64 in
+ *    float64 (the parity/debug build of the same kernels).
+ */
+#ifndef TT_B200_H
+#define TT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TT_OK 0
+#define TT_EINVAL 1        /* bad argument (shape, size, unsupported width) */
+#define TT_ENONFINITE 2    /* reserved: non-finite data detected host-side */
+#define TT_ECUDA 3         /* CUDA runtime error (launch, co-residency, ...) */
+
+#define TT_LOSS_MSE 0      /* tuner.py:373-375, mlp.py:105-108 */
+#define TT_LOSS_RANK 1     /* mlp.py:25-35 (pairwise logistic) */
+
+#define TT_MODE_TRAIN 0    /* forward + backward + Adam for every minibatch */
+#define TT_MODE_GRAD 1     /* one minibatch: forward + backward, write gradient */
+
+typedef void *tt_stream_t;
+
+int tt_abi_version(void);
+const char *tt_last_error(void);
+
+/* ------------------------------------------------------------------ PCA --
+ * replaces metrics.py:46-58 pairwise_comparison_accuracy (called per task by
+ * models.py:384-419 per_task_metrics and tuner.py:486-496 _grouped_pca).
+ * Tasks are CSR segments of (y, s); d_correct[t] receives the exact number
+ * of pairs i<j of task t with sign(y_i-y_j) == sign(s_i-s_j).  The caller
+ * zero-fills nothing: the call overwrites d_correct.  h_offsets is a HOST
+ * array (n_tasks+1) -- it is needed to plan the pair tiles. */
+size_t tt_pca_workspace_bytes(const int64_t *h_offsets, int32_t n_tasks);
+int tt_pca_counts(const double *d_y, const double *d_s, const int64_t *h_offsets,
+                  int32_t n_tasks, int64_t *d_correct, void *d_ws, size_t ws_bytes,
+                  tt_stream_t stream);
+
+/* replaces metrics.py:61-75 top_k_score: per task, d_pick[t] = max y over the
+ * min(k, n_t) best scores (stable: ties broken by lower index), d_best[t] =
+ * max y.  top_k_score = d_pick / d_best (computed by the caller). */
+int tt_topk(const double *d_y, const double *d_s, const int64_t *d_offsets, int32_t n_tasks,
+            int32_t k, double *d_pick, double *d_best, tt_stream_t stream);
+
+/* ------------------------------------------------------------ rank loss --
+ * replaces estimators/mlp.py:25-35 ranking_grad, one segment per minibatch;
+ * max_seg bounds the longest segment (sizes shared memory). */
+int tt_rank_loss_f32(const float *d_y, const float *d_s, const int64_t *d_offsets,
+                     int32_t n_segs, int32_t max_seg, float *d_loss, float *d_grad,
+                     tt_stream_t stream);
+int tt_rank_loss_f64(const double *d_y, const double *d_s, const int64_t *d_offsets,
+                     int32_t n_segs, int32_t max_seg, double *d_loss, double *d_grad,
+                     tt_stream_t stream);
+
+/* ----------------------------------------------------------------- Adam --
+ * replaces estimators/optim.py:33-46 Adam.step on a flat parameter vector.
+ * corr1 = 1 - b1^t, corr2 = 1 - b2^t (t = step counter after increment).
+ * d_mask (uint8 per element, may be NULL) selects trainable entries. */
+int tt_adam_step_f32(float *d_param, const float *d_grad, float *d_m, float *d_v, int64_t n,
+                     const uint8_t *d_mask, double lr, double b1, double b2, double eps,
+                     double corr1, double corr2, tt_stream_t stream);
+int tt_adam_step_f64(double *d_param, const double *d_grad, double *d_m, double *d_v, int64_t n,
+                     const uint8_t *d_mask, double lr, double b1, double b2, double eps,
+                     double corr1, double corr2, tt_stream_t stream);
+
+/* ---------------------------------------------------- attention tuner --
+ * replaces estimators/tuner.py RecurrentAttentionTuner._forward/_backward/
+ * loss_and_gradients/_train/predict (tuner.py:227-476).
+ *
+ * Parameters: one flat vector, tensors in the reference's dict order
+ * (tuner.py:194-210), each row-major:
+ *   for l < layers, for dir in (fw, bw): Wx[d_in][4H], Wh[H][4H], b[4H]
+ *   attn_Wq, attn_Wk, attn_Wv, attn_Wo [2H][2H], attn_bq[2H], attn_bo[2H],
+ *   head_W1[2H+C][64], head_b1[64], head_W2[64][1], head_b2[1]
+ * with d_in = step_width for l == 0 else 2H.  hidden in {4, 8, 16, 32}.
+ * Programs: CSR -- d_steps (total_rows x step_width), d_row_offsets (n+1,
+ * int64), d_ctx (n x ctx_len); every program has 1..max_steps rows. */
+int64_t tt_tuner_param_count(int32_t layers, int32_t hidden, int32_t step_width,
+                             int32_t ctx_len);
+size_t tt_tuner_predict_workspace_bytes(int32_t f64, int32_t layers, int32_t hidden,
+                                        int32_t max_steps);
+int tt_tuner_predict_f32(const float *d_params, const float *d_steps,
+                         const int64_t *d_row_offsets, const float *d_ctx, int64_t n,
+                         int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                         int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                         float *d_yhat, void *d_ws, size_t ws_bytes, tt_stream_t stream);
+int tt_tuner_predict_f64(const double *d_params, const double *d_steps,
+                         const int64_t *d_row_offsets, const double *d_ctx, int64_t n,
+                         int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                         int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                         double *d_yhat, void *d_ws, size_t ws_bytes, tt_stream_t stream);
+
+/* Training (tuner.py:427-466) / gradients (tuner.py:364-376).
+ * d_order lists sample indices; minibatch k is d_order[k*B, min((k+1)*B, n_order)).
+ * TT_MODE_TRAIN: every minibatch runs forward, loss, backward, a deterministic
+ *   fixed-order gradient reduction and the fused Adam update; d_corr holds
+ *   (1-b1^t, 1-b2^t) per minibatch; d_step_loss[k] receives the loss; on a
+ *   non-finite loss d_status[0] = k and the kernel stops before updating.
+ * TT_MODE_GRAD: exactly one minibatch (B = n_order); d_grad_out receives the
+ *   full gradient (param_count) and d_step_loss[0] the loss; no update.
+ * d_trainable: uint8 per parameter element or NULL (all trainable). */
+size_t tt_tuner_train_workspace_bytes(int32_t f64, int32_t layers, int32_t hidden,
+                                      int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                                      int32_t batch_size);
+int tt_tuner_train_f32(float *d_params, float *d_m, float *d_v, const float *d_steps,
+                       const int64_t *d_row_offsets, const float *d_ctx, const float *d_y,
+                       const int32_t *d_order, int64_t n_order, int32_t batch_size,
+                       int32_t loss_kind, int32_t mode, double lr, double b1, double b2,
+                       double eps, const double *d_corr, const uint8_t *d_trainable,
+                       int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                       int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                       float *d_step_loss, float *d_grad_out, int32_t *d_status, void *d_ws,
+                       size_t ws_bytes, tt_stream_t stream);
+int tt_tuner_train_f64(double *d_params, double *d_m, double *d_v, const double *d_steps,
+                       const int64_t *d_row_offsets, const double *d_ctx, const double *d_y,
+                       const int32_t *d_order, int64_t n_order, int32_t batch_size,
+                       int32_t loss_kind, int32_t mode, double lr, double b1, double b2,
+                       double eps, const double *d_corr, const uint8_t *d_trainable,
+                       int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                       int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                       double *d_step_loss, double *d_grad_out, int32_t *d_status, void *d_ws,
+                       size_t ws_bytes, tt_stream_t stream);
+
+/* ------------------------------------------------------------ cost MLP --
+ * replaces estimators/mlp.py CostMLP._forward/_backward/fit/predict
+ * (mlp.py:72-155).  Params flat in dict order W1[F][64], b1[64], W2[64][64],
+ * b2[64], W3[64][1], b3[1]; X is n x F row-major. */
+int64_t tt_mlp_param_count(int32_t n_features);
+int tt_mlp_predict_f32(const float *d_params, const float *d_X, int64_t n, int32_t n_features,
+                       float *d_out, tt_stream_t stream);
+int tt_mlp_predict_f64(const double *d_params, const double *d_X, int64_t n,
+                       int32_t n_features, double *d_out, tt_stream_t stream);
+size_t tt_mlp_train_workspace_bytes(int32_t f64, int32_t n_features, int32_t batch_size);
+int tt_mlp_train_f32(float *d_params, float *d_m, float *d_v, const float *d_X, const float *d_y,
+                     int32_t n_features, const int32_t *d_order, int64_t n_order,
+                     int32_t batch_size, int32_t loss_kind, int32_t mode, double lr, double b1,
+                     double b2, double eps, const double *d_corr, float *d_step_loss,
+                     float *d_grad_out, int32_t *d_status, void *d_ws, size_t ws_bytes,
+                     tt_stream_t stream);
+int tt_mlp_train_f64(double *d_params, double *d_m, double *d_v, const double *d_X,
+                     const double *d_y, int32_t n_features, const int32_t *d_order,
+                     int64_t n_order, int32_t batch_size, int32_t loss_kind, int32_t mode,
+                     double lr, double b1, double b2, double eps, const double *d_corr,
+                     double *d_step_loss, double *d_grad_out, int32_t *d_status, void *d_ws,
+                     size_t ws_bytes, tt_stream_t stream);
+
+/* ------------------------------------------------- pruning statistics --
+ * replaces sampling.py:37-59 filter_invalid's arithmetic (+ data.py:440-446
+ * throughput and numpy's linear quantile).  Records are CSR by task
+ * (d_task_offsets, n_tasks+1); d_valid marks non-error records (cost must be
+ * > 0 for them).  Outputs: d_thr[t] (NaN for tasks without valid records),
+ * d_survivors[t], d_task_keep[t], d_keep[r] (record kept by filter_invalid).
+ * Bit-exact with numpy float64. */
+size_t tt_prune_workspace_bytes(int64_t n_records);
+int tt_prune_stats(const int64_t *d_flops, const double *d_cost, const uint8_t *d_valid,
+                   const int64_t *d_task_offsets, int32_t n_tasks, double q,
+                   int32_t min_records, double *d_thr, uint8_t *d_keep, int32_t *d_survivors,
+                   uint8_t *d_task_keep, void *d_ws, size_t ws_bytes, tt_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TT_B200_H */

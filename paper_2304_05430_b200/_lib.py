@@ -1,0 +1,97 @@
+"""ctypes binding of libtt_b200.so (the C ABI declared in include/tt_b200.h).
+
+The product path has no fallback: if the shared library is missing or a CUDA
+device is absent, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtt_b200.so")
+
+_P, _I32, _I64, _D, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
+
+TT_LOSS_MSE, TT_LOSS_RANK = 0, 1
+TT_MODE_TRAIN, TT_MODE_GRAD = 0, 1
+
+# name -> (restype, argtypes); mirrors include/tt_b200.h one to one
+SIGNATURES: dict[str, tuple] = {
+    "tt_abi_version": (ctypes.c_int, []),
+    "tt_last_error": (ctypes.c_char_p, []),
+    "tt_pca_workspace_bytes": (_SZ, [_P, _I32]),
+    "tt_pca_counts": (ctypes.c_int, [_P, _P, _P, _I32, _P, _P, _SZ, _P]),
+    "tt_topk": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _P, _P, _P]),
+    "tt_rank_loss_f32": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _P, _P, _P]),
+    "tt_rank_loss_f64": (ctypes.c_int, [_P, _P, _P, _I32, _I32, _P, _P, _P]),
+    "tt_adam_step_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _D, _D, _D, _D, _D, _D, _P]),
+    "tt_adam_step_f64": (ctypes.c_int, [_P, _P, _P, _P, _I64, _P, _D, _D, _D, _D, _D, _D, _P]),
+    "tt_tuner_param_count": (_I64, [_I32, _I32, _I32, _I32]),
+    "tt_tuner_predict_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I32]),
+    "tt_tuner_predict_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64] + [_I32] * 7 + [_P, _P, _SZ, _P]),
+    "tt_tuner_predict_f64": (ctypes.c_int, [_P, _P, _P, _P, _I64] + [_I32] * 7 + [_P, _P, _SZ, _P]),
+    "tt_tuner_train_workspace_bytes": (_SZ, [_I32] * 7),
+    "tt_tuner_train_f32": (ctypes.c_int, [_P] * 7 + [_P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P, _P]
+                           + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
+    "tt_tuner_train_f64": (ctypes.c_int, [_P] * 7 + [_P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P, _P]
+                           + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
+    "tt_mlp_param_count": (_I64, [_I32]),
+    "tt_mlp_predict_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    "tt_mlp_predict_f64": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    "tt_mlp_train_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
+    "tt_mlp_train_f32": (ctypes.c_int, [_P] * 5 + [_I32, _P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P,
+                                                   _P, _P, _P, _P, _SZ, _P]),
+    "tt_mlp_train_f64": (ctypes.c_int, [_P] * 5 + [_I32, _P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P,
+                                                   _P, _P, _P, _P, _SZ, _P]),
+    "tt_prune_workspace_bytes": (_SZ, [_I64]),
+    "tt_prune_stats": (ctypes.c_int, [_P, _P, _P, _P, _I32, _D, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LibraryError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the shared library; raise if it is missing."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise LibraryError(
+                f"{path} is missing: build it with `python -m paper_2304_05430_b200.build` "
+                "(there is no CPU fallback)")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name, None)
+            if fn is None:  # reported by missing_symbols(); calling it raises
+                continue
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def call(name: str, *args) -> None:
+    """Invoke an int-returning entry point and raise on a non-zero status."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if rc != 0:
+        msg = lib.tt_last_error()
+        raise LibraryError(f"{name} failed (status {rc}): {msg.decode() if msg else ''}")
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def missing_symbols() -> list[str]:
+    lib = load()
+    return [n for n in SIGNATURES if getattr(lib, n, None) is None]

@@ -1,0 +1,121 @@
+// Shared device/host helpers for libtt_b200 (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <cmath>
+
+#include "../../include/tt_b200.h"
+
+namespace tt {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+
+#define TT_REQUIRE(cond, ...)        \
+  do {                               \
+    if (!(cond)) {                   \
+      ::tt::set_error(__VA_ARGS__);  \
+      return TT_EINVAL;              \
+    }                                \
+  } while (0)
+
+#define TT_CUDA(call)                                                           \
+  do {                                                                          \
+    cudaError_t e__ = (call);                                                   \
+    if (e__ != cudaSuccess) {                                                   \
+      ::tt::set_error("%s failed: %s", #call, cudaGetErrorString(e__));        \
+      return TT_ECUDA;                                                          \
+    }                                                                           \
+  } while (0)
+
+inline cudaStream_t as_stream(tt_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int sm_count();
+
+// ------------------------------------------------------------ arithmetic --
+// Activations.  float: ex2.approx-based exp + approximate reciprocal, error a
+// few ulp (well inside the 1e-5 score tolerance; tanh.approx's 5e-4 is not).
+// double: libdevice exp/tanh, matching numpy to ~1 ulp.
+template <typename R>
+struct Act;
+
+template <>
+struct Act<float> {
+  static __device__ __forceinline__ float sigmoid(float x) {
+    return __fdividef(1.0f, 1.0f + __expf(-x));
+  }
+  static __device__ __forceinline__ float tanh(float x) {
+    // 1 - 2/(e^{2x}+1): exact limits at +-inf, absolute error ~1e-7.
+    return 1.0f - __fdividef(2.0f, __expf(2.0f * x) + 1.0f);
+  }
+  static __device__ __forceinline__ float exp(float x) { return __expf(x); }
+  static __device__ __forceinline__ float softplus(float x) {
+    // log(1 + e^x) computed as max(x,0) + log1p(e^-|x|)  (np.logaddexp(0, x))
+    return fmaxf(x, 0.0f) + log1pf(__expf(-fabsf(x)));
+  }
+  static __device__ __forceinline__ float rsqrt(float x) { return rsqrtf(x); }
+};
+
+template <>
+struct Act<double> {
+  static __device__ __forceinline__ double sigmoid(double x) {
+    // tuner.py:27-33 split form
+    if (x >= 0.0) return 1.0 / (1.0 + ::exp(-x));
+    double e = ::exp(x);
+    return e / (1.0 + e);
+  }
+  static __device__ __forceinline__ double tanh(double x) { return ::tanh(x); }
+  static __device__ __forceinline__ double exp(double x) { return ::exp(x); }
+  static __device__ __forceinline__ double softplus(double x) {
+    return fmax(x, 0.0) + log1p(::exp(-fabs(x)));
+  }
+  static __device__ __forceinline__ double rsqrt(double x) { return 1.0 / ::sqrt(x); }
+};
+
+// ------------------------------------------------------------- reductions --
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Named barrier over `count` threads (multiple of 32); id 0 is __syncthreads.
+__device__ __forceinline__ void named_barrier(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Software grid barrier for cooperative (co-resident) launches.  `ctr` is a
+// zero-initialised counter; `target` advances by gridDim.x per barrier.
+__device__ __forceinline__ void grid_barrier(unsigned int* ctr, unsigned int& target) {
+  __syncthreads();
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+}  // namespace tt

@@ -1,0 +1,496 @@
+// Attention tuner kernels: bulk scoring (K5) and the fused training step
+// (K5 cached forward + K7 loss + K6 backward + deterministic reduction + K8
+// Adam) -- see tt_tuner.cuh / tt_tuner_train.cuh for the per-block code.
+#include "tt_tuner_train.cuh"
+
+namespace tt {
+
+constexpr int kScoreP = 8;  // programs per CTA tile in the scoring kernel
+
+// ----------------------------------------------------------- scoring --
+template <typename R, int P>
+struct ScoreSmemLayout {
+  static size_t bytes(const TDims& d) {
+    const size_t n = (size_t)2 * P * d.H + (size_t)2 * P * d.G + (size_t)3 * P * d.D +
+                     (size_t)P * d.heads * d.Tmax + (size_t)P * (d.D + d.C) +
+                     (size_t)P * kHeadHidden + P;
+    return n * sizeof(R) + 64;
+  }
+};
+
+template <typename R, int H, int P>
+__global__ void __launch_bounds__(kThreads) tuner_predict_kernel(
+    TDims dm, const R* __restrict__ prm, const R* __restrict__ steps,
+    const int64_t* __restrict__ rowoff, const R* __restrict__ ctx, int64_t n,
+    R* __restrict__ yhat, R* __restrict__ scratch, int64_t slot_elems) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ TileInfo<R, P> ti;
+  constexpr int D = 2 * H, G = 4 * H;
+  R* sp = reinterpret_cast<R*>(smem_raw);
+  R* sh_h = sp;
+  sp += 2 * P * H;
+  R* sh_g = sp;
+  sp += 2 * P * G;
+  AttnSmem<R, P> am;
+  am.pool = sp;
+  sp += P * D;
+  am.q = sp;
+  sp += P * D;
+  am.mix = sp;
+  sp += P * D;
+  am.alpha = sp;
+  sp += (int64_t)P * dm.heads * dm.Tmax;
+  am.z = sp;
+  sp += P * (D + dm.C);
+  am.a1 = sp;
+  sp += P * kHeadHidden;
+  R* sh_y = sp;
+  const int64_t TD = (int64_t)dm.Tmax * D;
+  R* buf[3];
+  buf[0] = scratch + (int64_t)blockIdx.x * slot_elems;
+  buf[1] = buf[0] + P * TD;
+  buf[2] = buf[1] + P * TD;
+  const int64_t n_tiles = (n + P - 1) / P;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    if (threadIdx.x < P) {
+      const int64_t p = tile * P + threadIdx.x;
+      if (p < n) {
+        const int64_t r0 = rowoff[p];
+        ti.len[threadIdx.x] = (int)(rowoff[p + 1] - r0);
+        ti.step0[threadIdx.x] = steps + r0 * dm.d0;
+        ti.ctx[threadIdx.x] = ctx + p * dm.C;
+        ti.prog[threadIdx.x] = p;
+      } else {
+        ti.len[threadIdx.x] = 0;
+        ti.step0[threadIdx.x] = steps;
+        ti.ctx[threadIdx.x] = ctx;
+        ti.prog[threadIdx.x] = -1;
+      }
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int l = 0; l < dm.L; ++l) {
+      const R* in0[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        in0[p] = l == 0 ? ti.step0[p] : buf[cur ^ 1] + p * TD;
+      const int stride = l == 0 ? dm.d0 : D;
+      lstm_layer_fwd<R, H, P, false>(dm, prm, l, ti, in0, stride, buf[cur], sh_h, sh_g, nullptr,
+                                     nullptr, nullptr);
+      __syncthreads();
+      cur ^= 1;
+    }
+    // final layer output is buf[cur ^ 1]; K -> buf[cur], V -> buf[2]
+    attention_head_fwd<R, H, P, false>(dm, prm, ti, buf[cur ^ 1], buf[cur], buf[2], am, nullptr,
+                                       sh_y);
+    if (threadIdx.x < P && ti.prog[threadIdx.x] >= 0) yhat[ti.prog[threadIdx.x]] = sh_y[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+// ----------------------------------------------------------- training --
+template <typename R>
+struct TrainArgs {
+  TDims dm;
+  TrainLayout ly;
+  R* prm;
+  R* m;
+  R* v;
+  const R* steps;
+  const int64_t* rowoff;
+  const R* ctx;
+  const R* y;
+  const int32_t* order;
+  int64_t n_order;
+  int B;
+  int loss_kind;
+  int mode;
+  int n_steps;
+  AdamHyper hyp;
+  const double* corr;
+  const uint8_t* trainable;
+  R* step_loss;
+  R* grad_out;
+  int32_t* status;
+  R* partial;          // [grid][NP]
+  R* sample_scratch;   // [grid][spc][sample_elems]
+  int spc;
+  R* bwd_scratch;      // [grid][bwd_elems]
+  R* batch_yhat;       // [B]
+  unsigned int* barrier;
+};
+
+template <typename R, int H>
+__global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ TileInfo<R, 1> ti;
+  __shared__ int s_stop;
+  constexpr int D = 2 * H, G = 4 * H, NQ = 128 / H;
+  const TDims& dm = a.dm;
+  const TrainLayout& ly = a.ly;
+  const int tid = threadIdx.x;
+  // ---- shared memory carve-up
+  R* sp = reinterpret_cast<R*>(smem_raw);
+  R* sh_h = sp;
+  sp += 2 * H;
+  R* sh_g = sp;
+  sp += 2 * G;
+  AttnSmem<R, 1> am;
+  am.pool = sp;
+  sp += D;
+  am.q = sp;
+  sp += D;
+  am.mix = sp;
+  sp += D;
+  am.alpha = sp;
+  sp += dm.heads * dm.Tmax;
+  am.z = sp;
+  sp += D + dm.C;
+  am.a1 = sp;
+  sp += kHeadHidden;
+  R* sh_y = sp;
+  sp += 4;
+  BwdSmem<R> bm;
+  bm.da1 = sp;
+  sp += kHeadHidden;
+  bm.dpool = sp;
+  sp += D;
+  bm.dmix = sp;
+  sp += D;
+  bm.dq = sp;
+  sp += D;
+  bm.dlog = sp;
+  sp += dm.heads * dm.Tmax;
+  bm.dz = sp;
+  sp += 2 * G;
+  bm.part = sp;
+  sp += 2 * NQ * H;
+  R* lb_y = sp;
+  sp += a.B;
+  R* lb_s = sp;
+  sp += a.B;
+  R* lb_d = sp;
+  sp += a.B;
+  R* red = sp;  // [kThreads]
+
+  const int64_t NP = dm.total;
+  R* part = a.partial + (int64_t)blockIdx.x * NP;
+  R* bws = a.bwd_scratch + (int64_t)blockIdx.x * ly.bwd_elems;
+  unsigned int bar_target = 0;
+  const int64_t TD = (int64_t)dm.Tmax * D;
+
+  for (int step = 0; step < a.n_steps; ++step) {
+    const int64_t b0 = (int64_t)step * a.B;
+    const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
+    // ---- forward with caches for this CTA's samples
+    int slot = 0;
+    for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
+      const int64_t idx = a.order[b0 + k];
+      R* smp = a.sample_scratch + ((int64_t)blockIdx.x * a.spc + slot) * ly.sample_elems;
+      if (tid == 0) {
+        const int64_t r0 = a.rowoff[idx];
+        ti.len[0] = (int)(a.rowoff[idx + 1] - r0);
+        ti.step0[0] = a.steps + r0 * dm.d0;
+        ti.ctx[0] = a.ctx + idx * dm.C;
+        ti.prog[0] = idx;
+      }
+      __syncthreads();
+      for (int l = 0; l < dm.L; ++l) {
+        const R* in0[1] = {l == 0 ? ti.step0[0] : smp + ly.S + (int64_t)(l - 1) * TD};
+        const int stride = l == 0 ? dm.d0 : D;
+        lstm_layer_fwd<R, H, 1, true>(dm, a.prm, l, ti, in0, stride, smp + ly.S + (int64_t)l * TD,
+                                      sh_h, sh_g, smp + ly.gates + (int64_t)l * 2 * dm.Tmax * G,
+                                      smp + ly.cst + (int64_t)l * 2 * dm.Tmax * H,
+                                      smp + ly.tcs + (int64_t)l * 2 * dm.Tmax * H);
+        __syncthreads();
+      }
+      AttnCache<R> cache{smp + ly.pin, smp + ly.q,  smp + ly.alpha, smp + ly.mix,
+                         smp + ly.z,   smp + ly.a1, smp + ly.yhat};
+      attention_head_fwd<R, H, 1, true>(dm, a.prm, ti, smp + ly.S + (int64_t)(dm.L - 1) * TD,
+                                        smp + ly.K, smp + ly.V, am, &cache, sh_y);
+      if (tid == 0) a.batch_yhat[k] = sh_y[0];
+      __syncthreads();
+    }
+    grid_barrier(a.barrier, bar_target);
+    // ---- loss over the whole minibatch (every CTA, identical arithmetic)
+    for (int k = tid; k < bn; k += kThreads) {
+      lb_y[k] = a.y[a.order[b0 + k]];
+      lb_s[k] = __ldcg(a.batch_yhat + k);
+    }
+    __syncthreads();
+    const R loss = a.loss_kind == TT_LOSS_RANK ? rank_loss_block<R>(lb_y, lb_s, bn, lb_d, red)
+                                               : mse_block<R>(lb_y, lb_s, bn, lb_d, red);
+    if (tid == 0) {
+      s_stop = !isfinite((double)loss);
+      if (blockIdx.x == 0) {
+        a.step_loss[step] = loss;
+        if (s_stop) a.status[0] = step;
+      }
+    }
+    __syncthreads();
+    if (s_stop) break;  // uniform across the grid: same inputs, same arithmetic
+    // ---- backward for this CTA's samples into its partial gradient
+    slot = 0;
+    for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
+      const int64_t idx = a.order[b0 + k];
+      const R* smp = a.sample_scratch + ((int64_t)blockIdx.x * a.spc + slot) * ly.sample_elems;
+      const int64_t r0 = a.rowoff[idx];
+      const int len = (int)(a.rowoff[idx + 1] - r0);
+      backward_sample<R, H>(dm, ly, a.prm, len, a.steps + r0 * dm.d0, lb_d[k], smp, bws, bm, part,
+                            slot == 0);
+    }
+    grid_barrier(a.barrier, bar_target);
+    // ---- deterministic fixed-order reduction + fused Adam (or gradient out)
+    const int nact = min((int)gridDim.x, bn);
+    const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
+    const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
+    for (int64_t p = (int64_t)blockIdx.x * kThreads + tid; p < NP; p += (int64_t)gridDim.x * kThreads) {
+      R g = 0;
+      for (int c = 0; c < nact; ++c) g += __ldcg(a.partial + (int64_t)c * NP + p);
+      if (a.mode == TT_MODE_GRAD) {
+        a.grad_out[p] = g;
+      } else if (!a.trainable || a.trainable[p]) {
+        R pp = __ldcg(a.prm + p), mm = a.m[p], vv = a.v[p];
+        adam_update<R>(pp, g, mm, vv, a.hyp, c1, c2);
+        a.prm[p] = pp;
+        a.m[p] = mm;
+        a.v[p] = vv;
+      }
+    }
+    grid_barrier(a.barrier, bar_target);
+  }
+}
+
+// ------------------------------------------------------------- dispatch --
+template <typename R>
+struct Launch {
+  template <int H>
+  static int predict_h(const TDims& dm, const R* prm, const R* steps, const int64_t* rowoff,
+                       const R* ctx, int64_t n, R* yhat, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+    constexpr int P = kScoreP;
+    const int64_t slot = (int64_t)3 * P * dm.Tmax * dm.D;
+    int grid = (int)std::min<int64_t>((n + P - 1) / P, (int64_t)sm_count() * 2);
+    const size_t need = (size_t)grid * slot * sizeof(R);
+    if (ws_bytes < need) {
+      // fewer resident slots if the caller gave a smaller workspace
+      grid = (int)(ws_bytes / (slot * sizeof(R)));
+      TT_REQUIRE(grid >= 1, "tuner predict: workspace too small");
+    }
+    const size_t smem = ScoreSmemLayout<R, P>::bytes(dm);
+    auto kern = tuner_predict_kernel<R, H, P>;
+    if (smem > 48 * 1024)
+      TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, kThreads, smem, st>>>(dm, prm, steps, rowoff, ctx, n, yhat,
+                                       static_cast<R*>(ws), slot);
+    return check_launch("tuner predict");
+  }
+
+  static int predict(const TDims& dm, const R* prm, const R* steps, const int64_t* rowoff,
+                     const R* ctx, int64_t n, R* yhat, void* ws, size_t ws_bytes,
+                     cudaStream_t st) {
+    switch (dm.H) {
+      case 4: return predict_h<4>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
+      case 8: return predict_h<8>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
+      case 16: return predict_h<16>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
+      case 32: return predict_h<32>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
+    }
+    set_error("tuner: hidden size %d unsupported (4, 8, 16, 32)", dm.H);
+    return TT_EINVAL;
+  }
+
+  static size_t train_smem(const TDims& d, int B) {
+    const int NQ = 128 / d.H;
+    const size_t n = 2 * d.H + 2 * d.G + 3 * d.D + d.heads * d.Tmax + d.D + d.C + kHeadHidden + 4 +
+                     kHeadHidden + 3 * d.D + d.heads * d.Tmax + 2 * d.G + 2 * NQ * d.H +
+                     3 * (size_t)B + kThreads;
+    return n * sizeof(R) + 64;
+  }
+
+  static int grid_for(int B) { return std::max(1, std::min(B, sm_count())); }
+
+  static size_t train_ws(const TDims& dm, int B) {
+    const TrainLayout ly = make_train_layout(dm);
+    const int grid = grid_for(B);
+    const int spc = (B + grid - 1) / grid;
+    size_t b = 0;
+    b += align_up((size_t)grid * dm.total * sizeof(R), 256);
+    b += align_up((size_t)grid * spc * ly.sample_elems * sizeof(R), 256);
+    b += align_up((size_t)grid * ly.bwd_elems * sizeof(R), 256);
+    b += align_up((size_t)B * sizeof(R), 256);
+    b += 256;
+    return b;
+  }
+
+  template <int H>
+  static int train_h(TrainArgs<R> a, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const int grid = grid_for(a.B);
+    a.spc = (a.B + grid - 1) / grid;
+    char* w = static_cast<char*>(ws);
+    TT_REQUIRE(ws_bytes >= train_ws(a.dm, a.B), "tuner train: workspace %zu < %zu", ws_bytes,
+               train_ws(a.dm, a.B));
+    a.partial = reinterpret_cast<R*>(w);
+    w += align_up((size_t)grid * a.dm.total * sizeof(R), 256);
+    a.sample_scratch = reinterpret_cast<R*>(w);
+    w += align_up((size_t)grid * a.spc * a.ly.sample_elems * sizeof(R), 256);
+    a.bwd_scratch = reinterpret_cast<R*>(w);
+    w += align_up((size_t)grid * a.ly.bwd_elems * sizeof(R), 256);
+    a.batch_yhat = reinterpret_cast<R*>(w);
+    w += align_up((size_t)a.B * sizeof(R), 256);
+    a.barrier = reinterpret_cast<unsigned int*>(w);
+    TT_CUDA(cudaMemsetAsync(a.barrier, 0, 256, st));
+    const size_t smem = train_smem(a.dm, a.B);
+    auto kern = tuner_train_kernel<R, H>;
+    TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    TT_REQUIRE(per_sm >= 1, "tuner train: kernel cannot be resident (smem %zu)", smem);
+    void* args[] = {&a};
+    TT_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, kThreads, args, smem, st));
+    return check_launch("tuner train");
+  }
+
+  static int train(TrainArgs<R> a, void* ws, size_t ws_bytes, cudaStream_t st) {
+    switch (a.dm.H) {
+      case 4: return train_h<4>(a, ws, ws_bytes, st);
+      case 8: return train_h<8>(a, ws, ws_bytes, st);
+      case 16: return train_h<16>(a, ws, ws_bytes, st);
+      case 32: return train_h<32>(a, ws, ws_bytes, st);
+    }
+    set_error("tuner: hidden size %d unsupported (4, 8, 16, 32)", a.dm.H);
+    return TT_EINVAL;
+  }
+};
+
+static int check_dims(int L, int H, int heads, int U, int d0, int C, int Tmax) {
+  TT_REQUIRE(L >= 1 && L <= kMaxLayers, "tuner: layers must be in [1, %d]", kMaxLayers);
+  TT_REQUIRE(H == 4 || H == 8 || H == 16 || H == 32, "tuner: hidden must be 4, 8, 16 or 32");
+  TT_REQUIRE(heads >= 1 && (2 * H) % heads == 0, "tuner: heads must divide 2*hidden");
+  TT_REQUIRE(U >= 1, "tuner: unroll must be >= 1");
+  TT_REQUIRE(d0 >= 1 && C >= 0, "tuner: bad step/context width");
+  TT_REQUIRE(Tmax >= 1 && Tmax <= 4096, "tuner: max_steps out of range");
+  return TT_OK;
+}
+
+template <typename R>
+static int predict_entry(const R* prm, const R* steps, const int64_t* rowoff, const R* ctx,
+                         int64_t n, int32_t L, int32_t H, int32_t heads, int32_t U, int32_t d0,
+                         int32_t C, int32_t Tmax, R* yhat, void* ws, size_t ws_bytes,
+                         tt_stream_t st) {
+  if (int rc = check_dims(L, H, heads, U, d0, C, Tmax)) return rc;
+  TT_REQUIRE(n >= 0, "tuner predict: negative n");
+  if (n == 0) return TT_OK;
+  const TDims dm = make_dims(L, H, heads, U, d0, C, Tmax);
+  return Launch<R>::predict(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, as_stream(st));
+}
+
+template <typename R>
+static int train_entry(R* prm, R* m, R* v, const R* steps, const int64_t* rowoff, const R* ctx,
+                       const R* y, const int32_t* order, int64_t n_order, int32_t B,
+                       int32_t loss_kind, int32_t mode, double lr, double b1, double b2,
+                       double eps, const double* corr, const uint8_t* trainable, int32_t L,
+                       int32_t H, int32_t heads, int32_t U, int32_t d0, int32_t C, int32_t Tmax,
+                       R* step_loss, R* grad_out, int32_t* status, void* ws, size_t ws_bytes,
+                       tt_stream_t st) {
+  if (int rc = check_dims(L, H, heads, U, d0, C, Tmax)) return rc;
+  TT_REQUIRE(B >= 1 && B <= 4096, "tuner train: batch size must be in [1, 4096]");
+  TT_REQUIRE(n_order >= 1, "tuner train: empty order");
+  TT_REQUIRE(mode == TT_MODE_TRAIN || mode == TT_MODE_GRAD, "tuner train: bad mode");
+  TT_REQUIRE(loss_kind == TT_LOSS_MSE || loss_kind == TT_LOSS_RANK, "tuner train: bad loss");
+  TT_REQUIRE(mode == TT_MODE_GRAD || corr != nullptr, "tuner train: corr required");
+  if (mode == TT_MODE_GRAD) TT_REQUIRE(n_order <= B, "tuner grad: one minibatch only");
+  TrainArgs<R> a{};
+  a.dm = make_dims(L, H, heads, U, d0, C, Tmax);
+  a.ly = make_train_layout(a.dm);
+  a.prm = prm;
+  a.m = m;
+  a.v = v;
+  a.steps = steps;
+  a.rowoff = rowoff;
+  a.ctx = ctx;
+  a.y = y;
+  a.order = order;
+  a.n_order = n_order;
+  a.B = B;
+  a.loss_kind = loss_kind;
+  a.mode = mode;
+  a.n_steps = (int)((n_order + B - 1) / B);
+  a.hyp = AdamHyper{lr, b1, b2, eps};
+  a.corr = corr;
+  a.trainable = trainable;
+  a.step_loss = step_loss;
+  a.grad_out = grad_out;
+  a.status = status;
+  return Launch<R>::train(a, ws, ws_bytes, as_stream(st));
+}
+
+}  // namespace tt
+
+using namespace tt;
+
+extern "C" {
+
+int64_t tt_tuner_param_count(int32_t L, int32_t H, int32_t d0, int32_t C) {
+  if (L < 1 || L > kMaxLayers) return -1;
+  return make_dims(L, H, 1, 1, d0, C, 1).total;
+}
+
+size_t tt_tuner_predict_workspace_bytes(int32_t f64, int32_t L, int32_t H, int32_t Tmax) {
+  (void)L;
+  const size_t es = f64 ? 8 : 4;
+  return (size_t)sm_count() * 2 * 3 * kScoreP * Tmax * 2 * H * es;
+}
+
+int tt_tuner_predict_f32(const float* prm, const float* steps, const int64_t* rowoff,
+                         const float* ctx, int64_t n, int32_t L, int32_t H, int32_t heads,
+                         int32_t U, int32_t d0, int32_t C, int32_t Tmax, float* yhat, void* ws,
+                         size_t ws_bytes, tt_stream_t st) {
+  return predict_entry<float>(prm, steps, rowoff, ctx, n, L, H, heads, U, d0, C, Tmax, yhat, ws,
+                              ws_bytes, st);
+}
+
+int tt_tuner_predict_f64(const double* prm, const double* steps, const int64_t* rowoff,
+                         const double* ctx, int64_t n, int32_t L, int32_t H, int32_t heads,
+                         int32_t U, int32_t d0, int32_t C, int32_t Tmax, double* yhat, void* ws,
+                         size_t ws_bytes, tt_stream_t st) {
+  return predict_entry<double>(prm, steps, rowoff, ctx, n, L, H, heads, U, d0, C, Tmax, yhat, ws,
+                               ws_bytes, st);
+}
+
+size_t tt_tuner_train_workspace_bytes(int32_t f64, int32_t L, int32_t H, int32_t d0, int32_t C,
+                                      int32_t Tmax, int32_t B) {
+  if (L < 1 || L > kMaxLayers || B < 1) return 0;
+  const TDims dm = make_dims(L, H, 2, 2, d0, C, Tmax);
+  // heads/unroll only size small cache segments; use generous upper bounds
+  TDims big = dm;
+  big.heads = 2 * H;
+  big.U = 16;
+  return f64 ? Launch<double>::train_ws(big, B) : Launch<float>::train_ws(big, B);
+}
+
+int tt_tuner_train_f32(float* prm, float* m, float* v, const float* steps, const int64_t* rowoff,
+                       const float* ctx, const float* y, const int32_t* order, int64_t n_order,
+                       int32_t B, int32_t loss_kind, int32_t mode, double lr, double b1,
+                       double b2, double eps, const double* corr, const uint8_t* trainable,
+                       int32_t L, int32_t H, int32_t heads, int32_t U, int32_t d0, int32_t C,
+                       int32_t Tmax, float* step_loss, float* grad_out, int32_t* status, void* ws,
+                       size_t ws_bytes, tt_stream_t st) {
+  return train_entry<float>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind, mode,
+                            lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C, Tmax,
+                            step_loss, grad_out, status, ws, ws_bytes, st);
+}
+
+int tt_tuner_train_f64(double* prm, double* m, double* v, const double* steps,
+                       const int64_t* rowoff, const double* ctx, const double* y,
+                       const int32_t* order, int64_t n_order, int32_t B, int32_t loss_kind,
+                       int32_t mode, double lr, double b1, double b2, double eps,
+                       const double* corr, const uint8_t* trainable, int32_t L, int32_t H,
+                       int32_t heads, int32_t U, int32_t d0, int32_t C, int32_t Tmax,
+                       double* step_loss, double* grad_out, int32_t* status, void* ws,
+                       size_t ws_bytes, tt_stream_t st) {
+  return train_entry<double>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind, mode,
+                             lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C, Tmax,
+                             step_loss, grad_out, status, ws, ws_bytes, st);
+}
+
+}  // extern "C"

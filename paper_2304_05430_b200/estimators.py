@@ -1,0 +1,588 @@
+"""Drop-in B200 estimators with the reference's names, constructor
+signatures, attributes and error behaviour.
+
+RecurrentAttentionTuner  <- estimators/tuner.py:154-483
+CostMLP                  <- estimators/mlp.py:38-163
+ranking_grad             <- estimators/mlp.py:25-35
+
+Host state mirrors the reference exactly: ``params_`` is a dict of float64
+arrays in the reference's order and names (a float64 master copy), Adam
+state is fresh per fit/continue_fit, ``train_curve_`` holds per-epoch tuples.
+All arithmetic runs in libtt_b200 kernels: one fused cooperative launch per
+epoch (forward, loss, backward, fixed-order gradient reduction and Adam for
+every minibatch), then the scoring kernel and the PCA counter for the curve.
+Initialisation reproduces the reference's Glorot draws from
+default_rng(seed) bit for bit; permutations come from the same
+default_rng(seed + offset).permutation calls.
+"""
+
+from __future__ import annotations
+
+import sys
+import threading
+
+import numpy as np
+from sklearn.base import BaseEstimator, RegressorMixin
+
+from . import _device, _lib, config
+from .errors import DataValidationError, NumericFailure
+from .layout import DevicePrograms
+from .metrics import group_offsets, pca_counts, pca_from_counts
+from .metrics import ranking_grad as _ranking_grad_gpu
+
+HEAD_HIDDEN = 64
+HIDDEN_WIDTH = 64
+SUPPORTED_HIDDEN = (4, 8, 16, 32)
+_BETA1, _BETA2, _EPS = 0.9, 0.999, 1e-8
+
+
+def _glorot(rng: np.random.Generator, fan_in: int, fan_out: int) -> np.ndarray:
+    bound = np.sqrt(6.0 / (fan_in + fan_out))
+    return rng.uniform(-bound, bound, size=(fan_in, fan_out))
+
+
+def ranking_grad(y, y_hat):
+    """Pairwise logistic loss and gradient (mlp.py:25-35) via the K7 kernel."""
+    return _ranking_grad_gpu(y, y_hat)
+
+
+def _seq_widths() -> tuple[int, int]:
+    """STEP_WIDTH / CONTEXT_LENGTH as the reference tuner module sees them
+    (honours patched module globals), else the defaults."""
+    mod = sys.modules.get("tensortune.estimators.tuner")
+    if mod is not None:
+        return int(mod.STEP_WIDTH), int(mod.CONTEXT_LENGTH)
+    return 6, 35
+
+
+def _bias_corrections(t0: int, n: int) -> np.ndarray:
+    """(1 - b1^t, 1 - b2^t) for t = t0+1 .. t0+n, as optim.py:35-36 computes them."""
+    out = np.empty(2 * n, dtype=np.float64)
+    for k in range(n):
+        t = t0 + k + 1
+        out[2 * k] = 1.0 - _BETA1**t
+        out[2 * k + 1] = 1.0 - _BETA2**t
+    return out
+
+
+class _DeviceParams:
+    """float64 host master dict <-> flat device vector in the kernel layout."""
+
+    def __init__(self):
+        self._lock = threading.Lock()
+        self._flat = None
+        self._key = None
+
+    def upload(self, host: dict, names: list, precision: str, force: bool):
+        with self._lock:
+            key = (precision, tuple(names))
+            if force or self._flat is None or self._key != key:
+                flat = np.concatenate([np.asarray(host[k], dtype=np.float64).ravel() for k in names])
+                self._flat = _device.to_dev(flat, _device.real_dtype(precision))
+                self._key = key
+            return self._flat
+
+    def invalidate(self):
+        with self._lock:
+            self._flat = None
+
+
+def _unflatten_into(host: dict, names: list, flat: np.ndarray) -> None:
+    o = 0
+    for k in names:
+        a = host[k]
+        a[...] = flat[o : o + a.size].reshape(a.shape)
+        o += a.size
+
+
+class _GpuParamsMixin:
+    """params_ as a property over the float64 host master.
+
+    Handing the dict out (params_, get_weights) marks it exposed: callers may
+    mutate the arrays in place (the reference's gradient checks do), so every
+    later device call re-uploads it.  Training downloads results into the
+    same arrays in place, like the reference's in-place Adam.
+    """
+
+    precision = None  # None -> config.PRECISION
+
+    def _prec(self) -> str:
+        return self.precision or config.PRECISION
+
+    @property
+    def params_(self):
+        host = self.__dict__.get("_host")
+        if host is None:
+            raise AttributeError("params_")
+        self.__dict__["_exposed"] = True
+        return host
+
+    @params_.setter
+    def params_(self, value):
+        self.__dict__["_host"] = value
+        self.__dict__["_exposed"] = True
+        self._devp().invalidate()
+
+    def _devp(self) -> _DeviceParams:
+        d = self.__dict__.get("_dev")
+        if d is None:
+            d = _DeviceParams()
+            self.__dict__["_dev"] = d
+        return d
+
+    def _fitted(self) -> bool:
+        return self.__dict__.get("_host") is not None
+
+    def _set_host(self, host: dict) -> None:
+        self.__dict__["_host"] = host
+        self.__dict__["_exposed"] = False
+        self._devp().invalidate()
+
+    def _device_flat(self, names: list):
+        return self._devp().upload(self.__dict__["_host"], names, self._prec(),
+                                   force=bool(self.__dict__.get("_exposed", False)))
+
+    def __getstate__(self):
+        state = dict(self.__dict__)
+        state.pop("_dev", None)
+        return state
+
+    def __setstate__(self, state):
+        self.__dict__.update(state)
+
+
+# =============================================================== tuner ==
+
+
+class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
+    """Sequence cost model: biLSTM stack, iterative attention, dense head."""
+
+    def __init__(
+        self,
+        batch_size: int = 16,
+        epochs: int = 200,
+        learning_rate: float = 1e-3,
+        recurrent_layers: int = 3,
+        hidden_size: int = 32,
+        attention_heads: int = 2,
+        attention_unroll_steps: int = 2,
+        loss: str = "rmse",
+        seed: int = 0,
+    ) -> None:
+        self.batch_size = batch_size
+        self.epochs = epochs
+        self.learning_rate = learning_rate
+        self.recurrent_layers = recurrent_layers
+        self.hidden_size = hidden_size
+        self.attention_heads = attention_heads
+        self.attention_unroll_steps = attention_unroll_steps
+        self.loss = loss
+        self.seed = seed
+
+    # -- parameters (tuner.py:181-223) ---------------------------------------
+
+    def _init_params(self) -> None:
+        if self.recurrent_layers < 1 or self.hidden_size < 1:
+            raise DataValidationError("network size parameters must be positive")
+        if self.attention_heads < 1 or self.attention_unroll_steps < 1:
+            raise DataValidationError("attention parameters must be positive")
+        if (2 * self.hidden_size) % self.attention_heads != 0:
+            raise DataValidationError("attention_heads must divide twice the hidden size")
+        if self.hidden_size not in SUPPORTED_HIDDEN:
+            raise DataValidationError(
+                f"hidden_size {self.hidden_size} is not supported by the B200 kernels "
+                f"(supported: {SUPPORTED_HIDDEN})")
+        d0, C = _seq_widths()
+        rng = np.random.default_rng(self.seed)
+        H = self.hidden_size
+        D = 2 * H
+        params: dict[str, np.ndarray] = {}
+        for layer in range(self.recurrent_layers):
+            d_in = d0 if layer == 0 else D
+            for direction in ("fw", "bw"):
+                prefix = f"lstm{layer}_{direction}"
+                params[f"{prefix}_Wx"] = _glorot(rng, d_in, 4 * H)
+                params[f"{prefix}_Wh"] = _glorot(rng, H, 4 * H)
+                bias = np.zeros(4 * H)
+                bias[H : 2 * H] = 1.0
+                params[f"{prefix}_b"] = bias
+        for name in ("Wq", "Wk", "Wv", "Wo"):
+            params[f"attn_{name}"] = _glorot(rng, D, D)
+        params["attn_bq"] = np.zeros(D)
+        params["attn_bo"] = np.zeros(D)
+        params["head_W1"] = _glorot(rng, D + C, HEAD_HIDDEN)
+        params["head_b1"] = np.zeros(HEAD_HIDDEN)
+        params["head_W2"] = _glorot(rng, HEAD_HIDDEN, 1)
+        params["head_b2"] = np.zeros(1)
+        self._set_host(params)
+
+    def param_groups(self) -> dict[str, list[str]]:
+        groups: dict[str, list[str]] = {"recurrent": [], "attention": [], "head": []}
+        for name in self.__dict__["_host"]:
+            if name.startswith("lstm"):
+                groups["recurrent"].append(name)
+            elif name.startswith("attn"):
+                groups["attention"].append(name)
+            else:
+                groups["head"].append(name)
+        return groups
+
+    def _canonical_names(self) -> list[str]:
+        names = []
+        for layer in range(self.recurrent_layers):
+            for direction in ("fw", "bw"):
+                for part in ("Wx", "Wh", "b"):
+                    names.append(f"lstm{layer}_{direction}_{part}")
+        names += [f"attn_{n}" for n in ("Wq", "Wk", "Wv", "Wo", "bq", "bo")]
+        names += ["head_W1", "head_b1", "head_W2", "head_b2"]
+        return names
+
+    def _dims(self) -> dict:
+        host = self.__dict__["_host"]
+        names = self._canonical_names()
+        missing = [n for n in names if n not in host]
+        if missing:
+            raise DataValidationError(f"weights do not match the architecture: missing {missing[:3]}")
+        H = int(host["lstm0_fw_Wh"].shape[0])
+        if H != self.hidden_size or H not in SUPPORTED_HIDDEN:
+            raise DataValidationError(f"weights have hidden size {H}, estimator {self.hidden_size}")
+        if (2 * H) % self.attention_heads != 0:
+            raise DataValidationError("attention_heads must divide twice the hidden size")
+        d0 = int(host["lstm0_fw_Wx"].shape[0])
+        C = int(host["head_W1"].shape[0]) - 2 * H
+        return dict(L=self.recurrent_layers, H=H, heads=self.attention_heads,
+                    U=self.attention_unroll_steps, d0=d0, C=C, names=names)
+
+    # -- device calls --------------------------------------------------------
+
+    def _dev_params(self, dims):
+        return self._device_flat(dims["names"])
+
+    def _predict_programs(self, prog: DevicePrograms, dims, flat=None):
+        t = _device.torch()
+        prec = self._prec()
+        fn = "tt_tuner_predict_f64" if prec == "fp64" else "tt_tuner_predict_f32"
+        flat = self._dev_params(dims) if flat is None else flat
+        out = _device.empty(prog.n, _device.real_dtype(prec))
+        lib = _lib.load()
+        nbytes = lib.tt_tuner_predict_workspace_bytes(int(prec == "fp64"), dims["L"], dims["H"],
+                                                      prog.max_steps)
+        ws = _device.workspace(nbytes, "tuner_predict")
+        _lib.call(fn, flat.data_ptr(), prog.steps.data_ptr(), prog.offsets.data_ptr(),
+                  prog.ctx.data_ptr(), prog.n, dims["L"], dims["H"], dims["heads"], dims["U"],
+                  dims["d0"], dims["C"], prog.max_steps, out.data_ptr(), ws.data_ptr(), nbytes,
+                  _device.stream_ptr())
+        del t
+        return out
+
+    def _launch_train(self, dims, flat, m, v, prog, y_dev, order, B, mode, lr, corr, mask):
+        t = _device.torch()
+        prec = self._prec()
+        dt = _device.real_dtype(prec)
+        lib = _lib.load()
+        nbytes = lib.tt_tuner_train_workspace_bytes(int(prec == "fp64"), dims["L"], dims["H"],
+                                                    dims["d0"], dims["C"], prog.max_steps, B)
+        ws = _device.workspace(nbytes, "tuner_train")
+        n_steps = (order.numel() + B - 1) // B
+        step_loss = _device.empty(max(n_steps, 1), dt)
+        status = _device.to_dev(np.array([-1], dtype=np.int32))
+        grad = _device.empty(flat.numel(), dt) if mode == _lib.TT_MODE_GRAD else None
+        fn = "tt_tuner_train_f64" if prec == "fp64" else "tt_tuner_train_f32"
+        loss_kind = _lib.TT_LOSS_RANK if self.loss == "ranking" else _lib.TT_LOSS_MSE
+        _lib.call(fn, flat.data_ptr(), _device.ptr(m), _device.ptr(v), prog.steps.data_ptr(),
+                  prog.offsets.data_ptr(), prog.ctx.data_ptr(), y_dev.data_ptr(), order.data_ptr(),
+                  order.numel(), B, loss_kind, mode, lr, _BETA1, _BETA2, _EPS,
+                  _device.ptr(corr), _device.ptr(mask), dims["L"], dims["H"], dims["heads"],
+                  dims["U"], dims["d0"], dims["C"], prog.max_steps, step_loss.data_ptr(),
+                  _device.ptr(grad), status.data_ptr(), ws.data_ptr(), nbytes,
+                  _device.stream_ptr())
+        del t
+        return step_loss, status, grad
+
+    # -- public API (tuner.py:364-483) ---------------------------------------
+
+    def loss_and_gradients(self, sequences, y):
+        dims = self._dims()
+        prec = self._prec()
+        dt = _device.real_dtype(prec)
+        prog = DevicePrograms.from_sequences(sequences, prec, dims["d0"], dims["C"])
+        y = np.asarray(y, dtype=np.float64)
+        n = prog.n
+        if y.shape != (n,):
+            raise DataValidationError("sequences and y must align")
+        if n > config.MAX_BATCH:
+            raise DataValidationError(f"loss_and_gradients supports up to {config.MAX_BATCH} sequences")
+        flat = self._dev_params(dims)
+        order = _device.to_dev(np.arange(n, dtype=np.int32))
+        step_loss, _, grad = self._launch_train(dims, flat, None, None, prog, _device.to_dev(y, dt),
+                                                order, n, _lib.TT_MODE_GRAD, 0.0, None, None)
+        g = grad.cpu().double().numpy()
+        out = {}
+        o = 0
+        host = self.__dict__["_host"]
+        sizes = {k: host[k].size for k in dims["names"]}
+        flat_parts = {}
+        for k in dims["names"]:
+            flat_parts[k] = g[o : o + sizes[k]].reshape(host[k].shape)
+            o += sizes[k]
+        for k in host:  # reference dict order
+            out[k] = flat_parts[k]
+        return float(step_loss[0].item()), out
+
+    def fit(self, sequences, y, eval_set=None, eval_groups=None):
+        if self.loss not in ("rmse", "ranking"):
+            raise DataValidationError(f"unknown loss {self.loss!r}")
+        if self.batch_size < 1 or self.epochs < 0:
+            raise DataValidationError("batch_size must be >= 1 and epochs >= 0")
+        y = np.asarray(y, dtype=np.float64)
+        if len(sequences) != y.shape[0] or not sequences:
+            raise DataValidationError("sequences and y must align and be non-empty")
+        self._init_params()
+        return self._train(sequences, y, self.epochs, self.learning_rate, None, eval_set,
+                           eval_groups)
+
+    def continue_fit(self, sequences, y, epochs: int, learning_rate: float, trainable=None,
+                     eval_set=None, eval_groups=None, seed_offset: int = 9001):
+        if not self._fitted():
+            raise DataValidationError("continue_fit called before fit")
+        y = np.asarray(y, dtype=np.float64)
+        return self._train(sequences, y, epochs, learning_rate, trainable, eval_set, eval_groups,
+                           seed_offset=seed_offset)
+
+    def _train(self, sequences, y, epochs, learning_rate, trainable, eval_set, eval_groups,
+               seed_offset: int = 1):
+        rng = np.random.default_rng(self.seed + seed_offset)
+        n = len(sequences)
+        self.train_curve_ = []
+        if epochs <= 0:
+            return self
+        dims = self._dims()
+        prec = self._prec()
+        dt = _device.real_dtype(prec)
+        prog = DevicePrograms.from_sequences(sequences, prec, dims["d0"], dims["C"])
+        y_dev = _device.to_dev(y, dt)
+        flat = self._dev_params(dims).clone()
+        NP = flat.numel()
+        m = _device.zeros(NP, dt)
+        v = _device.zeros(NP, dt)
+        mask = None
+        if trainable is not None:
+            host = self.__dict__["_host"]
+            mh = np.concatenate([np.full(host[k].size, k in trainable, dtype=np.uint8)
+                                 for k in dims["names"]])
+            mask = _device.to_dev(mh)
+        B = min(int(self.batch_size), n)
+        if B > config.MAX_BATCH:
+            raise DataValidationError(f"batch_size above {config.MAX_BATCH} is not supported")
+        ev = None
+        if eval_set is not None:
+            eprog = DevicePrograms.from_sequences(eval_set[0], prec, dims["d0"], dims["C"])
+            ey = np.asarray(eval_set[1], dtype=np.float64)
+            gperm = goff = None
+            if eval_groups is not None:
+                gperm, goff = group_offsets(eval_groups)
+            ev = (eprog, ey, gperm, goff)
+        t_step = 0
+        n_steps = (n + B - 1) // B
+        for epoch in range(epochs):
+            perm = rng.permutation(n).astype(np.int32)
+            corr = _device.to_dev(_bias_corrections(t_step, n_steps))
+            _, status, _ = self._launch_train(dims, flat, m, v, prog, y_dev, _device.to_dev(perm), B,
+                                              _lib.TT_MODE_TRAIN, float(learning_rate), corr, mask)
+            if int(status.item()) >= 0:
+                raise NumericFailure(f"loss became non-finite at epoch {epoch}")
+            t_step += n_steps
+            pred = self._predict_programs(prog, dims, flat).cpu().double().numpy()
+            train_rmse = float(np.sqrt(np.mean((pred - y) ** 2)))
+            val_rmse = val_pca = None
+            if ev is not None:
+                eprog, ey, gperm, goff = ev
+                vp = self._predict_programs(eprog, dims, flat).cpu().double().numpy()
+                val_rmse = float(np.sqrt(np.mean((vp - ey) ** 2)))
+                if gperm is not None:
+                    sizes = np.diff(goff)
+                    if np.any(sizes >= 2):
+                        vals = pca_from_counts(pca_counts(ey[gperm], vp[gperm], goff), goff)
+                        val_pca = float(np.mean([float(x) for x, s in zip(vals, sizes) if s >= 2]))
+            self.train_curve_.append((train_rmse, val_rmse, val_pca))
+        host = self.__dict__["_host"]
+        _unflatten_into(host, dims["names"], flat.cpu().double().numpy())
+        self._devp().invalidate()
+        return self
+
+    def predict(self, sequences, chunk: int = 256) -> np.ndarray:
+        if not self._fitted():
+            raise DataValidationError("predict called before fit")
+        if len(sequences) == 0:
+            return np.zeros(0)
+        dims = self._dims()
+        prog = DevicePrograms.from_sequences(sequences, self._prec(), dims["d0"], dims["C"])
+        return self._predict_programs(prog, dims).cpu().double().numpy()
+
+    def predict_device(self, prog: DevicePrograms):
+        """Scores of already device-resident programs (no host copies)."""
+        return self._predict_programs(prog, self._dims())
+
+    def get_weights(self) -> dict[str, np.ndarray]:
+        return dict(self.params_)
+
+    def set_weights(self, weights: dict[str, np.ndarray]) -> None:
+        self.params_ = {k: np.asarray(v, dtype=np.float64) for k, v in weights.items()}
+        self.train_curve_ = []
+
+
+# ================================================================= MLP ==
+
+
+def _check_matrix(X, name: str = "X") -> np.ndarray:
+    """estimators/gbdt.py:42-48."""
+    X = np.asarray(X, dtype=np.float64)
+    if X.ndim != 2:
+        raise DataValidationError(f"{name} must be 2-d, got shape {X.shape}")
+    if not np.isfinite(X).all():
+        raise DataValidationError(f"{name} contains non-finite values")
+    return X
+
+
+class CostMLP(_GpuParamsMixin, BaseEstimator, RegressorMixin):
+    """Tabular cost model F -> 64 -> 64 -> 1 trained with minibatch Adam."""
+
+    NAMES = ("W1", "b1", "W2", "b2", "W3", "b3")
+
+    def __init__(self, batch_size: int = 16, epochs: int = 200, learning_rate: float = 1e-3,
+                 loss: str = "rmse", seed: int = 0) -> None:
+        self.batch_size = batch_size
+        self.epochs = epochs
+        self.learning_rate = learning_rate
+        self.loss = loss
+        self.seed = seed
+
+    def _init_params(self, n_features: int) -> None:
+        rng = np.random.default_rng(self.seed)
+        h = HIDDEN_WIDTH
+        self._set_host({
+            "W1": _glorot(rng, n_features, h),
+            "b1": np.zeros(h),
+            "W2": _glorot(rng, h, h),
+            "b2": np.zeros(h),
+            "W3": _glorot(rng, h, 1),
+            "b3": np.zeros(1),
+        })
+        self.n_features_in_ = n_features
+
+    def _predict_dev(self, Xd, n, F, flat=None):
+        prec = self._prec()
+        flat = self._device_flat(list(self.NAMES)) if flat is None else flat
+        out = _device.empty(n, _device.real_dtype(prec))
+        fn = "tt_mlp_predict_f64" if prec == "fp64" else "tt_mlp_predict_f32"
+        _lib.call(fn, flat.data_ptr(), Xd.data_ptr(), n, F, out.data_ptr(), _device.stream_ptr())
+        return out
+
+    def _launch_train(self, flat, m, v, Xd, yd, F, order, B, mode, lr, corr):
+        prec = self._prec()
+        dt = _device.real_dtype(prec)
+        lib = _lib.load()
+        nbytes = lib.tt_mlp_train_workspace_bytes(int(prec == "fp64"), F, B)
+        ws = _device.workspace(nbytes, "mlp_train")
+        n_steps = (order.numel() + B - 1) // B
+        step_loss = _device.empty(max(n_steps, 1), dt)
+        status = _device.to_dev(np.array([-1], dtype=np.int32))
+        grad = _device.empty(flat.numel(), dt) if mode == _lib.TT_MODE_GRAD else None
+        fn = "tt_mlp_train_f64" if prec == "fp64" else "tt_mlp_train_f32"
+        loss_kind = _lib.TT_LOSS_RANK if self.loss == "ranking" else _lib.TT_LOSS_MSE
+        _lib.call(fn, flat.data_ptr(), _device.ptr(m), _device.ptr(v), Xd.data_ptr(), yd.data_ptr(),
+                  F, order.data_ptr(), order.numel(), B, loss_kind, mode, lr, _BETA1, _BETA2, _EPS,
+                  _device.ptr(corr), step_loss.data_ptr(), _device.ptr(grad), status.data_ptr(),
+                  ws.data_ptr(), nbytes, _device.stream_ptr())
+        return step_loss, status, grad
+
+    def loss_and_gradients(self, X, y):
+        X = np.asarray(X, dtype=np.float64)
+        y = np.asarray(y, dtype=np.float64)
+        n, F = X.shape
+        if n > config.MAX_BATCH:
+            raise DataValidationError(f"loss_and_gradients supports up to {config.MAX_BATCH} rows")
+        dt = _device.real_dtype(self._prec())
+        flat = self._device_flat(list(self.NAMES))
+        order = _device.to_dev(np.arange(n, dtype=np.int32))
+        step_loss, _, grad = self._launch_train(flat, None, None, _device.to_dev(X.ravel(), dt),
+                                                _device.to_dev(y, dt), F, order, n,
+                                                _lib.TT_MODE_GRAD, 0.0, None)
+        g = grad.cpu().double().numpy()
+        host = self.__dict__["_host"]
+        out, o = {}, 0
+        for k in self.NAMES:
+            out[k] = g[o : o + host[k].size].reshape(host[k].shape)
+            o += host[k].size
+        return float(step_loss[0].item()), {k: out[k] for k in host}
+
+    def fit(self, X, y, eval_set=None):
+        if self.loss not in ("rmse", "ranking"):
+            raise DataValidationError(f"unknown loss {self.loss!r}")
+        if self.batch_size < 1 or self.epochs < 0:
+            raise DataValidationError("batch_size must be >= 1 and epochs >= 0")
+        X = _check_matrix(X)
+        y = np.asarray(y, dtype=np.float64)
+        if y.shape != (X.shape[0],):
+            raise DataValidationError("y must be 1-d and match X rows")
+        self._init_params(X.shape[1])
+        rng = np.random.default_rng(self.seed + 1)
+        X_val = y_val = None
+        if eval_set is not None:
+            X_val = _check_matrix(eval_set[0], "X_val")
+            y_val = np.asarray(eval_set[1], dtype=np.float64)
+        self.train_curve_ = []
+        n, F = X.shape
+        if self.epochs == 0:
+            return self
+        prec = self._prec()
+        dt = _device.real_dtype(prec)
+        Xd = _device.to_dev(X.ravel(), dt)
+        yd = _device.to_dev(y, dt)
+        Xvd = _device.to_dev(X_val.ravel(), dt) if X_val is not None else None
+        flat = self._device_flat(list(self.NAMES)).clone()
+        m = _device.zeros(flat.numel(), dt)
+        v = _device.zeros(flat.numel(), dt)
+        B = min(int(self.batch_size), n)
+        if B > config.MAX_BATCH:
+            raise DataValidationError(f"batch_size above {config.MAX_BATCH} is not supported")
+        n_steps = (n + B - 1) // B
+        t_step = 0
+        for epoch in range(self.epochs):
+            perm = rng.permutation(n).astype(np.int32)
+            corr = _device.to_dev(_bias_corrections(t_step, n_steps))
+            _, status, _ = self._launch_train(flat, m, v, Xd, yd, F, _device.to_dev(perm), B,
+                                              _lib.TT_MODE_TRAIN, float(self.learning_rate), corr)
+            if int(status.item()) >= 0:
+                raise NumericFailure(f"loss became non-finite at epoch {epoch}")
+            t_step += n_steps
+            pred = self._predict_dev(Xd, n, F, flat).cpu().double().numpy()
+            train_rmse = float(np.sqrt(np.mean((pred - y) ** 2)))
+            val_rmse = None
+            if Xvd is not None:
+                pv = self._predict_dev(Xvd, X_val.shape[0], F, flat).cpu().double().numpy()
+                val_rmse = float(np.sqrt(np.mean((pv - y_val) ** 2)))
+            self.train_curve_.append((train_rmse, val_rmse))
+        _unflatten_into(self.__dict__["_host"], list(self.NAMES), flat.cpu().double().numpy())
+        self._devp().invalidate()
+        return self
+
+    def predict(self, X) -> np.ndarray:
+        if not self._fitted():
+            raise DataValidationError("predict called before fit")
+        X = _check_matrix(X)
+        if X.shape[1] != self.n_features_in_:
+            raise DataValidationError(f"expected {self.n_features_in_} features, got {X.shape[1]}")
+        if X.shape[0] == 0:
+            return np.zeros(0)
+        dt = _device.real_dtype(self._prec())
+        return self._predict_dev(_device.to_dev(X.ravel(), dt), X.shape[0],
+                                 X.shape[1]).cpu().double().numpy()
+
+    def get_weights(self) -> dict[str, np.ndarray]:
+        return dict(self.params_)
+
+    def set_weights(self, weights: dict[str, np.ndarray]) -> None:
+        self.params_ = {k: np.asarray(v, dtype=np.float64) for k, v in weights.items()}
+        self.n_features_in_ = self.__dict__["_host"]["W1"].shape[0]
+        self.train_curve_ = []

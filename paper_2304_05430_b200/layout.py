@@ -1,0 +1,82 @@
+"""K9: program layout (replaces the padded batch of tuner.py:36-52 _pack).
+
+The reference pads every chunk of 256 programs to (B, Tmax, 6) plus a mask;
+padding is inert (masked steps hold state, -1e30 logits, masked mean), so the
+device layout is CSR instead: all step rows of all programs back to back,
+int64 row offsets, one context row per program.  A program's forward
+direction runs t = 0..T-1 and its backward direction t = T-1..0 from zero
+state, which equals the reference's reversed padded sequence
+(tuner.py:242-243) exactly.
+
+Inputs are duck-typed StepSequence objects (features.py:70-92): ``.steps``
+(T, step_width) and ``.context`` (ctx_len,).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _device
+from .errors import DataValidationError
+
+
+@dataclass
+class HostPrograms:
+    steps: np.ndarray    # (rows, d0) float64
+    offsets: np.ndarray  # (n + 1,) int64
+    ctx: np.ndarray      # (n, C) float64
+
+    @property
+    def n(self) -> int:
+        return self.offsets.shape[0] - 1
+
+    @property
+    def max_steps(self) -> int:
+        return int(np.max(np.diff(self.offsets))) if self.n else 0
+
+
+def pack_sequences(seqs, step_width: int | None = None, ctx_len: int | None = None) -> HostPrograms:
+    if len(seqs) == 0:
+        raise DataValidationError("empty sequence batch")
+    steps = [np.asarray(s.steps, dtype=np.float64) for s in seqs]
+    ctxs = [np.asarray(s.context, dtype=np.float64) for s in seqs]
+    d0 = steps[0].shape[1] if steps[0].ndim == 2 else -1
+    C = ctxs[0].shape[0] if ctxs[0].ndim == 1 else -1
+    if step_width is not None and d0 != step_width:
+        raise DataValidationError(f"steps must be (n, {step_width}), got {steps[0].shape}")
+    if ctx_len is not None and C != ctx_len:
+        raise DataValidationError(f"context must have {ctx_len} slots, got {ctxs[0].shape}")
+    lens = np.empty(len(seqs), dtype=np.int64)
+    for i, (st, cx) in enumerate(zip(steps, ctxs)):
+        if st.ndim != 2 or st.shape[1] != d0 or st.shape[0] < 1:
+            raise DataValidationError(f"steps must be (n >= 1, {d0}), got {st.shape}")
+        if cx.shape != (C,):
+            raise DataValidationError(f"context must have {C} slots, got {cx.shape}")
+        lens[i] = st.shape[0]
+    off = np.zeros(len(seqs) + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    return HostPrograms(np.concatenate(steps, axis=0), off, np.stack(ctxs))
+
+
+class DevicePrograms:
+    """Device-resident CSR programs in the compute dtype."""
+
+    def __init__(self, host: HostPrograms, precision: str = "fp32"):
+        dt = _device.real_dtype(precision)
+        t = _device.torch()
+        self.precision = precision
+        self.n = host.n
+        self.d0 = host.steps.shape[1]
+        self.C = host.ctx.shape[1]
+        self.max_steps = host.max_steps
+        self.steps = _device.to_dev(host.steps.reshape(-1), dt)
+        self.offsets = _device.to_dev(host.offsets.astype(np.int64))
+        self.ctx = _device.to_dev(host.ctx.reshape(-1), dt)
+        self.host_offsets = host.offsets
+        self._t = t
+
+    @classmethod
+    def from_sequences(cls, seqs, precision="fp32", step_width=None, ctx_len=None):
+        return cls(pack_sequences(seqs, step_width, ctx_len), precision)
