@@ -1,0 +1,386 @@
+"""Benchmark of the B200 hot path on BASELINE.json configs[1]:
+
+  attention-inspired cost model (RecurrentAttentionTuner defaults: 3 biLSTM
+  layers, hidden 32, 2 heads, 2 attention passes) trained with the pairwise
+  rank loss on 64 tasks x 4096 programs (262,144 samples), minibatch 16
+  (paper Table 4), Adam lr 1e-3, float32, synthetic data.
+
+A "step" is one training epoch: 16,384 minibatches of 16, each one forward,
+rank loss, backward, fixed-order gradient reduction and fused Adam update --
+one cooperative kernel launch per epoch.  ``value`` = optimizer-consumed
+samples/s over K timed epochs with the dataset resident in HBM (device
+timed, CUDA events on the launching stream, L2 flushed between epochs).
+``e2e`` = the same metric through the public API
+``RecurrentAttentionTuner.continue_fit(seqs, y, epochs=1)`` from host step
+sequences: packing, pinned host->device copies, the epoch, the per-epoch
+train-set scoring for the curve and the device->host reads.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+--impl reference times the reference's algorithm on the host CPU (the
+float64 numpy oracle port in oracle/, kind "port"; the reference is pure
+Python and has no separate compiled form) on a bounded sample of the same
+workload.  Under torchrun only rank 0 runs it.
+
+Data: per program T ~ the step-count histogram measured on gen_dataset
+(SURVEY.md §6.2, T in 4..10, mean 7.1); step rows = one-hot kind (4),
+log2 knob in [0, 5], axis in {-1, 0, 1, 2}; context ~ N(0, 1) (35); labels
+per task min(c)/c with c ~ LogNormal(-9, 0.5).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_TASKS, PER_TASK, BATCH = 64, 4096, 16
+T_HIST = {4: 35, 5: 196, 6: 457, 7: 516, 8: 469, 9: 291, 10: 46}
+CPU_SAMPLE_SECONDS = 12.0
+
+
+# ----------------------------------------------------------------- data --
+
+
+def synth(n_tasks=N_TASKS, per_task=PER_TASK, seed=0):
+    """Host CSR programs + labels (float64)."""
+    rng = np.random.default_rng(seed)
+    n = n_tasks * per_task
+    ts = np.array(list(T_HIST))
+    ps = np.array(list(T_HIST.values()), dtype=np.float64)
+    lens = rng.choice(ts, size=n, p=ps / ps.sum())
+    rows = int(lens.sum())
+    steps = np.zeros((rows, 6))
+    kind = rng.integers(0, 4, size=rows)
+    steps[np.arange(rows), kind] = 1.0
+    steps[:, 4] = rng.integers(0, 6, size=rows)
+    steps[:, 5] = rng.integers(-1, 3, size=rows)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    ctx = rng.normal(size=(n, 35))
+    cost = rng.lognormal(-9.0, 0.5, size=(n_tasks, per_task))
+    y = (cost.min(axis=1, keepdims=True) / cost).ravel()
+    return steps, off, ctx, y, lens
+
+
+class Seq:
+    __slots__ = ("steps", "context")
+
+    def __init__(self, steps, context):
+        self.steps = steps
+        self.context = context
+
+
+def as_seqs(steps, off, ctx):
+    return [Seq(steps[off[i]:off[i + 1]], ctx[i]) for i in range(len(off) - 1)]
+
+
+def train_flops(lens):
+    """Algorithmic FLOPs of one training pass: 3 x forward, forward =
+    134,656*T + 45,568 per program (default dims)."""
+    return float(np.sum(3.0 * (134656.0 * lens + 45568.0)))
+
+
+# --------------------------------------------------------------- clocks --
+
+
+class Clocks:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self, gpu=0):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except Exception:  # noqa: BLE001
+            return None
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9 and r[0].strip() == str(gpu)]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        mx = float(rows[0][2])
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------ reference --
+
+
+def cpu_baseline(steps, off, ctx, y, seconds=CPU_SAMPLE_SECONDS):
+    """The reference algorithm (float64 numpy port, oracle/tuner.py) training
+    the same model with the same rank loss and batch size on the first
+    minibatches of a permutation, single BLAS thread, for ~`seconds`."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except Exception:  # noqa: BLE001
+        threadpool_limits = None
+    from oracle import tuner as otuner
+    from oracle.adam import AdamOracle
+
+    seqs = as_seqs(steps, off, ctx)
+    p = otuner.init_params(0)
+    opt = AdamOracle(p, 1e-3)
+    perm = np.random.default_rng(1).permutation(len(seqs))
+    ctxm = threadpool_limits(1) if threadpool_limits else None
+    done = 0
+    t0 = time.perf_counter()
+    k = 0
+    while time.perf_counter() - t0 < seconds:
+        b = perm[k * BATCH:(k + 1) * BATCH]
+        _, g = otuner.loss_and_gradients(p, [seqs[i] for i in b], y[b], "ranking")
+        opt.step(g)
+        done += len(b)
+        k += 1
+    dt = time.perf_counter() - t0
+    if ctxm is not None:
+        ctxm.__exit__(None, None, None)
+    return {"value": done / dt, "unit": "samples/s", "cores": 1, "kind": "port",
+            "sample": f"{k} minibatches x {BATCH} samples ({done}) of the same workload, "
+                      f"float64 numpy oracle port of tuner.py, 1 BLAS thread, {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    steps, off, ctx, y, lens = synth(8, 512, seed=0)  # a bounded sample of the same workload
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(steps, off, ctx, y, seconds=max(2.0, CPU_SAMPLE_SECONDS / 4))
+        if i >= args.warmup:
+            vals.append(r["value"])
+    v = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": "rank-loss train samples/sec", "value": v, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * BATCH / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "tuner rank-loss training, 64 tasks x 4096 programs, batch 16 (bounded sample)",
+                   "global_batch": BATCH, "seq_len": 10, "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "port",
+                         "sample": "per step ~3 s of minibatches of 16 from a 4096-program slice"},
+        "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- B200 --
+
+
+def flush_l2(buf):
+    buf.fill_(1)
+
+
+def run_b200(args, world, rank):
+    import torch
+
+    from paper_2304_05430_b200 import RecurrentAttentionTuner, _device, _lib
+    from paper_2304_05430_b200.estimators import _bias_corrections
+    from paper_2304_05430_b200.layout import DevicePrograms, HostPrograms
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    steps, off, ctx, y, lens = synth(seed=rank)
+    n = len(y)
+    host = HostPrograms(steps, off, ctx)
+    prog = DevicePrograms(host, "fp32")
+    yd = _device.to_dev(y, torch.float32)
+    est = RecurrentAttentionTuner(batch_size=BATCH, loss="ranking", seed=0)
+    est.precision = "fp32"
+    est._init_params()
+    dims = est._dims()
+    flat = est._dev_params(dims).clone()
+    m = torch.zeros_like(flat)
+    v = torch.zeros_like(flat)
+    rng = np.random.default_rng(1)
+    n_steps = (n + BATCH - 1) // BATCH
+    l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def epoch(t0):
+        perm = _device.to_dev(rng.permutation(n).astype(np.int32))
+        corr = _device.to_dev(_bias_corrections(t0, n_steps))
+        return est._launch_train(dims, flat, m, v, prog, yd, perm, BATCH, _lib.TT_MODE_TRAIN, 1e-3,
+                                 corr, None)
+
+    t_adam = 0
+    for _ in range(args.warmup):
+        epoch(t_adam)
+        t_adam += n_steps
+    torch.cuda.synchronize()
+    # pre-stage the timed epochs' inputs so the timed region holds only kernels
+    perms = [_device.to_dev(rng.permutation(n).astype(np.int32)) for _ in range(args.steps)]
+    corrs = [_device.to_dev(_bias_corrections(t_adam + k * n_steps, n_steps)) for k in range(args.steps)]
+    times = []
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out", f"clocks_rank{rank}.csv")
+                    if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else f"/tmp/clocks_{rank}.csv")
+    with clocks:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            flush_l2(l2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, status, _ = est._launch_train(dims, flat, m, v, prog, yd, perms[k], BATCH,
+                                             _lib.TT_MODE_TRAIN, 1e-3, corrs[k], None)
+            e1.record(stream)
+            times.append((e0, e1))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+    ms = [a.elapsed_time(b) for a, b in times]
+    assert int(status.item()) < 0, "non-finite loss during the benchmark"
+    t_mean = float(np.mean(ms)) / 1e3
+    if dist is not None:
+        tt = torch.tensor([t_mean], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_mean = float(tt.item())
+    value = world * n / t_mean
+    flops = train_flops(lens)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:  # noqa: BLE001
+        pass
+    peak = float(peaks.get("bf16_tflops_sustained", 1400.0))
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "train_kernel_traffic.json")))
+        traffic = prof.get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        pass
+    achieved = flops / t_mean / 1e12
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "kernel": "tuner_train_kernel<float,32> (one launch = one epoch)",
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback"}
+
+    # ---- e2e through the public API (host step sequences -> fit epoch)
+    e2e = None
+    if rank == 0 and not args.no_e2e:
+        seqs = as_seqs(steps, off, ctx)
+        est2 = RecurrentAttentionTuner(batch_size=BATCH, loss="ranking", seed=0, epochs=0)
+        est2.precision = "fp32"
+        est2.fit(seqs[:2], y[:2])
+        est2.continue_fit(seqs, y, epochs=1, learning_rate=1e-3)  # warm
+        torch.cuda.synchronize()
+        wall = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            est2.continue_fit(seqs, y, epochs=1, learning_rate=1e-3)
+            torch.cuda.synchronize()
+            wall.append(time.perf_counter() - t0)
+        h2d = steps.size * 4 + off.size * 8 + ctx.size * 4 + y.size * 4 + n * 4 + n_steps * 16
+        d2h = n * 4 + int(flat.numel()) * 4 + 4
+        e2e = {"value": n / float(np.mean(wall)), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "api": "RecurrentAttentionTuner.continue_fit(seqs, y, epochs=1)",
+               "s_per_step": float(np.mean(wall))}
+
+    # ---- secondary: bulk scoring and PCA throughput (configs 3 and 4 shapes)
+    extra = {}
+    if rank == 0 and not args.no_extra:
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        est._set_host(est.__dict__["_host"])
+        for _ in range(2):
+            est._predict_programs(prog, dims, flat)
+        flush_l2(l2)
+        s0.record(stream)
+        est._predict_programs(prog, dims, flat)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        sc_t = s0.elapsed_time(s1) / 1e3
+        extra["scoring_programs_per_s"] = n / sc_t
+        extra["scoring_tflops"] = float(np.sum(134656.0 * lens + 45568.0)) / sc_t / 1e12
+        from paper_2304_05430_b200 import metrics as gm
+
+        pred = est._predict_programs(prog, dims, flat).double()
+        toff = np.arange(0, n + 1, PER_TASK, dtype=np.int64)
+        yt = torch.tensor(y, dtype=torch.float64, device="cuda")
+        gm.pca_counts(yt, pred, toff)
+        torch.cuda.synchronize()
+        p0 = time.perf_counter()
+        c = gm.pca_counts(yt, pred, toff)
+        pt = time.perf_counter() - p0
+        pairs = N_TASKS * PER_TASK * (PER_TASK - 1) / 2
+        extra["pca_pairs_per_s"] = pairs / pt
+        extra["pca_mean"] = float(np.mean(c / (PER_TASK * (PER_TASK - 1) / 2)))
+
+    if rank == 0:
+        cpu = None if args.no_cpu else cpu_baseline(steps, off, ctx, y)
+        line = {
+            "metric": "rank-loss train samples/sec", "value": value, "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_mean * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "attention tuner (3x biLSTM h32, 2 heads x 2 passes) rank-loss "
+                                   "training, 64 tasks x 4096 programs, batch 16, Adam; 1 step = 1 epoch",
+                       "global_batch": BATCH * world, "seq_len": int(lens.max()),
+                       "parallelism": f"dp{world}" if world > 1 else "single",
+                       "l2": "flushed (256 MB write) between timed epochs"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(int(os.environ.get("LOCAL_RANK", 0))),
+            "extra": extra,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus == 1 else 1))
+    rank = int(os.environ.get("RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_b200(args, world, rank)
+
+
+if __name__ == "__main__":
+    main()

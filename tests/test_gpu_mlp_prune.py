@@ -1,0 +1,189 @@
+"""CostMLP kernels (K3/K4 + fused train loop) and the K2 pruning statistics
+vs the pinned oracle / reference goldens.
+
+Tolerances: fp64 build rel 1e-10 (predict, gradients, 3-epoch trajectory);
+fp32 build: predictions |d| <= 1e-5 * (1 + |y|), gradients relative-norm
+<= 1e-4.  Pruning: thresholds, masks and survivor sets bit-exact.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import pytest
+
+from conftest import golden, relative_gradient_error
+from oracle import mlp as omlp
+from oracle import sampling as osamp
+
+pytestmark = pytest.mark.gpu
+
+
+def mlp(precision, **kw):
+    from paper_2304_05430_b200 import CostMLP
+
+    m = CostMLP(**kw)
+    m.precision = precision
+    return m
+
+
+def test_mlp_init_predict_and_gradients_match_golden(cuda_ok):
+    g = golden("mlp.npz")
+    for prec, rtol, gtol in (("fp64", 1e-10, 1e-9), ("fp32", 1e-5, 1e-4)):
+        m = mlp(prec, epochs=0, seed=3).fit(g["X"], g["y"])
+        for k in omlp.NAMES:
+            assert np.array_equal(m.params_[k], g["init_" + k])
+        np.testing.assert_allclose(m.predict(g["X"]), g["pred"], rtol=rtol, atol=rtol)
+        for loss in ("rmse", "ranking"):
+            m.loss = loss
+            l, gr = m.loss_and_gradients(g["X"][:16], g["y"][:16])
+            assert l == pytest.approx(float(g[f"{loss}_loss"]), rel=rtol * 10)
+            assert relative_gradient_error(gr, {k: g[f"{loss}_g_{k}"] for k in gr}) <= gtol
+
+
+@pytest.mark.parametrize("loss", ["rmse", "ranking"])
+def test_mlp_training_trajectory_fp64(cuda_ok, loss):
+    g = golden("mlp.npz")
+    m = mlp("fp64", epochs=3, batch_size=8, learning_rate=3e-3, loss=loss, seed=1)
+    m.fit(g["fit_X"], g["fit_y"], eval_set=(g["fit_Xv"], g["fit_yv"]))
+    for k in omlp.NAMES:
+        np.testing.assert_allclose(m.params_[k], g[f"fit_{loss}_{k}"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(np.array(m.train_curve_), g[f"fit_{loss}_curve"], rtol=1e-9)
+
+
+def test_mlp_tenset_width_scoring_fp32(cuda_ok):
+    rng = np.random.default_rng(7)
+    X = rng.normal(size=(5000, 164))
+    y = rng.uniform(size=5000)
+    m = mlp("fp32", epochs=0, seed=0).fit(X, y)
+    want = omlp.predict(omlp.init_params(164, 0), X)
+    np.testing.assert_allclose(m.predict(X), want, rtol=0, atol=2e-5)
+
+
+def test_mlp_validation(cuda_ok):
+    from paper_2304_05430_b200.errors import DataValidationError, NumericFailure
+
+    with pytest.raises(DataValidationError, match="unknown loss"):
+        mlp("fp32", loss="hinge").fit(np.zeros((4, 2)), np.zeros(4))
+    with pytest.raises(DataValidationError):
+        mlp("fp32", batch_size=0).fit(np.zeros((4, 2)), np.zeros(4))
+    rng = np.random.default_rng(17)
+    with pytest.raises(NumericFailure, match="epoch 0"):
+        mlp("fp32", epochs=3, learning_rate=1e200).fit(rng.normal(size=(20, 3)), rng.normal(size=20))
+    m = mlp("fp32", epochs=0).fit(np.zeros((4, 3)), np.zeros(4))
+    with pytest.raises(DataValidationError, match="expected 3 features"):
+        m.predict(np.zeros((2, 4)))
+
+
+# ------------------------------------------------------------- pruning --
+
+
+def test_prune_stats_match_reference_bit_exact(cuda_ok):
+    from paper_2304_05430_b200 import sampling as gs
+
+    g = golden("sampling.npz")
+    for ci, (q, mr) in enumerate(g["cases"]):
+        thr, keep, surv, tkeep = gs.filter_stats(g["flops"], g["cost"], g["valid"], g["offsets"], q,
+                                                 int(mr))
+        np.testing.assert_array_equal(thr, g[f"thr_{ci}"])
+        np.testing.assert_array_equal(keep, g[f"keep_{ci}"])
+        np.testing.assert_array_equal(tkeep, g[f"tkeep_{ci}"])
+    for qi, q in enumerate(g["tie_q"]):
+        thr, keep, surv, tkeep = gs.filter_stats(g["tie_flops"], g["tie_cost"], g["tie_valid"],
+                                                 g["tie_off"], q, 1)
+        np.testing.assert_array_equal(thr, g[f"tie_thr_{qi}"])
+        othr, okeep, osurv, otk = osamp.filter_stats(g["tie_flops"], g["tie_cost"], g["tie_valid"],
+                                                     g["tie_off"], q, 1)
+        np.testing.assert_array_equal(keep, okeep)
+        np.testing.assert_array_equal(surv, osurv)
+
+
+def test_prune_stats_large_random_vs_oracle(cuda_ok):
+    from paper_2304_05430_b200 import sampling as gs
+
+    rng = np.random.default_rng(3)
+    sizes = rng.integers(0, 5000, size=40)
+    off = np.zeros(41, dtype=np.int64)
+    off[1:] = np.cumsum(sizes)
+    n = int(off[-1])
+    flops = rng.integers(1, 2**40, size=n)
+    flops[::5] = 2**62 + rng.integers(0, 1000, size=flops[::5].shape)
+    cost = np.round(rng.lognormal(-8, 1, size=n), 6)
+    valid = rng.random(n) > 0.03
+    for q in (0.0, 0.1, 0.55, 0.999):
+        got = gs.filter_stats(flops, cost, valid, off, q, 8)
+        want = osamp.filter_stats(flops, cost, valid, off, q, 8)
+        for a, b in zip(got, want):
+            np.testing.assert_array_equal(a, b)
+
+
+# duck-typed stand-ins for the reference Dataset API used by filter_invalid
+@dataclass
+class K:
+    op: str
+    flops: int
+
+
+@dataclass
+class T:
+    task_id: str
+    kernel: K
+
+
+@dataclass
+class Rec:
+    record_id: str
+    task_id: str
+    mean_cost: float | None
+    measured_flops: int
+    error_flag: bool = False
+
+
+@dataclass
+class DS:
+    hardware: list
+    tasks: list
+    records: list
+    records_by_task: dict = field(default_factory=dict)
+    record_by_id: dict = field(default_factory=dict)
+
+    @classmethod
+    def build(cls, hardware, tasks, records, validate=False):
+        ds = cls(list(hardware), list(tasks), list(records))
+        ds.records_by_task = {t.task_id: [] for t in tasks}
+        for r in records:
+            ds.record_by_id[r.record_id] = r
+            if r.task_id in ds.records_by_task:
+                ds.records_by_task[r.task_id].append(r.record_id)
+        return ds
+
+
+@dataclass
+class Cfg:
+    low_perf_quantile: float = 0.1
+    min_records_per_task: int = 8
+
+    def validate(self):
+        pass
+
+
+def test_filter_invalid_dataset_level_matches_golden(cuda_ok):
+    from paper_2304_05430_b200 import sampling as gs
+
+    g = golden("sampling.npz")
+    off = g["offsets"]
+    tasks, recs, order = [], [], []
+    for t in range(off.shape[0] - 1):
+        tasks.append(T(f"t{t}", K("matmul", 1000)))
+        for i in range(off[t], off[t + 1]):
+            ok = bool(g["valid"][i])
+            recs.append(Rec(f"r{i}", f"t{t}", float(g["cost"][i]) if ok else None,
+                            int(g["flops"][i]) if ok else 0, not ok))
+            order.append(f"r{i}")
+    ds = DS.build([], tasks, recs)
+    for ci, (q, mr) in enumerate(g["cases"]):
+        out = gs.filter_invalid(ds, Cfg(q, int(mr)))
+        kept = {r.record_id for r in out.records}
+        assert [rid in kept for rid in order] == list(g[f"keep_{ci}"])
+        assert [t.task_id in {x.task_id for x in out.tasks} for t in tasks] == list(g[f"tkeep_{ci}"])
