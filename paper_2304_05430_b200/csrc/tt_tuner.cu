@@ -5,21 +5,22 @@
 
 namespace tt {
 
-constexpr int kScoreP = 8;  // programs per CTA tile in the scoring kernel
+template <typename R>
+struct ScoreP {
+  static constexpr int value = sizeof(R) == 4 ? 8 : 4;  // programs per CTA tile
+};
 
 // ----------------------------------------------------------- scoring --
 template <typename R, int P>
-struct ScoreSmemLayout {
-  static size_t bytes(const TDims& d) {
-    const size_t n = (size_t)2 * P * d.H + (size_t)2 * P * d.G + (size_t)3 * P * d.D +
-                     (size_t)P * d.heads * d.Tmax + (size_t)P * (d.D + d.C) +
-                     (size_t)P * kHeadHidden + P;
-    return n * sizeof(R) + 64;
-  }
-};
+static size_t score_smem_bytes(const TDims& d) {
+  const size_t n = (size_t)2 * P * d.H + (size_t)2 * P * d.G +
+                   (size_t)3 * P * d.D + (size_t)P * d.heads * d.Tmax + (size_t)P * (d.D + d.C) +
+                   (size_t)P * kHeadHidden + kThreads + P + 8;
+  return n * sizeof(R) + 64;
+}
 
 template <typename R, int H, int P>
-__global__ void __launch_bounds__(kThreads) tuner_predict_kernel(
+__global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
     TDims dm, const R* __restrict__ prm, const R* __restrict__ steps,
     const int64_t* __restrict__ rowoff, const R* __restrict__ ctx, int64_t n,
     R* __restrict__ yhat, R* __restrict__ scratch, int64_t slot_elems) {
@@ -44,7 +45,10 @@ __global__ void __launch_bounds__(kThreads) tuner_predict_kernel(
   sp += P * (D + dm.C);
   am.a1 = sp;
   sp += P * kHeadHidden;
+  am.red = sp;
+  sp += kThreads;
   R* sh_y = sp;
+  const AttnW<R> aw = attn_global_view<R>(dm, prm);
   const int64_t TD = (int64_t)dm.Tmax * D;
   R* buf[3];
   buf[0] = scratch + (int64_t)blockIdx.x * slot_elems;
@@ -70,18 +74,13 @@ __global__ void __launch_bounds__(kThreads) tuner_predict_kernel(
     __syncthreads();
     int cur = 0;
     for (int l = 0; l < dm.L; ++l) {
-      const R* in0[P];
-#pragma unroll
-      for (int p = 0; p < P; ++p)
-        in0[p] = l == 0 ? ti.step0[p] : buf[cur ^ 1] + p * TD;
-      const int stride = l == 0 ? dm.d0 : D;
-      lstm_layer_fwd<R, H, P, false>(dm, prm, l, ti, in0, stride, buf[cur], sh_h, sh_g, nullptr,
-                                     nullptr, nullptr);
+      lstm_layer_fwd<R, H, P, false>(dm, prm, l, ti, buf[cur ^ 1], buf[cur], sh_h, sh_g,
+                                     buf[2] + P * TD, nullptr, nullptr, nullptr);
       __syncthreads();
       cur ^= 1;
     }
     // final layer output is buf[cur ^ 1]; K -> buf[cur], V -> buf[2]
-    attention_head_fwd<R, H, P, false>(dm, prm, ti, buf[cur ^ 1], buf[cur], buf[2], am, nullptr,
+    attention_head_fwd<R, H, P, false>(dm, aw, ti, buf[cur ^ 1], buf[cur], buf[2], am, nullptr,
                                        sh_y);
     if (threadIdx.x < P && ti.prog[threadIdx.x] >= 0) yhat[ti.prog[threadIdx.x]] = sh_y[threadIdx.x];
     __syncthreads();
@@ -112,13 +111,24 @@ struct TrainArgs {
   R* step_loss;
   R* grad_out;
   int32_t* status;
-  R* partial;          // [grid][NP]
-  R* sample_scratch;   // [grid][spc][sample_elems]
+  R* partial;          // [nsample_ctas][NP]
+  R* sample_scratch;   // [nsample_ctas][spc][sample_elems]
   int spc;
-  R* bwd_scratch;      // [grid][bwd_elems]
+  R* bwd_scratch;      // [nsample_ctas][bwd_elems]
   R* batch_yhat;       // [B]
+  R* lb;               // [3][B] loss staging (labels, scores, d/dscore) -- per CTA
   unsigned int* barrier;
 };
+
+template <typename R>
+static size_t train_smem_bytes(const TDims& d) {
+  const int NQ = 128 / d.H;
+  const int64_t wreg = std::max<int64_t>(attn_stage_elems(d), lstm_stage_elems(d));
+  const size_t n = (size_t)wreg + 2 * d.H + 2 * d.G + 3 * d.D + d.heads * d.Tmax + d.D + d.C +
+                   kHeadHidden + kThreads + 4 + kHeadHidden + 3 * d.D + d.heads * d.Tmax +
+                   2 * d.G + 2 * NQ * d.H + 8;
+  return n * sizeof(R) + 64;
+}
 
 template <typename R, int H>
 __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a) {
@@ -131,10 +141,14 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
   const int tid = threadIdx.x;
   // ---- shared memory carve-up
   R* sp = reinterpret_cast<R*>(smem_raw);
+  R* wst = sp;  // staged weights (attention/head, then per-layer LSTM)
+  sp += std::max<int64_t>(attn_stage_elems(dm), lstm_stage_elems(dm));
   R* sh_h = sp;
   sp += 2 * H;
   R* sh_g = sp;
   sp += 2 * G;
+  R* red = sp;
+  sp += kThreads;
   AttnSmem<R, 1> am;
   am.pool = sp;
   sp += D;
@@ -148,6 +162,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
   sp += D + dm.C;
   am.a1 = sp;
   sp += kHeadHidden;
+  am.red = red;
   R* sh_y = sp;
   sp += 4;
   BwdSmem<R> bm;
@@ -165,23 +180,24 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
   sp += 2 * G;
   bm.part = sp;
   sp += 2 * NQ * H;
-  R* lb_y = sp;
-  sp += a.B;
-  R* lb_s = sp;
-  sp += a.B;
-  R* lb_d = sp;
-  sp += a.B;
-  R* red = sp;  // [kThreads]
+  bm.red = red;
 
   const int64_t NP = dm.total;
+  const bool sampler = blockIdx.x < (unsigned)min((int)gridDim.x, a.B);
+  const int nsamp_ctas = min((int)gridDim.x, a.B);
   R* part = a.partial + (int64_t)blockIdx.x * NP;
   R* bws = a.bwd_scratch + (int64_t)blockIdx.x * ly.bwd_elems;
+  R* lb_y = a.lb + (int64_t)blockIdx.x * 3 * a.B;
+  R* lb_s = lb_y + a.B;
+  R* lb_d = lb_s + a.B;
   unsigned int bar_target = 0;
   const int64_t TD = (int64_t)dm.Tmax * D;
 
   for (int step = 0; step < a.n_steps; ++step) {
     const int64_t b0 = (int64_t)step * a.B;
     const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
+    AttnW<R> aw{};
+    if (sampler && (int)blockIdx.x < bn) aw = stage_attn<R>(dm, a.prm, wst);
     // ---- forward with caches for this CTA's samples
     int slot = 0;
     for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
@@ -196,52 +212,57 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
       }
       __syncthreads();
       for (int l = 0; l < dm.L; ++l) {
-        const R* in0[1] = {l == 0 ? ti.step0[0] : smp + ly.S + (int64_t)(l - 1) * TD};
-        const int stride = l == 0 ? dm.d0 : D;
-        lstm_layer_fwd<R, H, 1, true>(dm, a.prm, l, ti, in0, stride, smp + ly.S + (int64_t)l * TD,
-                                      sh_h, sh_g, smp + ly.gates + (int64_t)l * 2 * dm.Tmax * G,
+        lstm_layer_fwd<R, H, 1, true>(dm, a.prm, l, ti, smp + ly.S + (int64_t)(l - 1) * TD,
+                                      smp + ly.S + (int64_t)l * TD, sh_h, sh_g, bws + ly.xz,
+                                      smp + ly.gates + (int64_t)l * 2 * dm.Tmax * G,
                                       smp + ly.cst + (int64_t)l * 2 * dm.Tmax * H,
                                       smp + ly.tcs + (int64_t)l * 2 * dm.Tmax * H);
         __syncthreads();
       }
       AttnCache<R> cache{smp + ly.pin, smp + ly.q,  smp + ly.alpha, smp + ly.mix,
                          smp + ly.z,   smp + ly.a1, smp + ly.yhat};
-      attention_head_fwd<R, H, 1, true>(dm, a.prm, ti, smp + ly.S + (int64_t)(dm.L - 1) * TD,
+      attention_head_fwd<R, H, 1, true>(dm, aw, ti, smp + ly.S + (int64_t)(dm.L - 1) * TD,
                                         smp + ly.K, smp + ly.V, am, &cache, sh_y);
       if (tid == 0) a.batch_yhat[k] = sh_y[0];
       __syncthreads();
     }
     grid_barrier(a.barrier, bar_target);
-    // ---- loss over the whole minibatch (every CTA, identical arithmetic)
-    for (int k = tid; k < bn; k += kThreads) {
-      lb_y[k] = a.y[a.order[b0 + k]];
-      lb_s[k] = __ldcg(a.batch_yhat + k);
-    }
-    __syncthreads();
-    const R loss = a.loss_kind == TT_LOSS_RANK ? rank_loss_block<R>(lb_y, lb_s, bn, lb_d, red)
-                                               : mse_block<R>(lb_y, lb_s, bn, lb_d, red);
-    if (tid == 0) {
-      s_stop = !isfinite((double)loss);
-      if (blockIdx.x == 0) {
-        a.step_loss[step] = loss;
-        if (s_stop) a.status[0] = step;
+    if (sampler && (int)blockIdx.x < bn) {
+      // ---- loss over the whole minibatch (every sampling CTA, identical arithmetic)
+      for (int k = tid; k < bn; k += kThreads) {
+        lb_y[k] = a.y[a.order[b0 + k]];
+        lb_s[k] = __ldcg(a.batch_yhat + k);
+      }
+      __syncthreads();
+      const R loss = a.loss_kind == TT_LOSS_RANK ? rank_loss_block<R>(lb_y, lb_s, bn, lb_d, red)
+                                                 : mse_block<R>(lb_y, lb_s, bn, lb_d, red);
+      if (tid == 0) {
+        s_stop = !isfinite((double)loss);
+        if (blockIdx.x == 0) {
+          a.step_loss[step] = loss;
+          if (s_stop) a.status[0] = step;
+        }
+      }
+      __syncthreads();
+      // ---- backward for this CTA's samples into its partial gradient
+      if (!s_stop) {
+        slot = 0;
+        for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
+          const int64_t idx = a.order[b0 + k];
+          const R* smp = a.sample_scratch + ((int64_t)blockIdx.x * a.spc + slot) * ly.sample_elems;
+          const int64_t r0 = a.rowoff[idx];
+          const int len = (int)(a.rowoff[idx + 1] - r0);
+          if (slot > 0) aw = stage_attn<R>(dm, a.prm, wst);  // LSTM staging overwrote it
+          backward_sample<R, H>(dm, ly, a.prm, aw, len, a.steps + r0 * dm.d0, lb_d[k], smp, bws,
+                                bm, wst, part, slot == 0);
+        }
       }
     }
-    __syncthreads();
-    if (s_stop) break;  // uniform across the grid: same inputs, same arithmetic
-    // ---- backward for this CTA's samples into its partial gradient
-    slot = 0;
-    for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
-      const int64_t idx = a.order[b0 + k];
-      const R* smp = a.sample_scratch + ((int64_t)blockIdx.x * a.spc + slot) * ly.sample_elems;
-      const int64_t r0 = a.rowoff[idx];
-      const int len = (int)(a.rowoff[idx + 1] - r0);
-      backward_sample<R, H>(dm, ly, a.prm, len, a.steps + r0 * dm.d0, lb_d[k], smp, bws, bm, part,
-                            slot == 0);
-    }
     grid_barrier(a.barrier, bar_target);
-    // ---- deterministic fixed-order reduction + fused Adam (or gradient out)
-    const int nact = min((int)gridDim.x, bn);
+    // every CTA reads the stop flag published by CTA 0 (status) -- uniform exit
+    if (__ldcg(a.status) >= 0) break;
+    // ---- deterministic fixed-order reduction + fused Adam (or gradient out), all CTAs
+    const int nact = min(nsamp_ctas, bn);
     const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
     const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
     for (int64_t p = (int64_t)blockIdx.x * kThreads + tid; p < NP; p += (int64_t)gridDim.x * kThreads) {
@@ -268,19 +289,20 @@ struct Launch {
   static int predict_h(const TDims& dm, const R* prm, const R* steps, const int64_t* rowoff,
                        const R* ctx, int64_t n, R* yhat, void* ws, size_t ws_bytes,
                        cudaStream_t st) {
-    constexpr int P = kScoreP;
-    const int64_t slot = (int64_t)3 * P * dm.Tmax * dm.D;
-    int grid = (int)std::min<int64_t>((n + P - 1) / P, (int64_t)sm_count() * 2);
+    constexpr int P = ScoreP<R>::value;
+    const int64_t slot = (int64_t)3 * P * dm.Tmax * dm.D + (int64_t)2 * P * dm.Tmax * dm.G;
+    const size_t smem = score_smem_bytes<R, P>(dm);
+    auto kern = tuner_predict_kernel<R, H, P>;
+    TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    TT_REQUIRE(per_sm >= 1, "tuner predict: kernel cannot be resident (smem %zu)", smem);
+    int grid = (int)std::min<int64_t>((n + P - 1) / P, (int64_t)sm_count() * per_sm);
     const size_t need = (size_t)grid * slot * sizeof(R);
     if (ws_bytes < need) {
-      // fewer resident slots if the caller gave a smaller workspace
       grid = (int)(ws_bytes / (slot * sizeof(R)));
       TT_REQUIRE(grid >= 1, "tuner predict: workspace too small");
     }
-    const size_t smem = ScoreSmemLayout<R, P>::bytes(dm);
-    auto kern = tuner_predict_kernel<R, H, P>;
-    if (smem > 48 * 1024)
-      TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, kThreads, smem, st>>>(dm, prm, steps, rowoff, ctx, n, yhat,
                                        static_cast<R*>(ws), slot);
     return check_launch("tuner predict");
@@ -299,25 +321,22 @@ struct Launch {
     return TT_EINVAL;
   }
 
-  static size_t train_smem(const TDims& d, int B) {
-    const int NQ = 128 / d.H;
-    const size_t n = 2 * d.H + 2 * d.G + 3 * d.D + d.heads * d.Tmax + d.D + d.C + kHeadHidden + 4 +
-                     kHeadHidden + 3 * d.D + d.heads * d.Tmax + 2 * d.G + 2 * NQ * d.H +
-                     3 * (size_t)B + kThreads;
-    return n * sizeof(R) + 64;
+  static int grid_for(int B) {
+    (void)B;
+    return sm_count();  // sampling CTAs = min(grid, B); all CTAs reduce + update
   }
-
-  static int grid_for(int B) { return std::max(1, std::min(B, sm_count())); }
 
   static size_t train_ws(const TDims& dm, int B) {
     const TrainLayout ly = make_train_layout(dm);
     const int grid = grid_for(B);
-    const int spc = (B + grid - 1) / grid;
+    const int ns = std::min(grid, B);
+    const int spc = (B + ns - 1) / ns;
     size_t b = 0;
-    b += align_up((size_t)grid * dm.total * sizeof(R), 256);
-    b += align_up((size_t)grid * spc * ly.sample_elems * sizeof(R), 256);
-    b += align_up((size_t)grid * ly.bwd_elems * sizeof(R), 256);
+    b += align_up((size_t)ns * dm.total * sizeof(R), 256);
+    b += align_up((size_t)ns * spc * ly.sample_elems * sizeof(R), 256);
+    b += align_up((size_t)ns * ly.bwd_elems * sizeof(R), 256);
     b += align_up((size_t)B * sizeof(R), 256);
+    b += align_up((size_t)grid * 3 * B * sizeof(R), 256);
     b += 256;
     return b;
   }
@@ -325,21 +344,24 @@ struct Launch {
   template <int H>
   static int train_h(TrainArgs<R> a, void* ws, size_t ws_bytes, cudaStream_t st) {
     const int grid = grid_for(a.B);
-    a.spc = (a.B + grid - 1) / grid;
+    const int ns = std::min(grid, a.B);
+    a.spc = (a.B + ns - 1) / ns;
     char* w = static_cast<char*>(ws);
     TT_REQUIRE(ws_bytes >= train_ws(a.dm, a.B), "tuner train: workspace %zu < %zu", ws_bytes,
                train_ws(a.dm, a.B));
     a.partial = reinterpret_cast<R*>(w);
-    w += align_up((size_t)grid * a.dm.total * sizeof(R), 256);
+    w += align_up((size_t)ns * a.dm.total * sizeof(R), 256);
     a.sample_scratch = reinterpret_cast<R*>(w);
-    w += align_up((size_t)grid * a.spc * a.ly.sample_elems * sizeof(R), 256);
+    w += align_up((size_t)ns * a.spc * a.ly.sample_elems * sizeof(R), 256);
     a.bwd_scratch = reinterpret_cast<R*>(w);
-    w += align_up((size_t)grid * a.ly.bwd_elems * sizeof(R), 256);
+    w += align_up((size_t)ns * a.ly.bwd_elems * sizeof(R), 256);
     a.batch_yhat = reinterpret_cast<R*>(w);
     w += align_up((size_t)a.B * sizeof(R), 256);
+    a.lb = reinterpret_cast<R*>(w);
+    w += align_up((size_t)grid * 3 * a.B * sizeof(R), 256);
     a.barrier = reinterpret_cast<unsigned int*>(w);
     TT_CUDA(cudaMemsetAsync(a.barrier, 0, 256, st));
-    const size_t smem = train_smem(a.dm, a.B);
+    const size_t smem = train_smem_bytes<R>(a.dm);
     auto kern = tuner_train_kernel<R, H>;
     TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -398,6 +420,7 @@ static int train_entry(R* prm, R* m, R* v, const R* steps, const int64_t* rowoff
   TT_REQUIRE(mode == TT_MODE_TRAIN || mode == TT_MODE_GRAD, "tuner train: bad mode");
   TT_REQUIRE(loss_kind == TT_LOSS_MSE || loss_kind == TT_LOSS_RANK, "tuner train: bad loss");
   TT_REQUIRE(mode == TT_MODE_GRAD || corr != nullptr, "tuner train: corr required");
+  TT_REQUIRE(status != nullptr, "tuner train: status required");
   if (mode == TT_MODE_GRAD) TT_REQUIRE(n_order <= B, "tuner grad: one minibatch only");
   TrainArgs<R> a{};
   a.dm = make_dims(L, H, heads, U, d0, C, Tmax);
@@ -438,7 +461,9 @@ int64_t tt_tuner_param_count(int32_t L, int32_t H, int32_t d0, int32_t C) {
 size_t tt_tuner_predict_workspace_bytes(int32_t f64, int32_t L, int32_t H, int32_t Tmax) {
   (void)L;
   const size_t es = f64 ? 8 : 4;
-  return (size_t)sm_count() * 2 * 3 * kScoreP * Tmax * 2 * H * es;
+  const int P = f64 ? ScoreP<double>::value : ScoreP<float>::value;
+  const size_t slot = (size_t)3 * P * Tmax * 2 * H + (size_t)2 * P * Tmax * 4 * H;
+  return (size_t)sm_count() * 3 * slot * es;
 }
 
 int tt_tuner_predict_f32(const float* prm, const float* steps, const int64_t* rowoff,
@@ -460,9 +485,8 @@ int tt_tuner_predict_f64(const double* prm, const double* steps, const int64_t* 
 size_t tt_tuner_train_workspace_bytes(int32_t f64, int32_t L, int32_t H, int32_t d0, int32_t C,
                                       int32_t Tmax, int32_t B) {
   if (L < 1 || L > kMaxLayers || B < 1) return 0;
-  const TDims dm = make_dims(L, H, 2, 2, d0, C, Tmax);
+  TDims big = make_dims(L, H, 2, 2, d0, C, Tmax);
   // heads/unroll only size small cache segments; use generous upper bounds
-  TDims big = dm;
   big.heads = 2 * H;
   big.U = 16;
   return f64 ? Launch<double>::train_ws(big, B) : Launch<float>::train_ws(big, B);

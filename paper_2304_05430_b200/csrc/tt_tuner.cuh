@@ -16,6 +16,10 @@
 // recurrent matvec streams only h (shared memory, broadcast) and the layer
 // input row (L1, broadcast).  In the cell phase thread j owns hidden unit j of
 // a subset of programs, keeping the cell state in registers.
+//
+// Attention/head weights (4 x 2Hx2H, 2H+C x 64, biases) are staged once into
+// shared memory with a +1 padded row stride, so both column-owner (forward)
+// and row-owner (backward, transposed) matvecs are bank-conflict free.
 #pragma once
 
 #include "tt_ops.cuh"
@@ -82,9 +86,10 @@ inline TDims make_dims(int L, int H, int heads, int U, int d0, int C, int Tmax) 
   return d;
 }
 
-// Weight loads: TRAIN kernels re-read parameters that other CTAs update
-// (Adam) between grid barriers, so they use coherent ld.global (the barrier's
-// ld.acquire.gpu invalidates L1); scoring kernels use the read-only path.
+// Weight loads from global memory.  TRAIN kernels re-read parameters that
+// other CTAs update (Adam) between grid barriers, so they use coherent
+// ld.global (the barrier's ld.acquire.gpu invalidates L1); scoring kernels
+// use the read-only path.
 template <bool TRAIN, typename R>
 __device__ __forceinline__ R ldw(const R* p) {
   if constexpr (TRAIN)
@@ -93,8 +98,8 @@ __device__ __forceinline__ R ldw(const R* p) {
     return __ldg(p);
 }
 
-// dot(x[0:N], w[0:N]) with 4 independent partial sums; x is an aligned row in
-// global or shared memory (vectorised), w a register array.
+// dot(x[0:N], w[0:N]) with independent partial sums; x is a 16-B aligned row
+// in global or shared memory (vectorised), w a register array.
 template <int N>
 __device__ __forceinline__ float dot_reg(const float* __restrict__ x, const float (&w)[N]) {
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -142,16 +147,235 @@ struct TileInfo {
   int64_t prog[P];       // program index (-1 = empty)
 };
 
+// ----------------------------------------------------- staged weights --
+template <typename R>
+struct AttnW {
+  const R *Wq, *Wk, *Wv, *Wo;  // [D][ldd]
+  const R *bq, *bo;            // [D]
+  const R* W1;                 // [D+C][ld1]
+  const R *b1, *W2;            // [64]
+  R b2;
+  int ldd, ld1;
+};
+
+__host__ __device__ inline int64_t attn_stage_elems(const TDims& d) {
+  const int64_t n = 4LL * d.D * (d.D + 1) + 2LL * d.D + (int64_t)(d.D + d.C) * (kHeadHidden + 1) +
+                    2LL * kHeadHidden + 1;
+  return (n + 3) & ~int64_t(3);
+}
+
+// Staging of row-major matrices from global into shared memory with a padded
+// row stride.  All segments of one phase are copied by a single flattened
+// loop of 16-B vector loads, 8 in flight per thread, so a whole phase costs
+// about one L2 round trip instead of one per element.  Requirements (hold
+// for every tensor of the parameter layout): source 16-B aligned, cols a
+// multiple of the vector width.
+struct StageSeg {
+  int64_t src;  // element offset in the parameter vector
+  int64_t dst;  // element offset in the smem region
+  int cols, ld, nvec, vbase;  // vectors in this segment, prefix count
+};
+
+template <typename R>
+struct VecOf;
+template <>
+struct VecOf<float> {
+  using T = float4;
+  static constexpr int N = 4;
+};
+template <>
+struct VecOf<double> {
+  using T = double2;
+  static constexpr int N = 2;
+};
+
+template <typename R>
+__device__ __forceinline__ void store_vec(R* d, const float4& v) {
+  d[0] = v.x;
+  d[1] = v.y;
+  d[2] = v.z;
+  d[3] = v.w;
+}
+template <typename R>
+__device__ __forceinline__ void store_vec(R* d, const double2& v) {
+  d[0] = v.x;
+  d[1] = v.y;
+}
+
+template <typename R, int NS>
+__device__ void stage_segments(const R* __restrict__ prm, R* __restrict__ smem,
+                               const StageSeg (&sg)[NS], int nseg) {
+  using V = typename VecOf<R>::T;
+  constexpr int VN = VecOf<R>::N;
+  const int total = sg[nseg - 1].vbase + sg[nseg - 1].nvec;
+  constexpr int U = 8;
+  for (int i0 = threadIdx.x; i0 < total; i0 += U * kThreads) {
+    V v[U];
+    int seg[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * kThreads;
+      int s = 0;
+      while (s + 1 < nseg && i >= sg[s + 1].vbase) ++s;
+      seg[u] = s;
+      if (i < total) v[u] = reinterpret_cast<const V*>(prm + sg[s].src)[i - sg[s].vbase];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = i0 + u * kThreads;
+      if (i < total) {
+        const StageSeg& g = sg[seg[u]];
+        const int e = (i - g.vbase) * VN;
+        const int r = e / g.cols, c = e - r * g.cols;
+        store_vec<R>(smem + g.dst + (int64_t)r * g.ld + c, v[u]);
+      }
+    }
+  }
+}
+
+__host__ __device__ inline StageSeg make_seg(int64_t src, int64_t dst, int rows, int cols, int ld,
+                                             int vn, int& vbase) {
+  StageSeg s;
+  s.src = src;
+  s.dst = dst;
+  s.cols = cols;
+  s.ld = ld;
+  s.nvec = rows * cols / vn;
+  s.vbase = vbase;
+  vbase += s.nvec;
+  return s;
+}
+
+// All threads; ends with __syncthreads.  Layout: Wq Wk Wv Wo [D][D+1],
+// bq bo [D], W1 [D+C][65], b1 W2 [64].
+template <typename R>
+__device__ AttnW<R> stage_attn(const TDims& dm, const R* prm, R* dst) {
+  constexpr int VN = VecOf<R>::N;
+  const int D = dm.D;
+  AttnW<R> w;
+  w.ldd = D + 1;
+  w.ld1 = kHeadHidden + 1;
+  const int64_t DD = (int64_t)D * w.ldd;
+  const int64_t oW1 = 4 * DD + 2 * D;
+  const int64_t ob1 = oW1 + (int64_t)(D + dm.C) * w.ld1;
+  StageSeg sg[6];
+  int vb = 0;
+  sg[0] = make_seg(dm.Wq, 0, D, D, w.ldd, VN, vb);
+  sg[1] = make_seg(dm.Wk, DD, D, D, w.ldd, VN, vb);
+  sg[2] = make_seg(dm.Wv, 2 * DD, D, D, w.ldd, VN, vb);
+  sg[3] = make_seg(dm.Wo, 3 * DD, D, D, w.ldd, VN, vb);
+  sg[4] = make_seg(dm.W1, oW1, D + dm.C, kHeadHidden, w.ld1, VN, vb);
+  sg[5] = make_seg(dm.b1, ob1, 1, 2 * kHeadHidden, 2 * kHeadHidden, VN, vb);  // b1 | W2
+  stage_segments<R, 6>(prm, dst, sg, 6);
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {  // bq | bo (contiguous too, tiny)
+    dst[4 * DD + i] = prm[dm.bq + i];
+    dst[4 * DD + D + i] = prm[dm.bo + i];
+  }
+  w.Wq = dst;
+  w.Wk = dst + DD;
+  w.Wv = dst + 2 * DD;
+  w.Wo = dst + 3 * DD;
+  w.bq = dst + 4 * DD;
+  w.bo = dst + 4 * DD + D;
+  w.W1 = dst + oW1;
+  w.b1 = dst + ob1;
+  w.W2 = dst + ob1 + kHeadHidden;
+  w.b2 = prm[dm.b2];
+  __syncthreads();
+  return w;
+}
+
+// Unstaged view (read-only kernels: the batched matvecs of a P-program tile
+// read each weight once per tile with coalesced loads, so staging would only
+// cost occupancy).
+template <typename R>
+__device__ AttnW<R> attn_global_view(const TDims& dm, const R* prm) {
+  AttnW<R> w;
+  w.ldd = dm.D;
+  w.ld1 = kHeadHidden;
+  w.Wq = prm + dm.Wq;
+  w.Wk = prm + dm.Wk;
+  w.Wv = prm + dm.Wv;
+  w.Wo = prm + dm.Wo;
+  w.bq = prm + dm.bq;
+  w.bo = prm + dm.bo;
+  w.W1 = prm + dm.W1;
+  w.b1 = prm + dm.b1;
+  w.W2 = prm + dm.W2;
+  w.b2 = prm[dm.b2];
+  return w;
+}
+
+// --------------------------------------------------------- block matvecs --
+// out[c] = bias[c] + sum_{k<K} v[k] W[k*ld + c]   (c < NC, NC | 256)
+// Thread (c = tid % NC, s = tid / NC) sums k = s (mod S); the S partials are
+// combined in fixed order through `red` (deterministic).  Ends synced.
+template <typename R>
+__device__ void bmv_col(const R* v, const R* W, int ld, int K, int NC, const R* bias, R* out,
+                        R* red) {
+  const int S = kThreads / NC;
+  const int c = threadIdx.x % NC, s = threadIdx.x / NC;
+  R acc = 0;
+  for (int k = s; k < K; k += S) acc += v[k] * W[k * ld + c];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if ((int)threadIdx.x < NC) {
+    R t = 0;
+    for (int q = 0; q < S; ++q) t += red[q * NC + threadIdx.x];
+    out[threadIdx.x] = bias ? t + bias[threadIdx.x] : t;
+  }
+  __syncthreads();
+}
+
+// out[k] = sum_{c<NC} W[k*ld + c] v[c]   (k < NK, NK | 256).  Ends synced.
+template <typename R>
+__device__ void bmv_row(const R* W, int ld, const R* v, int NC, int NK, R* out, R* red) {
+  const int S = kThreads / NK;
+  const int k = threadIdx.x % NK, s = threadIdx.x / NK;
+  R acc = 0;
+  for (int c = s; c < NC; c += S) acc += W[k * ld + c] * v[c];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if ((int)threadIdx.x < NK) {
+    R t = 0;
+    for (int q = 0; q < S; ++q) t += red[q * NK + threadIdx.x];
+    out[threadIdx.x] = t;
+  }
+  __syncthreads();
+}
+
+// Batched over P programs: out[p*ldo + c] = bias[c] + sum_k v[p*ldv + k] W[k*ld + c].
+template <typename R, int P>
+__device__ void bmv_col_batch(const R* v, int ldv, const R* W, int ld, int K, int NC,
+                              const R* bias, R* out, int ldo) {
+  const int NG = kThreads / NC;
+  const int c = threadIdx.x % NC, g = threadIdx.x / NC;
+  for (int p0 = g; p0 < P; p0 += 2 * NG) {
+    const int p1 = p0 + NG;
+    R a0 = 0, a1 = 0;
+    const R* v0 = v + p0 * ldv;
+    const R* v1 = v + (p1 < P ? p1 : p0) * ldv;
+    for (int k = 0; k < K; ++k) {
+      const R wk = W[k * ld + c];
+      a0 += v0[k] * wk;
+      a1 += v1[k] * wk;
+    }
+    const R b = bias ? bias[c] : (R)0;
+    out[p0 * ldo + c] = a0 + b;
+    if (p1 < P) out[p1 * ldo + c] = a1 + b;
+  }
+}
+
 // ----------------------------------------------------------- LSTM layer --
-// One bidirectional layer for P programs.  `in0[p]` + t*in_stride is the input
-// row of program p at time t (raw steps for layer 0, previous layer output
-// otherwise).  Output rows: out[(p*Tmax + t)*D + dir*H + j].
+// One bidirectional layer for P programs.  The input row of program p at time
+// t is ti.step0[p] + t*d0 for layer 0 (raw steps) and inbuf + (p*Tmax+t)*D
+// otherwise (previous layer output).  Output rows:
+// out[(p*Tmax + t)*D + dir*H + j].
 // TRAIN (P == 1): also records gates / cell state / tanh(cell) per step.
 template <typename R, int H, int P, bool TRAIN>
 __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l,
-                               const TileInfo<R, P>& ti, const R* const* in0, int in_stride,
-                               R* __restrict__ out, R* sh_h, R* sh_g, R* cache_g, R* cache_c,
-                               R* cache_tc) {
+                               const TileInfo<R, P>& ti, const R* inbuf, R* __restrict__ out,
+                               R* sh_h, R* sh_g, R* xzbuf, R* cache_g, R* cache_c, R* cache_tc) {
   constexpr int G = 4 * H, D = 2 * H, NR = 128 / G, NQ = 128 / H;
   const int dir = threadIdx.x >> 7, lt = threadIdx.x & 127;
   const int c = lt % G, r = lt / G;
@@ -159,16 +383,28 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
   const int Tmax = dm.Tmax;
   const R* Wx = prm + dm.wx[l][dir];
   const R* Wh = prm + dm.wh[l][dir];
+  const R bc = ldw<TRAIN>(prm + dm.bb[l][dir] + c);
+  const int d_in = l == 0 ? dm.d0 : D;
+  // Input projection hoisted out of the recurrence (layers >= 1): for every
+  // valid (p, t), xz = b + x_t Wx[:, c].  Each thread later reads back only
+  // the entries it wrote, so no barrier is needed.  The Wx column is live
+  // only here, leaving the recurrence with the Wh column alone.
+  R* xz = xzbuf + (int64_t)dir * P * Tmax * G;
+  if (l > 0) {
+    R wx[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) wx[k] = ldw<TRAIN>(Wx + k * G + c);
+#pragma unroll 1
+    for (int p = r; p < P; p += NR) {
+      const int n = ti.len[p];
+      for (int t = 0; t < n; ++t)
+        xz[((int64_t)p * Tmax + t) * G + c] =
+            dot_reg<D>(inbuf + ((int64_t)p * Tmax + t) * D, wx) + bc;
+    }
+  }
   R wh[H];
 #pragma unroll
   for (int k = 0; k < H; ++k) wh[k] = ldw<TRAIN>(Wh + k * G + c);
-  R wx[D];
-  if (l > 0) {
-#pragma unroll
-    for (int k = 0; k < D; ++k) wx[k] = ldw<TRAIN>(Wx + k * G + c);
-  }
-  const R bc = ldw<TRAIN>(prm + dm.bb[l][dir] + c);
-  const int d_in = l == 0 ? dm.d0 : D;
   constexpr int NC = (P + NQ - 1) / NQ;
   R creg[NC];
 #pragma unroll
@@ -181,21 +417,23 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
   for (int p = 0; p < P; ++p) Tt = max(Tt, ti.len[p]);
   named_barrier(1 + dir, 128);
   for (int s = 0; s < Tt; ++s) {
-    // gate phase: z = b + x_t Wx + h Wh ; activation by gate block
-#pragma unroll
+    // gate phase: z = b + x_t Wx + h Wh ; activation by gate block.  One
+    // program at a time (not unrolled) keeps the register file for the
+    // stationary weight columns.
+#pragma unroll 1
     for (int p = r; p < P; p += NR) {
       const int n = ti.len[p];
       if (s < n) {
         const int t = dir == 0 ? s : n - 1 - s;
-        const R* x = in0[p] + (int64_t)t * in_stride;
         R z;
         if (l > 0) {
-          z = dot_reg<D>(x, wx);
+          z = xz[((int64_t)p * Tmax + t) * G + c];
         } else {
-          z = 0;
+          const R* x = ti.step0[p] + (int64_t)t * dm.d0;
+          z = bc;
           for (int k = 0; k < d_in; ++k) z += x[k] * ldw<TRAIN>(Wx + k * G + c);
         }
-        z += dot_reg<H>(hbase + p * H, wh) + bc;
+        z += dot_reg<H>(hbase + p * H, wh);
         const int gate = c / H;
         const R a = gate == 2 ? Act<R>::tanh(z) : Act<R>::sigmoid(z);
         gbase[p * G + c] = a;
@@ -240,6 +478,7 @@ struct AttnSmem {
   R* alpha;  // [P][heads][Tmax]
   R* z;      // [P][D + C]
   R* a1;     // [P][64]
+  R* red;    // [kThreads]
 };
 
 // Training cache of one sample (P == 1).
@@ -255,16 +494,18 @@ struct AttnCache {
 };
 
 // S, K, V: [P][Tmax][D] (global scratch).  Writes yhat[p] to out_yhat[p] for
-// occupied slots.  All 256 threads participate.
+// occupied slots.  All 256 threads participate; weights come from `w`
+// (shared memory).  P == 1 uses latency-oriented sliced matvecs.
 template <typename R, int H, int P, bool TRAIN>
-__device__ void attention_head_fwd(const TDims& dm, const R* __restrict__ prm,
-                                   const TileInfo<R, P>& ti, const R* __restrict__ S,
-                                   R* __restrict__ Kb, R* __restrict__ Vb, const AttnSmem<R, P>& sm,
+__device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const TileInfo<R, P>& ti,
+                                   const R* __restrict__ S, R* __restrict__ Kb,
+                                   R* __restrict__ Vb, const AttnSmem<R, P>& sm,
                                    const AttnCache<R>* cache, R* out_yhat) {
   constexpr int D = 2 * H;
   const int tid = threadIdx.x;
   const int Tmax = dm.Tmax, heads = dm.heads, dh = dm.dh, C = dm.C;
   const int warp = tid >> 5, lane = tid & 31;
+  const int Z = D + C;
   // p0 = masked mean (tuner.py:252-253)
   for (int i = tid; i < P * D; i += kThreads) {
     const int p = i / D, d = i % D;
@@ -279,35 +520,35 @@ __device__ void attention_head_fwd(const TDims& dm, const R* __restrict__ prm,
     constexpr int NGRP = kThreads / NCOL >= 1 ? kThreads / NCOL : 1;
     const int cc = tid % NCOL, grp = tid / NCOL;
     if (grp < NGRP) {
-      const R* W = prm + (cc < D ? dm.Wk : dm.Wv);
       const int col = cc % D;
-      R w[D];
+      const R* wp = (cc < D ? w.Wk : w.Wv) + col;
+      const int ld = w.ldd;
+      R wc[D];
 #pragma unroll
-      for (int k = 0; k < D; ++k) w[k] = ldw<TRAIN>(W + k * D + col);
+      for (int k = 0; k < D; ++k) {
+        wc[k] = *wp;
+        wp += ld;
+      }
       R* dst = cc < D ? Kb : Vb;
-      for (int p = grp; p < P; p += NGRP) {
+      for (int p = 0; p < P; ++p) {
         const int n = ti.len[p];
-        for (int t = 0; t < n; ++t) {
+        for (int t = grp; t < n; t += NGRP) {
           const int64_t row = ((int64_t)p * Tmax + t) * D;
-          dst[row + col] = dot_reg<D>(S + row, w);
+          dst[row + col] = dot_reg<D>(S + row, wc);
         }
       }
     }
   }
   __syncthreads();
-  const R inv_scale = (R)1 / sqrt((R)dh);
-  (void)inv_scale;
   const R sq = sqrt((R)dh);
   for (int u = 0; u < dm.U; ++u) {
     // q = pooled Wq + bq
-    for (int i = tid; i < P * D; i += kThreads) {
-      const int p = i / D, c = i % D;
-      const R* W = prm + dm.Wq + c;
-      R acc = 0;
-      for (int k = 0; k < D; ++k) acc += sm.pool[p * D + k] * ldw<TRAIN>(W + k * D);
-      sm.q[i] = acc + ldw<TRAIN>(prm + dm.bq + c);
+    if constexpr (P == 1)
+      bmv_col<R>(sm.pool, w.Wq, w.ldd, D, D, w.bq, sm.q, sm.red);
+    else {
+      bmv_col_batch<R, P>(sm.pool, D, w.Wq, w.ldd, D, D, w.bq, sm.q, D);
+      __syncthreads();
     }
-    __syncthreads();
     if constexpr (TRAIN) {
       for (int i = tid; i < D; i += kThreads) {
         cache->pin[u * D + i] = sm.pool[i];
@@ -355,17 +596,14 @@ __device__ void attention_head_fwd(const TDims& dm, const R* __restrict__ prm,
       for (int i = tid; i < heads * Tmax; i += kThreads) cache->alpha[u * heads * Tmax + i] = sm.alpha[i];
     }
     // pooled = mix Wo + bo
-    for (int i = tid; i < P * D; i += kThreads) {
-      const int p = i / D, c = i % D;
-      const R* W = prm + dm.Wo + c;
-      R acc = 0;
-      for (int k = 0; k < D; ++k) acc += sm.mix[p * D + k] * ldw<TRAIN>(W + k * D);
-      sm.pool[i] = acc + ldw<TRAIN>(prm + dm.bo + c);
+    if constexpr (P == 1)
+      bmv_col<R>(sm.mix, w.Wo, w.ldd, D, D, w.bo, sm.pool, sm.red);
+    else {
+      bmv_col_batch<R, P>(sm.mix, D, w.Wo, w.ldd, D, D, w.bo, sm.pool, D);
+      __syncthreads();
     }
-    __syncthreads();
   }
   // head: z = [pooled | ctx] ; a1 = tanh(z W1 + b1) ; yhat = sigmoid(a1 W2 + b2)
-  const int Z = D + C;
   for (int i = tid; i < P * Z; i += kThreads) {
     const int p = i / Z, k = i % Z;
     R v = 0;
@@ -376,22 +614,20 @@ __device__ void attention_head_fwd(const TDims& dm, const R* __restrict__ prm,
     sm.z[i] = v;
   }
   __syncthreads();
-  for (int i = tid; i < P * kHeadHidden; i += kThreads) {
-    const int p = i / kHeadHidden, c = i % kHeadHidden;
-    const R* W = prm + dm.W1 + c;
-    const R* zp = sm.z + p * Z;
-    R acc = 0;
-    for (int k = 0; k < Z; ++k) acc += zp[k] * ldw<TRAIN>(W + k * kHeadHidden);
-    sm.a1[i] = Act<R>::tanh(acc + ldw<TRAIN>(prm + dm.b1 + c));
+  if constexpr (P == 1)
+    bmv_col<R>(sm.z, w.W1, w.ld1, Z, kHeadHidden, w.b1, sm.a1, sm.red);
+  else {
+    bmv_col_batch<R, P>(sm.z, Z, w.W1, w.ld1, Z, kHeadHidden, w.b1, sm.a1, kHeadHidden);
+    __syncthreads();
   }
+  for (int i = tid; i < P * kHeadHidden; i += kThreads) sm.a1[i] = Act<R>::tanh(sm.a1[i]);
   __syncthreads();
   for (int p = warp; p < P; p += kThreads / 32) {
     R acc = 0;
-    for (int c = lane; c < kHeadHidden; c += 32)
-      acc += sm.a1[p * kHeadHidden + c] * ldw<TRAIN>(prm + dm.W2 + c);
+    for (int c = lane; c < kHeadHidden; c += 32) acc += sm.a1[p * kHeadHidden + c] * w.W2[c];
     acc = warp_sum(acc);
     if (lane == 0 && ti.len[p] > 0) {
-      const R yh = Act<R>::sigmoid(acc + ldw<TRAIN>(prm + dm.b2));
+      const R yh = Act<R>::sigmoid(acc + w.b2);
       out_yhat[p] = yh;
       if constexpr (TRAIN) cache->yhat[0] = yh;
     }

@@ -1,6 +1,11 @@
 // Attention tuner: backward pass of one sample (tuner.py:287-360 and
 // _LstmDirection.backward :102-151), accumulated into a per-CTA partial
 // gradient vector laid out exactly like the parameter vector.
+//
+// Weights come from shared memory: the attention/head block staged by
+// stage_attn (reused from the forward pass) and, per LSTM layer, both
+// directions' Wx/Wh staged with a +1 padded row stride so the transposed
+// products (dh = dz Wh^T, dX = dZ Wx^T) are bank-conflict free.
 #pragma once
 
 #include "tt_tuner.cuh"
@@ -11,7 +16,7 @@ namespace tt {
 // scratch.  Every segment is padded to 4 elements so rows stay 16-B aligned.
 struct TrainLayout {
   int64_t S, gates, cst, tcs, K, V, pin, q, mix, alpha, z, a1, yhat, sample_elems;
-  int64_t dS, dK, dV, dZ, dX, bwd_elems;
+  int64_t dS, dK, dV, dZ, dX, xz, bwd_elems;
   int NH;  // dX partial groups
 };
 
@@ -47,8 +52,17 @@ inline TrainLayout make_train_layout(const TDims& d) {
   t.dV = seg(TD);
   t.dZ = seg((int64_t)2 * d.Tmax * d.G);
   t.dX = seg((int64_t)2 * t.NH * TD);
+  t.xz = seg((int64_t)2 * d.Tmax * d.G);
   t.bwd_elems = o;
   return t;
+}
+
+// smem elements for one layer's staged LSTM weights (both directions)
+__host__ __device__ inline int64_t lstm_stage_elems(const TDims& d) {
+  const int64_t per_dir = (int64_t)(d.D + d.H) * (d.G + 1);  // layers >= 1 (layer 0 stages Wh only)
+  const int64_t l0 = (int64_t)d.H * (d.G + 1);
+  const int64_t n = 2 * (per_dir > l0 ? per_dir : l0);
+  return (n + 3) & ~int64_t(3);
 }
 
 template <typename R>
@@ -69,20 +83,37 @@ struct BwdSmem {
   R* dlog;  // [heads][Tmax]
   R* dz;    // [2][G]
   R* part;  // [2][NQ][H]
+  R* red;   // [kThreads]
 };
 
 // -------------------------------------------------- LSTM layer backward --
 // dS: in = d(loss)/d(layer output) [Tmax][D]; out (l > 0) = d/d(layer input).
+// wst: shared memory for this layer's weights (lstm_stage_elems).
 template <typename R, int H>
 __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* __restrict__ prm,
                                int l, int len, const R* xin, int in_stride, const R* smp,
-                               R* bws, const BwdSmem<R>& sm, R* part, bool fresh) {
+                               R* bws, const BwdSmem<R>& sm, R* wst, R* part, bool fresh) {
   constexpr int G = 4 * H, D = 2 * H, NQ = 128 / H, NW = (G + NQ - 1) / NQ;
   const int dir = threadIdx.x >> 7, lt = threadIdx.x & 127;
   const int j = lt % H, q = lt / H;
   const int Tmax = dm.Tmax;
-  const R* Wh = prm + dm.wh[l][dir];
-  const R* Wx = prm + dm.wx[l][dir];
+  const int ldg = G + 1;
+  const int d_in = l == 0 ? dm.d0 : D;
+  // ---- stage both directions' Wh (and Wx for l > 0) into shared memory
+  const int64_t per_dir = (int64_t)(l == 0 ? H : D + H) * ldg;
+  {
+    StageSeg sg[4];
+    int vb = 0, ns = 0;
+    constexpr int VN = VecOf<R>::N;
+    for (int d = 0; d < 2; ++d) {
+      sg[ns++] = make_seg(dm.wh[l][d], d * per_dir, H, G, ldg, VN, vb);
+      if (l > 0) sg[ns++] = make_seg(dm.wx[l][d], d * per_dir + (int64_t)H * ldg, D, G, ldg, VN, vb);
+    }
+    stage_segments<R, 4>(prm, wst, sg, ns);
+  }
+  __syncthreads();
+  const R* Whs = wst + dir * per_dir;
+  const R* Wxs = Whs + (int64_t)H * ldg;
   const R* gates = smp + ly.gates + (int64_t)l * 2 * Tmax * G;
   const R* cst = smp + ly.cst + (int64_t)l * 2 * Tmax * H;
   const R* tcs = smp + ly.tcs + (int64_t)l * 2 * Tmax * H;
@@ -95,7 +126,7 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
 #pragma unroll
   for (int i = 0; i < NW; ++i) {
     const int c = q + i * NQ;
-    whr[i] = c < G ? ldw<true>(Wh + j * G + c) : (R)0;
+    whr[i] = c < G ? Whs[j * ldg + c] : (R)0;
   }
   R dwh[H];
 #pragma unroll
@@ -157,11 +188,25 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
 #pragma unroll
     for (int k = 0; k < H; ++k) put(part, dm.wh[l][dir] + (int64_t)k * G + lt, dwh[k], fresh);
     put(part, dm.bb[l][dir] + lt, dbc, fresh);
-    const int d_in = l == 0 ? dm.d0 : D;
-    for (int k = 0; k < d_in; ++k) {
-      R acc = 0;
-      for (int t = 0; t < len; ++t) acc += xin[(int64_t)t * in_stride + k] * dZ[(int64_t)t * G + lt];
-      put(part, dm.wx[l][dir] + (int64_t)k * G + lt, acc, fresh);
+    // dWx[k][c] = sum_t x_t[k] dZ[t][c]
+    if (l > 0) {
+      R acc[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc[k] = 0;
+      for (int t = 0; t < len; ++t) {
+        const R dz = dZ[(int64_t)t * G + lt];
+        const R* xr = xin + (int64_t)t * in_stride;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[k] += xr[k] * dz;
+      }
+#pragma unroll
+      for (int k = 0; k < D; ++k) put(part, dm.wx[l][dir] + (int64_t)k * G + lt, acc[k], fresh);
+    } else {
+      for (int k = 0; k < d_in; ++k) {
+        R acc = 0;
+        for (int t = 0; t < len; ++t) acc += xin[(int64_t)t * in_stride + k] * dZ[(int64_t)t * G + lt];
+        put(part, dm.wx[l][dir] + (int64_t)k * G + lt, acc, fresh);
+      }
     }
   }
   if (l > 0) {
@@ -169,13 +214,18 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
     const int NH = ly.NH;
     const int k = lt % D, hq = lt / D;
     if (hq < NH) {
-      constexpr int NXC = G;  // upper bound on columns per thread
       R* dX = bws + ly.dX + ((int64_t)(dir * NH + hq) * Tmax) * D;
+      const R* wr = Wxs + (int64_t)k * ldg;
       for (int t = 0; t < len; ++t) {
         const R* dzt = dZ + (int64_t)t * G;
-        R acc = 0;
-        for (int c = hq; c < NXC; c += NH) acc += ldw<true>(Wx + (int64_t)k * G + c) * dzt[c];
-        dX[(int64_t)t * D + k] = acc;
+        R a0 = 0, a1 = 0;
+        int c = hq;
+        for (; c + NH < G; c += 2 * NH) {
+          a0 += wr[c] * dzt[c];
+          a1 += wr[c + NH] * dzt[c + NH];
+        }
+        if (c < G) a0 += wr[c] * dzt[c];
+        dX[(int64_t)t * D + k] = a0 + a1;
       }
     }
   }
@@ -193,10 +243,12 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
 }
 
 // ------------------------------------------------------- sample backward --
+// aw: attention/head weights staged in shared memory (stage_attn); wst: the
+// LSTM staging region (may alias aw's storage -- aw is dead by then).
 template <typename R, int H>
 __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R* __restrict__ prm,
-                                int len, const R* step0, R dy, const R* smp, R* bws,
-                                const BwdSmem<R>& sm, R* part, bool fresh) {
+                                const AttnW<R>& aw, int len, const R* step0, R dy, const R* smp,
+                                R* bws, const BwdSmem<R>& sm, R* wst, R* part, bool fresh) {
   constexpr int D = 2 * H;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Tmax = dm.Tmax, heads = dm.heads, dh = dm.dh, C = dm.C, U = dm.U;
@@ -210,7 +262,7 @@ __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R*
   if (tid < kHeadHidden) {
     const R av = a1[tid];
     put(part, dm.W2 + tid, av * dl, fresh);
-    const R da = dl * ldw<true>(prm + dm.W2 + tid) * ((R)1 - av * av);
+    const R da = dl * aw.W2[tid] * ((R)1 - av * av);
     sm.da1[tid] = da;
     put(part, dm.b1 + tid, da, fresh);
   }
@@ -220,12 +272,7 @@ __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R*
     const int k = i / kHeadHidden, c = i % kHeadHidden;
     put(part, dm.W1 + i, z[k] * sm.da1[c], fresh);
   }
-  for (int k = tid; k < D; k += kThreads) {
-    R acc = 0;
-    for (int c = 0; c < kHeadHidden; ++c) acc += ldw<true>(prm + dm.W1 + k * kHeadHidden + c) * sm.da1[c];
-    sm.dpool[k] = acc;
-  }
-  __syncthreads();
+  bmv_row<R>(aw.W1, aw.ld1, sm.da1, kHeadHidden, D, sm.dpool, sm.red);
   // ---- attention passes in reverse (tuner.py:310-328)
   const R* Kb = smp + ly.K;
   const R* Vb = smp + ly.V;
@@ -239,12 +286,7 @@ __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R*
     const R* al = smp + ly.alpha + (int64_t)u * heads * Tmax;
     for (int i = tid; i < D * D; i += kThreads) put(part, dm.Wo + i, mix[i / D] * sm.dpool[i % D], st);
     for (int c = tid; c < D; c += kThreads) put(part, dm.bo + c, sm.dpool[c], st);
-    for (int k = tid; k < D; k += kThreads) {
-      R acc = 0;
-      for (int c = 0; c < D; ++c) acc += ldw<true>(prm + dm.Wo + k * D + c) * sm.dpool[c];
-      sm.dmix[k] = acc;
-    }
-    __syncthreads();
+    bmv_row<R>(aw.Wo, aw.ldd, sm.dpool, D, D, sm.dmix, sm.red);
     for (int h = warp; h < heads; h += kThreads / 32) {
       R sacc = 0;
       for (int t = lane; t < len; t += 32) {
@@ -281,42 +323,49 @@ __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R*
     __syncthreads();
     for (int i = tid; i < D * D; i += kThreads) put(part, dm.Wq + i, pin[i / D] * sm.dq[i % D], st);
     for (int c = tid; c < D; c += kThreads) put(part, dm.bq + c, sm.dq[c], st);
-    for (int k = tid; k < D; k += kThreads) {
-      R acc = 0;
-      for (int c = 0; c < D; ++c) acc += ldw<true>(prm + dm.Wq + k * D + c) * sm.dq[c];
-      sm.dpool[k] = acc;
-    }
-    __syncthreads();
+    bmv_row<R>(aw.Wq, aw.ldd, sm.dq, D, D, sm.dpool, sm.red);
   }
   // ---- d S (tuner.py:331-338)
   const R* S = smp + ly.S + (int64_t)(dm.L - 1) * Tmax * D;
+  // gWk / gWv: thread column cc in [0, 2D), accumulators over k in registers
   for (int cc = tid; cc < 2 * D; cc += kThreads) {
     const R* src = cc < D ? dK : dV;
     const int col = cc % D;
     const int64_t off = cc < D ? dm.Wk : dm.Wv;
-    for (int k = 0; k < D; ++k) {
-      R acc = 0;
-      for (int t = 0; t < len; ++t) acc += S[(int64_t)t * D + k] * src[(int64_t)t * D + col];
-      put(part, off + (int64_t)k * D + col, acc, fresh);
+    R acc[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k] = 0;
+    for (int t = 0; t < len; ++t) {
+      const R g = src[(int64_t)t * D + col];
+      const R* sr = S + (int64_t)t * D;
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc[k] += sr[k] * g;
     }
+#pragma unroll
+    for (int k = 0; k < D; ++k) put(part, off + (int64_t)k * D + col, acc[k], fresh);
   }
   R* dS = bws + ly.dS;
   const R denom = (R)(len > 1 ? len : 1);
   for (int i = tid; i < len * D; i += kThreads) {
     const int t = i / D, k = i % D;
+    const R* wk = aw.Wk + k * aw.ldd;
+    const R* wv = aw.Wv + k * aw.ldd;
+    const R* dkr = dK + (int64_t)t * D;
+    const R* dvr = dV + (int64_t)t * D;
     R a = 0, b = 0;
     for (int c = 0; c < D; ++c) {
-      a += dK[(int64_t)t * D + c] * ldw<true>(prm + dm.Wk + k * D + c);
-      b += dV[(int64_t)t * D + c] * ldw<true>(prm + dm.Wv + k * D + c);
+      a += dkr[c] * wk[c];
+      b += dvr[c] * wv[c];
     }
     dS[i] = (sm.dpool[k] / denom + a) + b;
   }
   __syncthreads();
-  // ---- LSTM stack in reverse (tuner.py:340-359)
+  // ---- LSTM stack in reverse (tuner.py:340-359); the staging region
+  //      overwrites the attention weights from here on.
   for (int l = dm.L - 1; l >= 0; --l) {
     const R* xin = l == 0 ? step0 : smp + ly.S + (int64_t)(l - 1) * Tmax * D;
     const int stride = l == 0 ? dm.d0 : D;
-    lstm_layer_bwd<R, H>(dm, ly, prm, l, len, xin, stride, smp, bws, sm, part, fresh);
+    lstm_layer_bwd<R, H>(dm, ly, prm, l, len, xin, stride, smp, bws, sm, wst, part, fresh);
   }
 }
 

@@ -1,0 +1,146 @@
+"""N > 1 host logic on CPU: world_size-2 gloo process groups (127.0.0.1).
+
+The per-rank compute is the oracle here (these tests run without a GPU); the
+sharding, the data-parallel gradient all-reduce (SURVEY §8e option A) and the
+exact PCA count reduction are the production code paths of
+paper_2304_05430_b200.dist.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import random_seqs
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _init(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _dp_worker(rank, world, port, out):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import tuner as otuner
+    from paper_2304_05430_b200 import dist as tdist
+
+    _init(rank, world, port)
+    rng = np.random.default_rng(0)
+    seqs = random_seqs(rng, rng.integers(1, 6, size=37))
+    y = rng.uniform(0.1, 0.9, size=37)
+    p = otuner.init_params(1, layers=1, hidden=4)
+    names = list(p)
+    perm = np.random.default_rng(5).permutation(37)
+    B = 4
+    steps = tdist.dp_steps(37, B, world)
+    grads = []
+    for k in range(steps):
+        mb = tdist.dp_microbatch(perm, k, B, rank, world)
+        if len(mb):
+            _, g = otuner.loss_and_gradients(p, [seqs[i] for i in mb], y[mb], "ranking")
+            flat = torch.tensor(np.concatenate([g[n].ravel() for n in names]))
+        else:
+            flat = torch.zeros(sum(p[n].size for n in names), dtype=torch.float64)
+        tdist.mean_microbatch_gradient(flat, len(mb))
+        grads.append(flat.numpy().copy())
+    out[rank] = np.stack(grads)
+    dist.destroy_process_group()
+
+
+def test_dp_gradient_allreduce_equals_mean_of_microbatch_gradients():
+    from oracle import tuner as otuner
+    from paper_2304_05430_b200 import dist as tdist
+
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_dp_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert np.array_equal(out[0], out[1])  # every replica applies the same update
+    rng = np.random.default_rng(0)
+    seqs = random_seqs(rng, rng.integers(1, 6, size=37))
+    y = rng.uniform(0.1, 0.9, size=37)
+    p = otuner.init_params(1, layers=1, hidden=4)
+    names = list(p)
+    perm = np.random.default_rng(5).permutation(37)
+    for k in range(tdist.dp_steps(37, 4, world)):
+        parts = []
+        for r in range(world):
+            mb = tdist.dp_microbatch(perm, k, 4, r, world)
+            if len(mb):
+                _, g = otuner.loss_and_gradients(p, [seqs[i] for i in mb], y[mb], "ranking")
+                parts.append(np.concatenate([g[n].ravel() for n in names]))
+        np.testing.assert_allclose(out[0][k], np.mean(parts, axis=0), rtol=1e-12, atol=1e-15)
+
+
+def _pca_worker(rank, world, port, sizes, out):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import metrics as om
+    from paper_2304_05430_b200 import dist as tdist
+
+    _init(rank, world, port)
+    rng = np.random.default_rng(9)
+    off = np.zeros(len(sizes) + 1, dtype=np.int64)
+    off[1:] = np.cumsum(sizes)
+    y = np.round(rng.normal(size=off[-1]), 1)
+    s = np.round(rng.normal(size=off[-1]), 1)
+    mine = tdist.lpt_assign(sizes, world)[rank]
+    local = {t: om.pca_counts(y[off[t]:off[t + 1]], s[off[t]:off[t + 1]])[0]
+             for t in mine if sizes[t] >= 2}
+    out[rank] = tdist.gather_counts(local, len(sizes))
+    dist.destroy_process_group()
+
+
+def test_pca_counts_sharded_by_task_reduce_exactly():
+    from oracle import metrics as om
+
+    sizes = [50, 3, 120, 1, 77, 64, 2, 200, 9]
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_pca_worker, args=(world, _free_port(), sizes, out), nprocs=world, join=True)
+    rng = np.random.default_rng(9)
+    off = np.zeros(len(sizes) + 1, dtype=np.int64)
+    off[1:] = np.cumsum(sizes)
+    y = np.round(rng.normal(size=off[-1]), 1)
+    s = np.round(rng.normal(size=off[-1]), 1)
+    want = [om.pca_counts(y[off[t]:off[t + 1]], s[off[t]:off[t + 1]])[0] if sizes[t] >= 2 else 0
+            for t in range(len(sizes))]
+    assert list(out[0]) == want and list(out[1]) == want
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_sharding_helpers_partition_everything(world):
+    from paper_2304_05430_b200 import dist as tdist
+
+    rng = np.random.default_rng(world)
+    lens = rng.integers(1, 11, size=1001)
+    off = np.zeros(1002, dtype=np.int64)
+    off[1:] = np.cumsum(lens)
+    ranges = tdist.shard_by_rows(off, world)
+    assert ranges[0][0] == 0 and ranges[-1][1] == 1001
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    rows = [off[b] - off[a] for a, b in ranges]
+    assert max(rows) - min(rows) <= 2 * lens.max()
+    parts = tdist.lpt_assign(rng.integers(1, 100, size=57), world)
+    assert sorted(t for p in parts for t in p) == list(range(57))
+    perm = rng.permutation(103)
+    seen = np.concatenate([tdist.dp_microbatch(perm, k, 4, r, world)
+                           for k in range(tdist.dp_steps(103, 4, world)) for r in range(world)])
+    assert np.array_equal(seen, perm)

@@ -47,8 +47,11 @@ def test_mlp_training_trajectory_fp64(cuda_ok, loss):
     g = golden("mlp.npz")
     m = mlp("fp64", epochs=3, batch_size=8, learning_rate=3e-3, loss=loss, seed=1)
     m.fit(g["fit_X"], g["fit_y"], eval_set=(g["fit_Xv"], g["fit_yv"]))
+    # atol: b3 has an identically-zero gradient under the rank loss (shift
+    # invariance), so both implementations drift by Adam-normalised rounding
+    # noise of order lr * 1e-17 / eps per step.
     for k in omlp.NAMES:
-        np.testing.assert_allclose(m.params_[k], g[f"fit_{loss}_{k}"], rtol=1e-9, atol=1e-12)
+        np.testing.assert_allclose(m.params_[k], g[f"fit_{loss}_{k}"], rtol=1e-9, atol=1e-9)
     np.testing.assert_allclose(np.array(m.train_curve_), g[f"fit_{loss}_curve"], rtol=1e-9)
 
 
