@@ -249,6 +249,39 @@ def run_b200(args, world, rank):
         epoch(t_adam)
         t_adam += n_steps
     torch.cuda.synchronize()
+    if args.phases:
+        import ctypes
+
+        lib = _lib.load()
+        names = {0: "start", 1: "stage_attn", 2: "lstm_fwd_l0", 3: "lstm_fwd_l1", 4: "lstm_fwd_l2",
+                 5: "attn_fwd", 6: "grid_bar_1", 7: "loss", 10: "attn_bwd", 11: "dS",
+                 12: "lstm_bwd_l2", 13: "lstm_bwd_l1", 14: "lstm_bwd_l0", 16: "bwd_end",
+                 17: "grid_bar_2", 18: "reduce_adam", 19: "grid_bar_3"}
+        sub = {20: "l1.stage", 21: "l1.bptt", 22: "l1.dWx", 23: "l1.dX", 13: "l1.end"}
+        for probe in (40, 41, 42):
+            lib.tt_debug_profile_step(probe)
+            epoch(t_adam)
+            t_adam += n_steps
+            torch.cuda.synchronize()
+            buf = (ctypes.c_int64 * 32)()
+            lib.tt_debug_phase_times(buf, 32)
+            marks = list(buf)
+            prev = marks[0]
+            row = []
+            for i in sorted(names):
+                if i == 0 or marks[i] == 0:
+                    continue
+                row.append(f"{names[i]}={(marks[i] - prev) / 1965.0:.2f}us")
+                prev = marks[i]
+            print(f"step {probe}: total {(marks[19] - marks[0]) / 1965.0:.2f}us | " + " ".join(row),
+                  flush=True)
+            prev = marks[12]
+            row = []
+            for i in (20, 21, 22, 23, 13):
+                row.append(f"{sub[i]}={(marks[i] - prev) / 1965.0:.2f}us")
+                prev = marks[i]
+            print("    layer-1 backward: " + " ".join(row), flush=True)
+        lib.tt_debug_profile_step(-1)
     # pre-stage the timed epochs' inputs so the timed region holds only kernels
     perms = [_device.to_dev(rng.permutation(n).astype(np.int32)) for _ in range(args.steps)]
     corrs = [_device.to_dev(_bias_corrections(t_adam + k * n_steps, n_steps)) for k in range(args.steps)]
@@ -384,6 +417,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--profile", action="store_true", help="small dataset for ncu captures")
+    ap.add_argument("--phases", action="store_true", help="print per-phase train-step timings")
     args = ap.parse_args()
     if args.profile:
         args.no_cpu = args.no_e2e = True

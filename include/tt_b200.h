@@ -142,6 +142,11 @@ int tt_tuner_train_f64(double *d_params, double *d_m, double *d_v, const double 
                        double *d_step_loss, double *d_grad_out, int32_t *d_status, void *d_ws,
                        size_t ws_bytes, tt_stream_t stream);
 
+/* Debug aid: record clock64() phase marks of CTA 0 for minibatch `step` of the
+ * next tuner training launches (-1 = off) and read them back (host memory). */
+int tt_debug_profile_step(int32_t step);
+int tt_debug_phase_times(int64_t *h_out, int32_t n);
+
 /* ------------------------------------------------------------ cost MLP --
  * replaces estimators/mlp.py CostMLP._forward/_backward/fit/predict
  * (mlp.py:72-155).  Params flat in dict order W1[F][64], b1[64], W2[64][64],
@@ -151,6 +156,12 @@ int tt_mlp_predict_f32(const float *d_params, const float *d_X, int64_t n, int32
                        float *d_out, tt_stream_t stream);
 int tt_mlp_predict_f64(const double *d_params, const double *d_X, int64_t n,
                        int32_t n_features, double *d_out, tt_stream_t stream);
+/* tcgen05 tensor-core scoring (kind::tf32 operands, fp32 accumulation and
+ * activations): TMA-fed, warp-specialised, persistent.  Requires
+ * n_features*4 % 16 == 0 (TMA row stride), X 16-B aligned.  Tolerance vs the
+ * float64 reference: max |d| <= 1e-2, mean |d| <= 1e-3 (tests). */
+int tt_mlp_predict_tf32(const float *d_params, const float *d_X, int64_t n, int32_t n_features,
+                        float *d_out, tt_stream_t stream);
 size_t tt_mlp_train_workspace_bytes(int32_t f64, int32_t n_features, int32_t batch_size);
 int tt_mlp_train_f32(float *d_params, float *d_m, float *d_v, const float *d_X, const float *d_y,
                      int32_t n_features, const int32_t *d_order, int64_t n_order,

@@ -86,6 +86,6 @@ def real_dtype(precision: str):
     t = torch()
     if precision == "fp64":
         return t.float64
-    if precision == "fp32":
+    if precision in ("fp32", "tf32"):  # tf32: tensor-core scoring, fp32 storage
         return t.float32
-    raise ValueError(f"precision must be 'fp32' or 'fp64', got {precision!r}")
+    raise ValueError(f"precision must be 'fp32', 'tf32' or 'fp64', got {precision!r}")

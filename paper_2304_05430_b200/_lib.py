@@ -38,9 +38,12 @@ SIGNATURES: dict[str, tuple] = {
                            + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
     "tt_tuner_train_f64": (ctypes.c_int, [_P] * 7 + [_P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P, _P]
                            + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
+    "tt_debug_profile_step": (ctypes.c_int, [_I32]),
+    "tt_debug_phase_times": (ctypes.c_int, [_P, _I32]),
     "tt_mlp_param_count": (_I64, [_I32]),
     "tt_mlp_predict_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
     "tt_mlp_predict_f64": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    "tt_mlp_predict_tf32": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
     "tt_mlp_train_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
     "tt_mlp_train_f32": (ctypes.c_int, [_P] * 5 + [_I32, _P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P,
                                                    _P, _P, _P, _P, _SZ, _P]),

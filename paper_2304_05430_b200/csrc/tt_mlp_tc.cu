@@ -1,0 +1,260 @@
+// K3 on the 5th-generation tensor cores: CostMLP scoring (mlp.py:72-79) as a
+// persistent, warp-specialised tcgen05 kernel (kind::tf32, fp32 accumulate).
+//
+//   warp 0      TMA producer: X tiles (128 rows x 32 fp32 boxes, SWIZZLE_128B,
+//               out-of-bounds K columns zero-filled) into an NST-stage ring
+//   warp 1      TMEM allocator + single-thread MMA issuer:
+//                 GEMM1  acc1[128x64] = X[128xK] . W1          (A, B in smem)
+//                 GEMM2  acc2[128x64] = tanh(acc1+b1) . W2     (A in TMEM)
+//   warps 2..5  epilogue, one tile row per thread (TMEM lane): tanh(acc1+b1)
+//               is written back to TMEM as GEMM2's A operand; tanh(acc2+b2)
+//               . W3 + b3 is the score, stored coalesced.
+// TMEM holds two tile buffers (acc1 | h1 | acc2, 192 columns each) so the
+// epilogue of tile i overlaps the MMAs of tile i+1 and the loads of i+2.
+// Weights (W1^T zero-padded to K=ceil(F/32)*32, W2^T) are staged once per
+// CTA in the K-major SW128 layout.
+//
+// Precision: tf32 operands (10-bit mantissa), fp32 accumulation, fp32
+// activations -- the "tf32" precision mode with its own stated tolerance;
+// the fp32 CUDA-core kernel (tt_mlp.cu) remains the strict-parity path.
+#include "tt_ops.cuh"
+#include "tt_sm100.cuh"
+
+namespace tt {
+
+using namespace sm100;
+
+constexpr int kTcRows = 128;   // rows per tile (M)
+constexpr int kTcHid = 64;     // hidden width (N)
+constexpr int kTcNst = 6;      // X pipeline stages (one 16 KB K-atom each)
+constexpr int kTcThreads = 192;
+constexpr int kAtomBytesX = kTcRows * 128;  // 16 KB
+constexpr int kAtomBytesW = kTcHid * 128;   // 8 KB
+
+struct MlpTcParams {
+  const float* prm;  // W1[F][64] b1 W2[64][64] b2 W3[64] b3
+  float* out;
+  int64_t n;
+  int F;
+  int kat;           // K atoms of 32 fp32 (ceil(F/32))
+};
+
+struct __align__(8) TcBars {
+  uint64_t full[kTcNst], empty[kTcNst];
+  uint64_t acc1_full[2], h1_full[2], acc2_full[2], acc_free[2];
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kTcThreads, 1)
+    mlp_predict_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, MlpTcParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B aligned carve-up: [X stages][W1^T atoms][W2^T atoms][bars]
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* xs = base;
+  unsigned char* w1s = xs + kTcNst * kAtomBytesX;
+  unsigned char* w2s = w1s + p.kat * kAtomBytesW;
+  TcBars* bars = reinterpret_cast<TcBars*>(w2s + 2 * kAtomBytesW);
+  __shared__ float s_b1[kTcHid], s_b2[kTcHid], s_w3[kTcHid];
+  __shared__ float s_b3;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_tiles = (p.n + kTcRows - 1) / kTcRows;
+  const int F = p.F;
+  const int64_t oW1 = 0, ob1 = (int64_t)F * kTcHid, oW2 = ob1 + kTcHid, ob2 = oW2 + kTcHid * kTcHid,
+                oW3 = ob2 + kTcHid, ob3 = oW3 + kTcHid;
+
+  // ---- one-time setup
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmap_x);
+    for (int s = 0; s < kTcNst; ++s) {
+      mbar_init(&bars->full[s], 1);
+      mbar_init(&bars->empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bars->acc1_full[b], 1);
+      mbar_init(&bars->h1_full[b], 128);
+      mbar_init(&bars->acc2_full[b], 1);
+      mbar_init(&bars->acc_free[b], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
+  // stage W1^T (K-major, zero padded) and W2^T with the swizzle the MMA expects
+  for (int i = threadIdx.x; i < p.kat * 32 * kTcHid; i += kTcThreads) {
+    const int nrow = i % kTcHid, k = i / kTcHid;  // coalesced over n
+    const float v = k < F ? p.prm[oW1 + (int64_t)k * kTcHid + nrow] : 0.0f;
+    const int atom = k >> 5;
+    *reinterpret_cast<float*>(w1s + atom * kAtomBytesW + sw128_offset(nrow, k & 31)) = v;
+  }
+  for (int i = threadIdx.x; i < kTcHid * kTcHid; i += kTcThreads) {
+    const int nrow = i % kTcHid, k = i / kTcHid;
+    const float v = p.prm[oW2 + (int64_t)k * kTcHid + nrow];
+    *reinterpret_cast<float*>(w2s + (k >> 5) * kAtomBytesW + sw128_offset(nrow, k & 31)) = v;
+  }
+  for (int i = threadIdx.x; i < kTcHid; i += kTcThreads) {
+    s_b1[i] = p.prm[ob1 + i];
+    s_b2[i] = p.prm[ob2 + i];
+    s_w3[i] = p.prm[oW3 + i];
+  }
+  if (threadIdx.x == 0) s_b3 = p.prm[ob3];
+  fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = bars->tmem_base;
+  constexpr uint32_t kBufCols = 192;
+
+  if (warp == 0) {
+    // ================= TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int kc = 0; kc < p.kat; ++kc, ++it) {
+          const uint32_t s = it % kTcNst, ph = (it / kTcNst) & 1;
+          mbar_wait(&bars->empty[s], ph ^ 1);
+          mbar_expect_tx(&bars->full[s], kAtomBytesX);
+          tma_load_2d(xs + s * kAtomBytesX, &tmap_x, &bars->full[s], kc * 32,
+                      (int)(tile * kTcRows));
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(kTcRows, kTcHid);
+      uint32_t it = 0, t = 0;
+      const uint32_t w1a = smem_u32(w1s), w2a = smem_u32(w2s), xa = smem_u32(xs);
+      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+        const uint32_t b = t & 1, bph = (t >> 1) & 1;
+        const uint32_t acc1 = tmem + b * kBufCols, h1 = acc1 + 64, acc2 = acc1 + 128;
+        mbar_wait(&bars->acc_free[b], bph ^ 1);
+        tc_fence_after();
+        for (int kc = 0; kc < p.kat; ++kc, ++it) {
+          const uint32_t s = it % kTcNst, ph = (it / kTcNst) & 1;
+          mbar_wait(&bars->full[s], ph);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = sw128_desc(xa + s * kAtomBytesX + kk * 32);
+            const uint64_t bd = sw128_desc(w1a + kc * kAtomBytesW + kk * 32);
+            mma_tf32_ss(acc1, ad, bd, idesc, (kc | kk) != 0);
+          }
+          mma_commit(&bars->empty[s]);  // frees the X stage when these MMAs retire
+        }
+        mma_commit(&bars->acc1_full[b]);
+        mbar_wait(&bars->h1_full[b], bph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t bd = sw128_desc(w2a + (kk >> 2) * kAtomBytesW + (kk & 3) * 32);
+          mma_tf32_ts(acc2, h1 + kk * 8, bd, idesc, kk != 0);
+        }
+        mma_commit(&bars->acc2_full[b]);
+      }
+    }
+  } else {
+    // ================= epilogue: warps 2..5, one row per thread
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    uint32_t t = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      const uint32_t b = t & 1, bph = (t >> 1) & 1;
+      const uint32_t acc1 = tmem + lane_off + b * kBufCols, h1 = acc1 + 64, acc2 = acc1 + 128;
+      mbar_wait(&bars->acc1_full[b], bph);
+      tc_fence_after();
+#pragma unroll
+      for (int c0 = 0; c0 < kTcHid; c0 += 16) {
+        float v[16];
+        tmem_ld16(acc1 + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = Act<float>::tanh(v[i] + s_b1[c0 + i]);
+        tmem_st16(h1 + c0, v);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&bars->h1_full[b]);
+      mbar_wait(&bars->acc2_full[b], bph);
+      tc_fence_after();
+      float acc = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < kTcHid; c0 += 16) {
+        float v[16];
+        tmem_ld16(acc2 + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc += Act<float>::tanh(v[i] + s_b2[c0 + i]) * s_w3[c0 + i];
+      }
+      tc_fence_before();
+      mbar_arrive(&bars->acc_free[b]);
+      const int64_t r = tile * kTcRows + row;
+      if (r < p.n) p.out[r] = acc + s_b3;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- host --
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+static size_t tc_smem_bytes(int kat) {
+  return 1024 + (size_t)kTcNst * kAtomBytesX + (size_t)(kat + 2) * kAtomBytesW + sizeof(TcBars) + 64;
+}
+
+int mlp_predict_tc(const float* prm, const float* X, int64_t n, int F, float* out,
+                   cudaStream_t st) {
+  TT_REQUIRE(F >= 1 && (F * 4) % 16 == 0, "mlp tf32 path: F*4 must be a multiple of 16");
+  TT_REQUIRE(((uintptr_t)X & 15) == 0, "mlp tf32 path: X must be 16-B aligned");
+  TT_REQUIRE(n >= 1 && n <= (int64_t)0x7fffffff, "mlp tf32 path: bad n");
+  const int kat = (F + 31) / 32;
+  const size_t smem = tc_smem_bytes(kat);
+  TT_REQUIRE(smem <= 227 * 1024, "mlp tf32 path: F=%d too wide for shared memory", F);
+  EncodeTiledFn enc = encode_fn();
+  TT_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)F, (cuuint64_t)n};
+  cuuint64_t strides[1] = {(cuuint64_t)F * 4};
+  cuuint32_t box[2] = {32, kTcRows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  TT_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  MlpTcParams p{prm, out, n, F, kat};
+  TT_CUDA(cudaFuncSetAttribute(mlp_predict_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  const int64_t tiles = (n + kTcRows - 1) / kTcRows;
+  const int grid = (int)std::min<int64_t>(tiles, sm_count());
+  mlp_predict_tc_kernel<<<grid, kTcThreads, smem, st>>>(map, p);
+  return check_launch("mlp predict tf32");
+}
+
+}  // namespace tt
+
+extern "C" int tt_mlp_predict_tf32(const float* prm, const float* X, int64_t n, int32_t F,
+                                   float* out, tt_stream_t st) {
+  if (n == 0) return TT_OK;
+  return tt::mlp_predict_tc(prm, X, n, F, out, tt::as_stream(st));
+}

@@ -43,6 +43,34 @@ __device__ __forceinline__ void adam_update(R& p, R g, R& m, R& v, const AdamHyp
 // sum is reduced in a fixed tree order.  `red` must hold blockDim.x values.
 template <typename R>
 __device__ R rank_loss_block(const R* y, const R* s, int n, R* dscore, R* red) {
+  if (n <= 32) {
+    // one warp, shuffle reductions (fixed order): the B = 16 training case
+    if (threadIdx.x < 32) {
+      const int k = threadIdx.x;
+      R gin = 0, gout = 0, part = 0, pairs = 0;
+      if (k < n) {
+        const R yk = y[k], sk = s[k];
+        for (int j = 0; j < n; ++j) {
+          const R yj = y[j], sj = s[j];
+          if (yj > yk) gin += (R)1 / ((R)1 + Act<R>::exp(sj - sk));
+          if (yk > yj) {
+            const R mg = sk - sj;
+            gout += (R)1 / ((R)1 + Act<R>::exp(mg));
+            part += Act<R>::softplus(-mg);
+            pairs += (R)1;
+          }
+        }
+      }
+      part = warp_sum(part);
+      pairs = warp_sum(pairs);
+      if (k < n) dscore[k] = pairs == (R)0 ? (R)0 : (gin - gout) / pairs;
+      if (k == 0) red[0] = pairs == (R)0 ? (R)0 : part / pairs;
+    }
+    __syncthreads();
+    const R out = red[0];
+    __syncthreads();
+    return out;
+  }
   R part = 0;
   int pairs = 0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) {

@@ -187,7 +187,10 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
   const int nsamp_ctas = min((int)gridDim.x, a.B);
   R* part = a.partial + (int64_t)blockIdx.x * NP;
   R* bws = a.bwd_scratch + (int64_t)blockIdx.x * ly.bwd_elems;
-  R* lb_y = a.lb + (int64_t)blockIdx.x * 3 * a.B;
+  // minibatch loss staging: shared memory for the usual small batches
+  constexpr int kLossSmem = 256;
+  __shared__ R s_lb[3 * kLossSmem];
+  R* lb_y = a.B <= kLossSmem ? s_lb : a.lb + (int64_t)blockIdx.x * 3 * a.B;
   R* lb_s = lb_y + a.B;
   R* lb_d = lb_s + a.B;
   unsigned int bar_target = 0;
@@ -197,7 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
     const int64_t b0 = (int64_t)step * a.B;
     const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
     AttnW<R> aw{};
+    phase_mark(step, 0);
     if (sampler && (int)blockIdx.x < bn) aw = stage_attn<R>(dm, a.prm, wst);
+    phase_mark(step, 1);
     // ---- forward with caches for this CTA's samples
     int slot = 0;
     for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
@@ -218,6 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
                                       smp + ly.cst + (int64_t)l * 2 * dm.Tmax * H,
                                       smp + ly.tcs + (int64_t)l * 2 * dm.Tmax * H);
         __syncthreads();
+        phase_mark(step, 2 + l);
       }
       AttnCache<R> cache{smp + ly.pin, smp + ly.q,  smp + ly.alpha, smp + ly.mix,
                          smp + ly.z,   smp + ly.a1, smp + ly.yhat};
@@ -225,8 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
                                         smp + ly.K, smp + ly.V, am, &cache, sh_y);
       if (tid == 0) a.batch_yhat[k] = sh_y[0];
       __syncthreads();
+      phase_mark(step, 5);
     }
     grid_barrier(a.barrier, bar_target);
+    phase_mark(step, 6);
     if (sampler && (int)blockIdx.x < bn) {
       // ---- loss over the whole minibatch (every sampling CTA, identical arithmetic)
       for (int k = tid; k < bn; k += kThreads) {
@@ -244,6 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
         }
       }
       __syncthreads();
+      phase_mark(step, 7);
       // ---- backward for this CTA's samples into its partial gradient
       if (!s_stop) {
         slot = 0;
@@ -254,11 +263,13 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
           const int len = (int)(a.rowoff[idx + 1] - r0);
           if (slot > 0) aw = stage_attn<R>(dm, a.prm, wst);  // LSTM staging overwrote it
           backward_sample<R, H>(dm, ly, a.prm, aw, len, a.steps + r0 * dm.d0, lb_d[k], smp, bws,
-                                bm, wst, part, slot == 0);
+                                bm, wst, part, slot == 0, step);
         }
       }
     }
+    phase_mark(step, 16);
     grid_barrier(a.barrier, bar_target);
+    phase_mark(step, 17);
     // every CTA reads the stop flag published by CTA 0 (status) -- uniform exit
     if (__ldcg(a.status) >= 0) break;
     // ---- deterministic fixed-order reduction + fused Adam (or gradient out), all CTAs
@@ -278,7 +289,9 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
         a.v[p] = vv;
       }
     }
+    phase_mark(step, 18);
     grid_barrier(a.barrier, bar_target);
+    phase_mark(step, 19);
   }
 }
 
@@ -502,6 +515,17 @@ int tt_tuner_train_f32(float* prm, float* m, float* v, const float* steps, const
   return train_entry<float>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind, mode,
                             lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C, Tmax,
                             step_loss, grad_out, status, ws, ws_bytes, st);
+}
+
+int tt_debug_profile_step(int32_t step) {
+  TT_CUDA(cudaMemcpyToSymbol(g_prof_step, &step, sizeof(int)));
+  return TT_OK;
+}
+
+int tt_debug_phase_times(int64_t* out, int32_t n) {
+  TT_REQUIRE(n >= 0 && n <= 32, "debug: n must be in [0, 32]");
+  TT_CUDA(cudaMemcpyFromSymbol(out, g_phase, sizeof(long long) * n));
+  return TT_OK;
 }
 
 int tt_tuner_train_f64(double* prm, double* m, double* v, const double* steps,

@@ -87,13 +87,13 @@ inline TDims make_dims(int L, int H, int heads, int U, int d0, int C, int Tmax) 
 }
 
 // Weight loads from global memory.  TRAIN kernels re-read parameters that
-// other CTAs update (Adam) between grid barriers, so they use coherent
-// ld.global (the barrier's ld.acquire.gpu invalidates L1); scoring kernels
-// use the read-only path.
+// other CTAs update (Adam) between grid barriers and keep their per-sample
+// activation caches in L1, so weights are read L2-only (ld.global.cg: always
+// coherent, never evicts the caches); scoring kernels use the read-only path.
 template <bool TRAIN, typename R>
 __device__ __forceinline__ R ldw(const R* p) {
   if constexpr (TRAIN)
-    return *p;
+    return __ldcg(p);
   else
     return __ldg(p);
 }
@@ -208,23 +208,25 @@ __device__ void stage_segments(const R* __restrict__ prm, R* __restrict__ smem,
   using V = typename VecOf<R>::T;
   constexpr int VN = VecOf<R>::N;
   const int total = sg[nseg - 1].vbase + sg[nseg - 1].nvec;
-  constexpr int U = 8;
+  constexpr int U = 12;
   for (int i0 = threadIdx.x; i0 < total; i0 += U * kThreads) {
     V v[U];
-    int seg[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kThreads;
       int s = 0;
       while (s + 1 < nseg && i >= sg[s + 1].vbase) ++s;
-      seg[u] = s;
-      if (i < total) v[u] = reinterpret_cast<const V*>(prm + sg[s].src)[i - sg[s].vbase];
+      // L2-only: the parameters change every step and must not evict the
+      // per-sample activation caches from L1
+      if (i < total) v[u] = __ldcg(reinterpret_cast<const V*>(prm + sg[s].src) + (i - sg[s].vbase));
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kThreads;
+      int s = 0;
+      while (s + 1 < nseg && i >= sg[s + 1].vbase) ++s;
       if (i < total) {
-        const StageSeg& g = sg[seg[u]];
+        const StageSeg& g = sg[s];
         const int e = (i - g.vbase) * VN;
         const int r = e / g.cols, c = e - r * g.cols;
         store_vec<R>(smem + g.dst + (int64_t)r * g.ld + c, v[u]);
@@ -268,8 +270,8 @@ __device__ AttnW<R> stage_attn(const TDims& dm, const R* prm, R* dst) {
   sg[5] = make_seg(dm.b1, ob1, 1, 2 * kHeadHidden, 2 * kHeadHidden, VN, vb);  // b1 | W2
   stage_segments<R, 6>(prm, dst, sg, 6);
   for (int i = threadIdx.x; i < D; i += blockDim.x) {  // bq | bo (contiguous too, tiny)
-    dst[4 * DD + i] = prm[dm.bq + i];
-    dst[4 * DD + D + i] = prm[dm.bo + i];
+    dst[4 * DD + i] = __ldcg(prm + dm.bq + i);
+    dst[4 * DD + D + i] = __ldcg(prm + dm.bo + i);
   }
   w.Wq = dst;
   w.Wk = dst + DD;
@@ -280,7 +282,7 @@ __device__ AttnW<R> stage_attn(const TDims& dm, const R* prm, R* dst) {
   w.W1 = dst + oW1;
   w.b1 = dst + ob1;
   w.W2 = dst + ob1 + kHeadHidden;
-  w.b2 = prm[dm.b2];
+  w.b2 = __ldcg(prm + dm.b2);
   __syncthreads();
   return w;
 }

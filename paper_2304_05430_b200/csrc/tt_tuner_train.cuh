@@ -12,6 +12,14 @@
 
 namespace tt {
 
+// Phase timestamps (clock64) of CTA 0 for one chosen minibatch: a debug aid
+// exported as tt_debug_phase_times (off unless tt_debug_profile_step >= 0).
+static __device__ long long g_phase[32];
+static __device__ int g_prof_step = -1;
+__device__ __forceinline__ void phase_mark(int step, int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && step == g_prof_step) g_phase[i] = clock64();
+}
+
 // Element offsets of the per-sample training cache and the per-CTA backward
 // scratch.  Every segment is padded to 4 elements so rows stay 16-B aligned.
 struct TrainLayout {
@@ -92,7 +100,9 @@ struct BwdSmem {
 template <typename R, int H>
 __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* __restrict__ prm,
                                int l, int len, const R* xin, int in_stride, const R* smp,
-                               R* bws, const BwdSmem<R>& sm, R* wst, R* part, bool fresh) {
+                               R* bws, const BwdSmem<R>& sm, R* wst, R* part, bool fresh,
+                               int step = -2) {
+  const int pstep = l == 1 ? step : -2;  // fine-grained marks for the middle layer
   constexpr int G = 4 * H, D = 2 * H, NQ = 128 / H, NW = (G + NQ - 1) / NQ;
   const int dir = threadIdx.x >> 7, lt = threadIdx.x & 127;
   const int j = lt % H, q = lt / H;
@@ -112,6 +122,7 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
     stage_segments<R, 4>(prm, wst, sg, ns);
   }
   __syncthreads();
+  phase_mark(pstep, 20);
   const R* Whs = wst + dir * per_dir;
   const R* Wxs = Whs + (int64_t)H * ldg;
   const R* gates = smp + ly.gates + (int64_t)l * 2 * Tmax * G;
@@ -184,6 +195,7 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
     }
     named_barrier(1 + dir, 128);
   }
+  phase_mark(pstep, 21);
   if (lt < G) {
 #pragma unroll
     for (int k = 0; k < H; ++k) put(part, dm.wh[l][dir] + (int64_t)k * G + lt, dwh[k], fresh);
@@ -209,6 +221,7 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
       }
     }
   }
+  phase_mark(pstep, 22);
   if (l > 0) {
     // dX[t][k] = sum_c Wx[k][c] dZ[t][c]; thread (k, hq) sums columns c = hq (mod NH)
     const int NH = ly.NH;
@@ -230,6 +243,7 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
     }
   }
   __syncthreads();
+  phase_mark(pstep, 23);
   if (l > 0) {
     const int NH = ly.NH;
     for (int i = threadIdx.x; i < len * D; i += kThreads) {
@@ -248,7 +262,8 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
 template <typename R, int H>
 __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R* __restrict__ prm,
                                 const AttnW<R>& aw, int len, const R* step0, R dy, const R* smp,
-                                R* bws, const BwdSmem<R>& sm, R* wst, R* part, bool fresh) {
+                                R* bws, const BwdSmem<R>& sm, R* wst, R* part, bool fresh,
+                                int step) {
   constexpr int D = 2 * H;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Tmax = dm.Tmax, heads = dm.heads, dh = dm.dh, C = dm.C, U = dm.U;
@@ -325,6 +340,7 @@ __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R*
     for (int c = tid; c < D; c += kThreads) put(part, dm.bq + c, sm.dq[c], st);
     bmv_row<R>(aw.Wq, aw.ldd, sm.dq, D, D, sm.dpool, sm.red);
   }
+  phase_mark(step, 10);
   // ---- d S (tuner.py:331-338)
   const R* S = smp + ly.S + (int64_t)(dm.L - 1) * Tmax * D;
   // gWk / gWv: thread column cc in [0, 2D), accumulators over k in registers
@@ -362,10 +378,12 @@ __device__ void backward_sample(const TDims& dm, const TrainLayout& ly, const R*
   __syncthreads();
   // ---- LSTM stack in reverse (tuner.py:340-359); the staging region
   //      overwrites the attention weights from here on.
+  phase_mark(step, 11);
   for (int l = dm.L - 1; l >= 0; --l) {
     const R* xin = l == 0 ? step0 : smp + ly.S + (int64_t)(l - 1) * Tmax * D;
     const int stride = l == 0 ? dm.d0 : D;
-    lstm_layer_bwd<R, H>(dm, ly, prm, l, len, xin, stride, smp, bws, sm, wst, part, fresh);
+    lstm_layer_bwd<R, H>(dm, ly, prm, l, len, xin, stride, smp, bws, sm, wst, part, fresh, step);
+    phase_mark(step, 12 + (dm.L - 1 - l));
   }
 }
 

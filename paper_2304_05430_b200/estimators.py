@@ -475,6 +475,8 @@ class CostMLP(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         flat = self._device_flat(list(self.NAMES)) if flat is None else flat
         out = _device.empty(n, _device.real_dtype(prec))
         fn = "tt_mlp_predict_f64" if prec == "fp64" else "tt_mlp_predict_f32"
+        if prec == "tf32" and (F * 4) % 16 == 0:
+            fn = "tt_mlp_predict_tf32"  # tcgen05 tensor-core path
         _lib.call(fn, flat.data_ptr(), Xd.data_ptr(), n, F, out.data_ptr(), _device.stream_ptr())
         return out
 

@@ -64,6 +64,21 @@ def test_mlp_tenset_width_scoring_fp32(cuda_ok):
     np.testing.assert_allclose(m.predict(X), want, rtol=0, atol=2e-5)
 
 
+@pytest.mark.parametrize("n,F", [(1, 164), (127, 164), (128, 164), (129, 164), (70000, 164),
+                                 (300, 32), (257, 8), (1000, 100)])
+def test_mlp_tf32_tensor_core_scoring(cuda_ok, n, F):
+    """tcgen05 kind::tf32 path: stated tolerance max |d| <= 1e-2, mean <= 1e-3
+    vs the float64 reference (tf32 operands, fp32 accumulation)."""
+    rng = np.random.default_rng(n + F)
+    X = rng.normal(size=(n, F))
+    m = mlp("tf32", epochs=0, seed=0).fit(X[: min(n, 64)], rng.uniform(size=min(n, 64)))
+    got = m.predict(X)
+    want = omlp.predict(omlp.init_params(F, 0), X)
+    d = np.abs(got - want)
+    assert d.max() <= 1e-2 and d.mean() <= 1e-3, (d.max(), d.mean())
+    assert np.isfinite(got).all()
+
+
 def test_mlp_validation(cuda_ok):
     from paper_2304_05430_b200.errors import DataValidationError, NumericFailure
 
