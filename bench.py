@@ -205,6 +205,43 @@ def flush_l2(buf):
     buf.fill_(1)
 
 
+def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
+    """CostMLP bulk scoring at TenSet width (configs[0]/[2] shape): the
+    tcgen05 tf32 kernel and the fp32 CUDA-core kernel, HBM roofline
+    (algorithmic bytes 4F + 4 per row)."""
+    import torch
+
+    from paper_2304_05430_b200 import CostMLP, _lib
+
+    g = torch.Generator(device="cuda").manual_seed(0)
+    X = torch.randn(n, F, device="cuda", generator=g)
+    est = CostMLP(epochs=0, seed=0)
+    est._init_params(F)
+    out = {}
+    for prec, fn in (("tf32", "tt_mlp_predict_tf32"), ("fp32", "tt_mlp_predict_f32")):
+        est.precision = prec
+        flat = est._device_flat(list(est.NAMES))
+        y = torch.empty(n, device="cuda")
+        for _ in range(3):
+            _lib.call(fn, flat.data_ptr(), X.data_ptr(), n, F, y.data_ptr(), stream.cuda_stream)
+        ts = []
+        for _ in range(5):
+            flush_l2(l2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _lib.call(fn, flat.data_ptr(), X.data_ptr(), n, F, y.data_ptr(), stream.cuda_stream)
+            e1.record(stream)
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        t = float(np.mean([a.elapsed_time(b) for a, b in ts])) / 1e3
+        gbs = n * (4 * F + 4) / t / 1e9
+        out[f"mlp_{prec}_rows_per_s"] = n / t
+        out[f"mlp_{prec}_hbm_gbs"] = gbs
+        out[f"mlp_{prec}_hbm_frac"] = gbs / float(peaks.get("hbm_gbs", 6552.0))
+    return out
+
+
 def run_b200(args, world, rank):
     import torch
 
@@ -238,7 +275,18 @@ def run_b200(args, world, rank):
     l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
 
+    dp = None
+    if world > 1:
+        # data parallel: every rank holds its own 64x4096 shard (weak scaling);
+        # global step = per-rank microbatch of 16 -> NCCL gradient all-reduce
+        # -> replicated fused Adam (paper_2304_05430_b200.dist)
+        from paper_2304_05430_b200.dist import DataParallelTunerEpoch
+
+        dp = DataParallelTunerEpoch(est, prog, yd, BATCH)
+
     def epoch(t0):
+        if dp is not None:
+            return dp.run(rng.permutation(n), 1e-3, local_shard=True)
         perm = _device.to_dev(rng.permutation(n).astype(np.int32))
         corr = _device.to_dev(_bias_corrections(t0, n_steps))
         return est._launch_train(dims, flat, m, v, prog, yd, perm, BATCH, _lib.TT_MODE_TRAIN, 1e-3,
@@ -249,7 +297,7 @@ def run_b200(args, world, rank):
         epoch(t_adam)
         t_adam += n_steps
     torch.cuda.synchronize()
-    if args.phases:
+    if args.phases and dp is None:
         import ctypes
 
         lib = _lib.load()
@@ -297,15 +345,19 @@ def run_b200(args, world, rank):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _, status, _ = est._launch_train(dims, flat, m, v, prog, yd, perms[k], BATCH,
-                                             _lib.TT_MODE_TRAIN, 1e-3, corrs[k], None)
+            if dp is not None:
+                dp.run(rng.permutation(n), 1e-3, local_shard=True)
+                status = None
+            else:
+                _, status, _ = est._launch_train(dims, flat, m, v, prog, yd, perms[k], BATCH,
+                                                 _lib.TT_MODE_TRAIN, 1e-3, corrs[k], None)
             e1.record(stream)
             times.append((e0, e1))
         torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
     ms = [a.elapsed_time(b) for a, b in times]
-    assert int(status.item()) < 0, "non-finite loss during the benchmark"
+    assert status is None or int(status.item()) < 0, "non-finite loss during the benchmark"
     t_mean = float(np.mean(ms)) / 1e3
     if dist is not None:
         tt = torch.tensor([t_mean], device="cuda")
@@ -382,6 +434,7 @@ def run_b200(args, world, rank):
         pairs = N_TASKS * PER_TASK * (PER_TASK - 1) / 2
         extra["pca_pairs_per_s"] = pairs / pt
         extra["pca_mean"] = float(np.mean(c / (PER_TASK * (PER_TASK - 1) / 2)))
+        extra.update(mlp_scoring(l2, stream, peaks))
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(steps, off, ctx, y)
@@ -398,7 +451,8 @@ def run_b200(args, world, rank):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps,
+            # fused path: one cooperative launch per epoch; DP: grad kernel + Adam per step
+            "gpu_launches": args.steps if dp is None else 2 * n_steps * args.steps,
             "clocks": clocks.summary(int(os.environ.get("LOCAL_RANK", 0))),
             "extra": extra,
         }

@@ -118,6 +118,7 @@ struct TrainArgs {
   R* batch_yhat;       // [B]
   R* lb;               // [3][B] loss staging (labels, scores, d/dscore) -- per CTA
   unsigned int* barrier;
+  int cache_smem;      // per-sample caches + backward scratch live in shared memory
 };
 
 template <typename R>
@@ -181,12 +182,19 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
   bm.part = sp;
   sp += 2 * NQ * H;
   bm.red = red;
+  // Per-sample forward caches and the backward scratch: shared memory when
+  // they fit (the grid barrier's acquire invalidates L1, so global-memory
+  // caches would come back from L2 on every dependent BPTT access).
+  sp = reinterpret_cast<R*>((reinterpret_cast<uintptr_t>(sp) + 31) & ~uintptr_t(31));
+  R* const cache_base = a.cache_smem ? sp
+                                     : a.sample_scratch + (int64_t)blockIdx.x * a.spc * ly.sample_elems;
 
   const int64_t NP = dm.total;
   const bool sampler = blockIdx.x < (unsigned)min((int)gridDim.x, a.B);
   const int nsamp_ctas = min((int)gridDim.x, a.B);
   R* part = a.partial + (int64_t)blockIdx.x * NP;
-  R* bws = a.bwd_scratch + (int64_t)blockIdx.x * ly.bwd_elems;
+  R* bws = a.cache_smem ? sp + (int64_t)a.spc * ly.sample_elems
+                        : a.bwd_scratch + (int64_t)blockIdx.x * ly.bwd_elems;
   // minibatch loss staging: shared memory for the usual small batches
   constexpr int kLossSmem = 256;
   __shared__ R s_lb[3 * kLossSmem];
@@ -201,13 +209,17 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
     const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
     AttnW<R> aw{};
     phase_mark(step, 0);
-    if (sampler && (int)blockIdx.x < bn) aw = stage_attn<R>(dm, a.prm, wst);
+    if (sampler && (int)blockIdx.x < bn) {
+      // labels of the whole minibatch, fetched early (used after the barrier)
+      for (int k = tid; k < bn; k += kThreads) lb_y[k] = a.y[a.order[b0 + k]];
+      aw = stage_attn<R, D>(dm, a.prm, wst);
+    }
     phase_mark(step, 1);
     // ---- forward with caches for this CTA's samples
     int slot = 0;
     for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
       const int64_t idx = a.order[b0 + k];
-      R* smp = a.sample_scratch + ((int64_t)blockIdx.x * a.spc + slot) * ly.sample_elems;
+      R* smp = cache_base + (int64_t)slot * ly.sample_elems;
       if (tid == 0) {
         const int64_t r0 = a.rowoff[idx];
         ti.len[0] = (int)(a.rowoff[idx + 1] - r0);
@@ -237,10 +249,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
     phase_mark(step, 6);
     if (sampler && (int)blockIdx.x < bn) {
       // ---- loss over the whole minibatch (every sampling CTA, identical arithmetic)
-      for (int k = tid; k < bn; k += kThreads) {
-        lb_y[k] = a.y[a.order[b0 + k]];
-        lb_s[k] = __ldcg(a.batch_yhat + k);
-      }
+      for (int k = tid; k < bn; k += kThreads) lb_s[k] = __ldcg(a.batch_yhat + k);
       __syncthreads();
       const R loss = a.loss_kind == TT_LOSS_RANK ? rank_loss_block<R>(lb_y, lb_s, bn, lb_d, red)
                                                  : mse_block<R>(lb_y, lb_s, bn, lb_d, red);
@@ -258,10 +267,10 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
         slot = 0;
         for (int k = blockIdx.x; k < bn; k += gridDim.x, ++slot) {
           const int64_t idx = a.order[b0 + k];
-          const R* smp = a.sample_scratch + ((int64_t)blockIdx.x * a.spc + slot) * ly.sample_elems;
+          const R* smp = cache_base + (int64_t)slot * ly.sample_elems;
           const int64_t r0 = a.rowoff[idx];
           const int len = (int)(a.rowoff[idx + 1] - r0);
-          if (slot > 0) aw = stage_attn<R>(dm, a.prm, wst);  // LSTM staging overwrote it
+          if (slot > 0) aw = stage_attn<R, D>(dm, a.prm, wst);  // LSTM staging overwrote it
           backward_sample<R, H>(dm, ly, a.prm, aw, len, a.steps + r0 * dm.d0, lb_d[k], smp, bws,
                                 bm, wst, part, slot == 0, step);
         }
@@ -374,7 +383,16 @@ struct Launch {
     w += align_up((size_t)grid * 3 * a.B * sizeof(R), 256);
     a.barrier = reinterpret_cast<unsigned int*>(w);
     TT_CUDA(cudaMemsetAsync(a.barrier, 0, 256, st));
-    const size_t smem = train_smem_bytes<R>(a.dm);
+    size_t smem = train_smem_bytes<R>(a.dm);
+    {
+      int dev = 0, optin = 0;
+      TT_CUDA(cudaGetDevice(&dev));
+      TT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+      const size_t cache = ((size_t)a.spc * a.ly.sample_elems + a.ly.bwd_elems) * sizeof(R) + 64;
+      const size_t static_smem = 3 * 256 * sizeof(R) + 1024;  // s_lb, TileInfo, flags
+      a.cache_smem = smem + cache + static_smem <= (size_t)optin ? 1 : 0;
+      if (a.cache_smem) smem += cache;
+    }
     auto kern = tuner_train_kernel<R, H>;
     TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;

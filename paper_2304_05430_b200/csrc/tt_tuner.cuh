@@ -159,22 +159,10 @@ struct AttnW {
 };
 
 __host__ __device__ inline int64_t attn_stage_elems(const TDims& d) {
-  const int64_t n = 4LL * d.D * (d.D + 1) + 2LL * d.D + (int64_t)(d.D + d.C) * (kHeadHidden + 1) +
-                    2LL * kHeadHidden + 1;
+  // [Wq|Wk|Wv|Wo|bq|bo] (4D+2 rows x D, ld D+1) then [W1|b1|W2] (D+C+2 rows x 64, ld 65)
+  const int64_t n = (int64_t)(4 * d.D + 2) * (d.D + 1) + (int64_t)(d.D + d.C + 2) * (kHeadHidden + 1);
   return (n + 3) & ~int64_t(3);
 }
-
-// Staging of row-major matrices from global into shared memory with a padded
-// row stride.  All segments of one phase are copied by a single flattened
-// loop of 16-B vector loads, 8 in flight per thread, so a whole phase costs
-// about one L2 round trip instead of one per element.  Requirements (hold
-// for every tensor of the parameter layout): source 16-B aligned, cols a
-// multiple of the vector width.
-struct StageSeg {
-  int64_t src;  // element offset in the parameter vector
-  int64_t dst;  // element offset in the smem region
-  int cols, ld, nvec, vbase;  // vectors in this segment, prefix count
-};
 
 template <typename R>
 struct VecOf;
@@ -202,86 +190,55 @@ __device__ __forceinline__ void store_vec(R* d, const double2& v) {
   d[1] = v.y;
 }
 
-template <typename R, int NS>
-__device__ void stage_segments(const R* __restrict__ prm, R* __restrict__ smem,
-                               const StageSeg (&sg)[NS], int nseg) {
+// Copy `rows` contiguous rows of COLS elements (16-B aligned source) into
+// shared memory with row stride `ld` (padding breaks bank conflicts of the
+// transposed accesses).  16-B vector loads, U in flight per thread, L2-only
+// (the parameters change every step; L1 keeps the activation caches); the
+// row/column split is a compile-time shift.
+template <typename R, int COLS>
+__device__ __forceinline__ void stage_rows(R* __restrict__ dst, int ld, const R* __restrict__ src,
+                                           int rows) {
   using V = typename VecOf<R>::T;
   constexpr int VN = VecOf<R>::N;
-  const int total = sg[nseg - 1].vbase + sg[nseg - 1].nvec;
-  constexpr int U = 12;
+  constexpr int VPR = COLS / VN;
+  static_assert(COLS % VN == 0, "row width must be a multiple of the vector width");
+  const int total = rows * VPR;
+  const V* s = reinterpret_cast<const V*>(src);
+  constexpr int U = 8;
   for (int i0 = threadIdx.x; i0 < total; i0 += U * kThreads) {
     V v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kThreads;
-      int s = 0;
-      while (s + 1 < nseg && i >= sg[s + 1].vbase) ++s;
-      // L2-only: the parameters change every step and must not evict the
-      // per-sample activation caches from L1
-      if (i < total) v[u] = __ldcg(reinterpret_cast<const V*>(prm + sg[s].src) + (i - sg[s].vbase));
+      if (i < total) v[u] = __ldcg(s + i);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i = i0 + u * kThreads;
-      int s = 0;
-      while (s + 1 < nseg && i >= sg[s + 1].vbase) ++s;
-      if (i < total) {
-        const StageSeg& g = sg[s];
-        const int e = (i - g.vbase) * VN;
-        const int r = e / g.cols, c = e - r * g.cols;
-        store_vec<R>(smem + g.dst + (int64_t)r * g.ld + c, v[u]);
-      }
+      if (i < total) store_vec<R>(dst + (i / VPR) * ld + (i % VPR) * VN, v[u]);
     }
   }
 }
 
-__host__ __device__ inline StageSeg make_seg(int64_t src, int64_t dst, int rows, int cols, int ld,
-                                             int vn, int& vbase) {
-  StageSeg s;
-  s.src = src;
-  s.dst = dst;
-  s.cols = cols;
-  s.ld = ld;
-  s.nvec = rows * cols / vn;
-  s.vbase = vbase;
-  vbase += s.nvec;
-  return s;
-}
-
-// All threads; ends with __syncthreads.  Layout: Wq Wk Wv Wo [D][D+1],
-// bq bo [D], W1 [D+C][65], b1 W2 [64].
-template <typename R>
+// All threads; ends with __syncthreads.  The parameter layout keeps
+// Wq,Wk,Wv,Wo,bq,bo and W1,b1,W2 contiguous, so two block copies suffice.
+template <typename R, int D>
 __device__ AttnW<R> stage_attn(const TDims& dm, const R* prm, R* dst) {
-  constexpr int VN = VecOf<R>::N;
-  const int D = dm.D;
   AttnW<R> w;
   w.ldd = D + 1;
   w.ld1 = kHeadHidden + 1;
-  const int64_t DD = (int64_t)D * w.ldd;
-  const int64_t oW1 = 4 * DD + 2 * D;
-  const int64_t ob1 = oW1 + (int64_t)(D + dm.C) * w.ld1;
-  StageSeg sg[6];
-  int vb = 0;
-  sg[0] = make_seg(dm.Wq, 0, D, D, w.ldd, VN, vb);
-  sg[1] = make_seg(dm.Wk, DD, D, D, w.ldd, VN, vb);
-  sg[2] = make_seg(dm.Wv, 2 * DD, D, D, w.ldd, VN, vb);
-  sg[3] = make_seg(dm.Wo, 3 * DD, D, D, w.ldd, VN, vb);
-  sg[4] = make_seg(dm.W1, oW1, D + dm.C, kHeadHidden, w.ld1, VN, vb);
-  sg[5] = make_seg(dm.b1, ob1, 1, 2 * kHeadHidden, 2 * kHeadHidden, VN, vb);  // b1 | W2
-  stage_segments<R, 6>(prm, dst, sg, 6);
-  for (int i = threadIdx.x; i < D; i += blockDim.x) {  // bq | bo (contiguous too, tiny)
-    dst[4 * DD + i] = __ldcg(prm + dm.bq + i);
-    dst[4 * DD + D + i] = __ldcg(prm + dm.bo + i);
-  }
+  R* d2 = dst + (int64_t)(4 * D + 2) * w.ldd;
+  stage_rows<R, D>(dst, w.ldd, prm + dm.Wq, 4 * D + 2);
+  stage_rows<R, kHeadHidden>(d2, w.ld1, prm + dm.W1, D + dm.C + 2);
   w.Wq = dst;
-  w.Wk = dst + DD;
-  w.Wv = dst + 2 * DD;
-  w.Wo = dst + 3 * DD;
-  w.bq = dst + 4 * DD;
-  w.bo = dst + 4 * DD + D;
-  w.W1 = dst + oW1;
-  w.b1 = dst + ob1;
-  w.W2 = dst + ob1 + kHeadHidden;
+  w.Wk = dst + D * w.ldd;
+  w.Wv = dst + 2 * D * w.ldd;
+  w.Wo = dst + 3 * D * w.ldd;
+  w.bq = dst + 4 * D * w.ldd;
+  w.bo = dst + (4 * D + 1) * w.ldd;
+  w.W1 = d2;
+  w.b1 = d2 + (int64_t)(D + dm.C) * w.ld1;
+  w.W2 = d2 + (int64_t)(D + dm.C + 1) * w.ld1;
   w.b2 = __ldcg(prm + dm.b2);
   __syncthreads();
   return w;

@@ -67,7 +67,8 @@ inline TrainLayout make_train_layout(const TDims& d) {
 
 // smem elements for one layer's staged LSTM weights (both directions)
 __host__ __device__ inline int64_t lstm_stage_elems(const TDims& d) {
-  const int64_t per_dir = (int64_t)(d.D + d.H) * (d.G + 1);  // layers >= 1 (layer 0 stages Wh only)
+  // layers >= 1: 2 x [Wx | Wh | b] rows (D + H + 1); layer 0 stages Wh only
+  const int64_t per_dir = (int64_t)(d.D + d.H + 1) * (d.G + 1);
   const int64_t l0 = (int64_t)d.H * (d.G + 1);
   const int64_t n = 2 * (per_dir > l0 ? per_dir : l0);
   return (n + 3) & ~int64_t(3);
@@ -109,22 +110,27 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
   const int Tmax = dm.Tmax;
   const int ldg = G + 1;
   const int d_in = l == 0 ? dm.d0 : D;
-  // ---- stage both directions' Wh (and Wx for l > 0) into shared memory
-  const int64_t per_dir = (int64_t)(l == 0 ? H : D + H) * ldg;
-  {
-    StageSeg sg[4];
-    int vb = 0, ns = 0;
-    constexpr int VN = VecOf<R>::N;
-    for (int d = 0; d < 2; ++d) {
-      sg[ns++] = make_seg(dm.wh[l][d], d * per_dir, H, G, ldg, VN, vb);
-      if (l > 0) sg[ns++] = make_seg(dm.wx[l][d], d * per_dir + (int64_t)H * ldg, D, G, ldg, VN, vb);
-    }
-    stage_segments<R, 4>(prm, wst, sg, ns);
+  // ---- stage the layer's weights into shared memory.  In the parameter
+  // layout a direction is [Wx | Wh | b] and the bw block follows the fw one,
+  // so layers >= 1 are one contiguous block of 2*(D+H+1) rows; layer 0 only
+  // needs Wh (its dX is discarded, dWx does not read Wx).
+  int64_t per_dir;
+  const R* Whs;
+  const R* Wxs;
+  if (l > 0) {
+    per_dir = (int64_t)(D + H + 1) * ldg;
+    stage_rows<R, G>(wst, ldg, prm + dm.wx[l][0], 2 * (D + H + 1));
+    Wxs = wst + dir * per_dir;
+    Whs = Wxs + (int64_t)D * ldg;
+  } else {
+    per_dir = (int64_t)H * ldg;
+    stage_rows<R, G>(wst, ldg, prm + dm.wh[0][0], H);
+    stage_rows<R, G>(wst + per_dir, ldg, prm + dm.wh[0][1], H);
+    Whs = wst + dir * per_dir;
+    Wxs = nullptr;
   }
   __syncthreads();
   phase_mark(pstep, 20);
-  const R* Whs = wst + dir * per_dir;
-  const R* Wxs = Whs + (int64_t)H * ldg;
   const R* gates = smp + ly.gates + (int64_t)l * 2 * Tmax * G;
   const R* cst = smp + ly.cst + (int64_t)l * 2 * Tmax * H;
   const R* tcs = smp + ly.tcs + (int64_t)l * 2 * Tmax * H;
@@ -223,24 +229,19 @@ __device__ void lstm_layer_bwd(const TDims& dm, const TrainLayout& ly, const R* 
   }
   phase_mark(pstep, 22);
   if (l > 0) {
-    // dX[t][k] = sum_c Wx[k][c] dZ[t][c]; thread (k, hq) sums columns c = hq (mod NH)
-    const int NH = ly.NH;
+    // dX[t][k] = sum_c Wx[k][c] dZ[t][c]; thread (k, hq) owns the contiguous
+    // column slice [hq*CW, (hq+1)*CW) of row k in registers and streams the
+    // dZ rows as broadcast vector loads.
+    constexpr int NHc = 128 / D;          // column groups (== ly.NH)
+    constexpr int CW = G / NHc;           // columns per group
     const int k = lt % D, hq = lt / D;
-    if (hq < NH) {
-      R* dX = bws + ly.dX + ((int64_t)(dir * NH + hq) * Tmax) * D;
-      const R* wr = Wxs + (int64_t)k * ldg;
-      for (int t = 0; t < len; ++t) {
-        const R* dzt = dZ + (int64_t)t * G;
-        R a0 = 0, a1 = 0;
-        int c = hq;
-        for (; c + NH < G; c += 2 * NH) {
-          a0 += wr[c] * dzt[c];
-          a1 += wr[c + NH] * dzt[c + NH];
-        }
-        if (c < G) a0 += wr[c] * dzt[c];
-        dX[(int64_t)t * D + k] = a0 + a1;
-      }
-    }
+    R wr[CW];
+    const R* wrow = Wxs + (int64_t)k * ldg + hq * CW;
+#pragma unroll
+    for (int c = 0; c < CW; ++c) wr[c] = wrow[c];
+    R* dX = bws + ly.dX + ((int64_t)(dir * NHc + hq) * Tmax) * D;
+    for (int t = 0; t < len; ++t)
+      dX[(int64_t)t * D + k] = dot_reg<CW>(dZ + (int64_t)t * G + hq * CW, wr);
   }
   __syncthreads();
   phase_mark(pstep, 23);

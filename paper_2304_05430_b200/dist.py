@@ -69,6 +69,68 @@ def mean_microbatch_gradient(grad, n_local: int, group=None):
     return grad
 
 
+class DataParallelTunerEpoch:
+    """One data-parallel training epoch of a RecurrentAttentionTuner replica.
+
+    Per global step k: the rank's microbatch (dp_microbatch) runs the fused
+    kernel in gradient mode (forward, rank/MSE loss, backward, fixed-order
+    per-sample reduction), the flat fp32 gradient (330 KB for the default
+    tuner) is all-reduced over NCCL, and the standalone fused Adam kernel
+    applies the identical update on every replica.
+    """
+
+    def __init__(self, est, prog, y_dev, batch: int, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _device
+
+        self.est, self.prog, self.y, self.B, self.group = est, prog, y_dev, batch, group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.dims = est._dims()
+        self.flat = est._dev_params(self.dims).clone()
+        self.m = torch.zeros_like(self.flat)
+        self.v = torch.zeros_like(self.flat)
+        self.t = 0
+        self._dev = _device
+
+    def run(self, perm: np.ndarray, lr: float, local_shard: bool = False) -> int:
+        """Train over `perm`; returns the number of global steps taken.
+
+        local_shard=False: `perm` is the global permutation (identical on every
+        rank) and rank r takes slice r of each global minibatch.
+        local_shard=True: every rank holds its own data shard and `perm` is a
+        permutation of it; global step k uses each rank's k-th local slice."""
+        import torch
+
+        from . import _lib
+        from .estimators import _BETA1, _BETA2, _EPS
+
+        n = len(perm)
+        perm_dev = self._dev.to_dev(np.asarray(perm, dtype=np.int32))
+        steps = (n + self.B - 1) // self.B if local_shard else dp_steps(n, self.B, self.world)
+        stream = self._dev.stream_ptr()
+        for k in range(steps):
+            lo = k * self.B if local_shard else k * self.world * self.B + self.rank * self.B
+            cnt = max(0, min(self.B, n - lo))
+            if cnt > 0:
+                order = perm_dev[lo: lo + cnt]
+                _, _, grad = self.est._launch_train(self.dims, self.flat, None, None, self.prog,
+                                                    self.y, order, cnt, _lib.TT_MODE_GRAD, 0.0,
+                                                    None, None)
+            else:
+                grad = torch.zeros_like(self.flat)
+            mean_microbatch_gradient(grad, cnt, self.group)
+            self.t += 1
+            c1 = 1.0 - _BETA1**self.t
+            c2 = 1.0 - _BETA2**self.t
+            _lib.call("tt_adam_step_f32" if self.flat.dtype == torch.float32 else "tt_adam_step_f64",
+                      self.flat.data_ptr(), grad.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                      self.flat.numel(), None, lr, _BETA1, _BETA2, _EPS, c1, c2, stream)
+        return steps
+
+
 def gather_counts(local_counts: dict, n_tasks: int, group=None) -> np.ndarray:
     """Combine per-task int64 counts computed on disjoint task sets."""
     import torch
