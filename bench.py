@@ -156,12 +156,14 @@ def cpu_baseline(steps, off, ctx, y, seconds=CPU_SAMPLE_SECONDS):
     p = otuner.init_params(0)
     opt = AdamOracle(p, 1e-3)
     perm = np.random.default_rng(1).permutation(len(seqs))
+    n_full = max(1, len(seqs) // BATCH)  # wrap around the sample's minibatches
     ctxm = threadpool_limits(1) if threadpool_limits else None
     done = 0
     t0 = time.perf_counter()
     k = 0
     while time.perf_counter() - t0 < seconds:
-        b = perm[k * BATCH:(k + 1) * BATCH]
+        j = k % n_full
+        b = perm[j * BATCH:(j + 1) * BATCH]
         _, g = otuner.loss_and_gradients(p, [seqs[i] for i in b], y[b], "ranking")
         opt.step(g)
         done += len(b)
