@@ -244,6 +244,49 @@ def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
     return out
 
 
+def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam):
+    """Per-phase marks of one minibatch inside the train kernel (CTA 0 clock64
+    at 1965 MHz; the first gradient-job CTA in %globaltimer ns)."""
+    import ctypes
+
+    import torch
+
+    from paper_2304_05430_b200 import _device, _lib
+    from paper_2304_05430_b200.estimators import _bias_corrections
+
+    lib = _lib.load()
+    names = {0: "start", 1: "adam_wait", 2: "fwd_l0", 3: "fwd_l1", 4: "fwd_l2", 5: "attn_fwd",
+             6: "yhat_xchg", 7: "loss", 10: "attn_bwd+dS", 11: "bptt_l2", 12: "dX_l2",
+             13: "bptt_l1", 14: "dX_l1", 15: "bptt_l0", 16: "bwd_end"}
+    for probe in (40, 41, 42):
+        lib.tt_debug_profile_step(probe)
+        buf0 = (ctypes.c_int64 * 32)()
+        ctypes.memmove(buf0, (ctypes.c_int64 * 32)(), 32 * 8)
+        perm = _device.to_dev(rng.permutation(n).astype(np.int32))
+        corr = _device.to_dev(_bias_corrections(t_adam, n_steps))
+        est._launch_train(dims, flat, m, v, prog, yd, perm, BATCH, _lib.TT_MODE_TRAIN, 1e-3, corr, None)
+        t_adam += n_steps
+        torch.cuda.synchronize()
+        buf = (ctypes.c_int64 * 32)()
+        lib.tt_debug_phase_times(buf, 32)
+        mk = list(buf)
+        prev = mk[0]
+        row = []
+        for i in sorted(names):
+            if i == 0 or mk[i] == 0 or mk[i] < prev:
+                continue
+            row.append(f"{names[i]}={(mk[i] - prev) / 1965.0:.2f}")
+            prev = mk[i]
+        last = max(i for i in names if mk[i] >= mk[0] and mk[i] != 0)
+        jobs = ""
+        if mk[20] and mk[30]:
+            jobs = (f" | job CTA: start-after-cta0-bwd={(mk[20] - mk[30]) / 1e3:.2f}us "
+                    f"jobs={(mk[21] - mk[20]) / 1e3:.2f}us")
+        print(f"step {probe}: cta0 {(mk[last] - mk[0]) / 1965.0:.2f}us | " + " ".join(row) + jobs,
+              flush=True)
+    lib.tt_debug_profile_step(-1)
+
+
 def run_b200(args, world, rank):
     import torch
 
@@ -300,38 +343,8 @@ def run_b200(args, world, rank):
         t_adam += n_steps
     torch.cuda.synchronize()
     if args.phases and dp is None:
-        import ctypes
-
-        lib = _lib.load()
-        names = {0: "start", 1: "stage_attn", 2: "lstm_fwd_l0", 3: "lstm_fwd_l1", 4: "lstm_fwd_l2",
-                 5: "attn_fwd", 6: "grid_bar_1", 7: "loss", 10: "attn_bwd", 11: "dS",
-                 12: "lstm_bwd_l2", 13: "lstm_bwd_l1", 14: "lstm_bwd_l0", 16: "bwd_end",
-                 17: "grid_bar_2", 18: "reduce_adam", 19: "grid_bar_3"}
-        sub = {20: "l1.stage", 21: "l1.bptt", 22: "l1.dWx", 23: "l1.dX", 13: "l1.end"}
-        for probe in (40, 41, 42):
-            lib.tt_debug_profile_step(probe)
-            epoch(t_adam)
-            t_adam += n_steps
-            torch.cuda.synchronize()
-            buf = (ctypes.c_int64 * 32)()
-            lib.tt_debug_phase_times(buf, 32)
-            marks = list(buf)
-            prev = marks[0]
-            row = []
-            for i in sorted(names):
-                if i == 0 or marks[i] == 0:
-                    continue
-                row.append(f"{names[i]}={(marks[i] - prev) / 1965.0:.2f}us")
-                prev = marks[i]
-            print(f"step {probe}: total {(marks[19] - marks[0]) / 1965.0:.2f}us | " + " ".join(row),
-                  flush=True)
-            prev = marks[12]
-            row = []
-            for i in (20, 21, 22, 23, 13):
-                row.append(f"{sub[i]}={(marks[i] - prev) / 1965.0:.2f}us")
-                prev = marks[i]
-            print("    layer-1 backward: " + " ".join(row), flush=True)
-        lib.tt_debug_profile_step(-1)
+        print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam)
+        t_adam += 3 * n_steps
     # pre-stage the timed epochs' inputs so the timed region holds only kernels
     perms = [_device.to_dev(rng.permutation(n).astype(np.int32)) for _ in range(args.steps)]
     corrs = [_device.to_dev(_bias_corrections(t_adam + k * n_steps, n_steps)) for k in range(args.steps)]

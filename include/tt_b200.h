@@ -142,6 +142,12 @@ int tt_tuner_train_f64(double *d_params, double *d_m, double *d_v, const double 
                        double *d_step_loss, double *d_grad_out, int32_t *d_status, void *d_ws,
                        size_t ws_bytes, tt_stream_t stream);
 
+/* Kernel selection for tt_tuner_train_f32: 0 = automatic (the latency-path
+ * kernel when hidden = 32, batch <= #SMs and the per-sample caches fit in
+ * shared memory, else the generic kernel), 1 = generic only, 2 = latency path
+ * only (TT_EINVAL when not eligible).  Process-wide; for tests and benches. */
+int tt_tuner_train_set_path(int32_t path);
+
 /* Debug aid: record clock64() phase marks of CTA 0 for minibatch `step` of the
  * next tuner training launches (-1 = off) and read them back (host memory). */
 int tt_debug_profile_step(int32_t step);

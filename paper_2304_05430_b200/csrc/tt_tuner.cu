@@ -1,9 +1,13 @@
 // Attention tuner kernels: bulk scoring (K5) and the fused training step
 // (K5 cached forward + K7 loss + K6 backward + deterministic reduction + K8
 // Adam) -- see tt_tuner.cuh / tt_tuner_train.cuh for the per-block code.
-#include "tt_tuner_train.cuh"
+#include <type_traits>
+
+#include "tt_tuner_fast.cuh"
 
 namespace tt {
+
+static int g_train_path = 0;  // 0 auto, 1 generic kernel only, 2 fast kernel only (tests)
 
 template <typename R>
 struct ScoreP {
@@ -404,6 +408,37 @@ struct Launch {
   }
 
   static int train(TrainArgs<R> a, void* ws, size_t ws_bytes, cudaStream_t st) {
+    if constexpr (std::is_same<R, float>::value) {
+      // v4 latency path (tt_tuner_fast.cuh) when eligible, else the generic kernel
+      FastPlan fp;
+      const bool ok = g_train_path != 1 && fast_plan(a.dm, a.B, sm_count(), fp) &&
+                      ws_bytes >= fast_ws_bytes(a.dm, a.B);
+      if (ok) {
+        FastArgs f{};
+        f.dm = a.dm;
+        f.prm = a.prm;
+        f.m = a.m;
+        f.v = a.v;
+        f.steps = a.steps;
+        f.rowoff = a.rowoff;
+        f.ctx = a.ctx;
+        f.y = a.y;
+        f.order = a.order;
+        f.n_order = a.n_order;
+        f.B = a.B;
+        f.loss_kind = a.loss_kind;
+        f.mode = a.mode;
+        f.n_steps = a.n_steps;
+        f.hyp = a.hyp;
+        f.corr = a.corr;
+        f.trainable = a.trainable;
+        f.step_loss = a.step_loss;
+        f.grad_out = a.grad_out;
+        f.status = a.status;
+        return fast_launch(f, fp, ws, st);
+      }
+      TT_REQUIRE(g_train_path != 2, "tuner train: fast path requested but not eligible");
+    }
     switch (a.dm.H) {
       case 4: return train_h<4>(a, ws, ws_bytes, st);
       case 8: return train_h<8>(a, ws, ws_bytes, st);
@@ -520,7 +555,8 @@ size_t tt_tuner_train_workspace_bytes(int32_t f64, int32_t L, int32_t H, int32_t
   // heads/unroll only size small cache segments; use generous upper bounds
   big.heads = 2 * H;
   big.U = 16;
-  return f64 ? Launch<double>::train_ws(big, B) : Launch<float>::train_ws(big, B);
+  if (f64) return Launch<double>::train_ws(big, B);
+  return std::max(Launch<float>::train_ws(big, B), fast_ws_bytes(big, B));
 }
 
 int tt_tuner_train_f32(float* prm, float* m, float* v, const float* steps, const int64_t* rowoff,
@@ -533,6 +569,12 @@ int tt_tuner_train_f32(float* prm, float* m, float* v, const float* steps, const
   return train_entry<float>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind, mode,
                             lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C, Tmax,
                             step_loss, grad_out, status, ws, ws_bytes, st);
+}
+
+int tt_tuner_train_set_path(int32_t path) {
+  TT_REQUIRE(path >= 0 && path <= 2, "train path must be 0 (auto), 1 (generic) or 2 (fast)");
+  g_train_path = path;
+  return TT_OK;
 }
 
 int tt_debug_profile_step(int32_t step) {

@@ -1,0 +1,152 @@
+"""The two tuner training kernels behind tt_tuner_train_f32:
+
+* the v4 latency path (csrc/tt_tuner_fast.cuh): hidden 32, batch <= #SMs,
+  per-sample caches in shared memory, weight gradients reduced by
+  parameter-slice jobs;
+* the generic kernel (csrc/tt_tuner.cu tuner_train_kernel): any hidden size,
+  per-CTA partial gradients.
+
+Both are checked against the float64 oracle (oracle/tuner.py, pinned to the
+reference goldens) and against each other.  Tolerances as test_gpu_tuner.py:
+fp32 loss rel 1e-5, gradients relative-norm 1e-4 per tensor, trajectories in
+norm (Adam amplifies fp32 noise on near-zero gradient entries).
+"""
+
+from __future__ import annotations
+
+import contextlib
+
+import numpy as np
+import pytest
+
+from conftest import random_seqs, relative_gradient_error
+from oracle import tuner as otuner
+
+pytestmark = pytest.mark.gpu
+
+
+@contextlib.contextmanager
+def train_path(path: int):
+    from paper_2304_05430_b200 import _lib
+
+    _lib.call("tt_tuner_train_set_path", path)
+    try:
+        yield
+    finally:
+        _lib.call("tt_tuner_train_set_path", 0)
+
+
+def make(**kw):
+    from paper_2304_05430_b200 import RecurrentAttentionTuner
+
+    m = RecurrentAttentionTuner(**kw)
+    m.precision = "fp32"
+    return m
+
+
+def _grads(m, seqs, y):
+    loss, g = m.loss_and_gradients(seqs, y)
+    return loss, g
+
+
+@pytest.mark.parametrize("loss", ["rmse", "ranking"])
+def test_fast_and_generic_gradients_match_oracle(cuda_ok, loss):
+    rng = np.random.default_rng(41)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=16))
+    y = rng.uniform(0.1, 0.9, size=16)
+    m = make(epochs=0, seed=4, loss=loss).fit(seqs, y)
+    p = otuner.init_params(4)
+    want_l, want = otuner.loss_and_gradients(p, seqs, y, loss)
+    out = {}
+    for path in (1, 2):
+        with train_path(path):
+            l, g = _grads(m, seqs, y)
+        assert l == pytest.approx(want_l, rel=1e-5), path
+        assert relative_gradient_error(g, want) <= 1e-4, path
+        out[path] = g
+    assert relative_gradient_error(out[2], out[1]) <= 1e-4
+
+
+def test_fast_path_odd_batches(cuda_ok):
+    """Batch sizes that leave most CTAs as gradient jobs, single sample,
+    length-1 programs, and the maximum step count the smem plan admits."""
+    rng = np.random.default_rng(8)
+    p = otuner.init_params(6)
+    for lens in ([1], [1, 1, 1], [3, 12, 1, 7, 2], list(rng.integers(1, 13, size=33))):
+        seqs = random_seqs(rng, lens)
+        y = rng.uniform(0.1, 0.9, size=len(seqs))
+        m = make(epochs=0, seed=6, loss="ranking").fit(seqs, y)
+        with train_path(2):
+            l, g = _grads(m, seqs, y)
+        want_l, want = otuner.loss_and_gradients(p, seqs, y, "ranking")
+        assert l == pytest.approx(want_l, rel=1e-5, abs=1e-7)
+        if want_l > 0:
+            assert relative_gradient_error(g, want) <= 1e-4, lens
+
+
+def test_fast_path_tenset_width(cuda_ok):
+    """164-wide step rows (the tuner is width-generic)."""
+    rng = np.random.default_rng(2)
+    seqs = random_seqs(rng, rng.integers(1, 9, size=12), d0=164)
+    y = rng.uniform(0.1, 0.9, size=12)
+    p = otuner.init_params(1, d0=164)
+    m = make(epochs=0, seed=1, loss="ranking")
+    m.set_weights(p)
+    np.testing.assert_allclose(m.predict(seqs), otuner.predict(p, seqs), rtol=0, atol=1e-5)
+    with train_path(2):
+        l, g = _grads(m, seqs, y)
+    want_l, want = otuner.loss_and_gradients(p, seqs, y, "ranking")
+    assert l == pytest.approx(want_l, rel=1e-5)
+    assert relative_gradient_error(g, want) <= 1e-4
+
+
+@pytest.mark.parametrize("loss", ["rmse", "ranking"])
+def test_fast_path_trajectory_with_partial_batch(cuda_ok, loss):
+    rng = np.random.default_rng(13)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=37))  # 2 x 16 + 5
+    y = rng.uniform(0.1, 0.9, size=37)
+    with train_path(2):
+        m = make(epochs=2, batch_size=16, loss=loss, seed=3).fit(seqs, y)
+    p = otuner.init_params(3)
+    curve = otuner.train(p, seqs, y, epochs=2, lr=1e-3, batch_size=16, seed=3, loss=loss)
+    np.testing.assert_allclose([c[0] for c in m.train_curve_], [c[0] for c in curve], rtol=1e-3)
+    for k in p:
+        err = np.linalg.norm(m.params_[k] - p[k]) / max(np.linalg.norm(p[k]), 1e-12)
+        assert err <= 2e-3, (k, err)
+
+
+def test_fast_path_frozen_groups_and_refit(cuda_ok):
+    rng = np.random.default_rng(17)
+    seqs = random_seqs(rng, rng.integers(1, 9, size=48))
+    y = rng.uniform(0.1, 0.9, size=48)
+    with train_path(2):
+        a = make(epochs=1, batch_size=16, loss="ranking", seed=5).fit(seqs, y)
+        b = make(epochs=1, batch_size=16, loss="ranking", seed=5).fit(seqs, y)
+        for k in a.params_:
+            assert np.array_equal(a.params_[k], b.params_[k]), k  # deterministic reduction
+        groups = a.param_groups()
+        heads = set(groups["attention"]) | set(groups["head"])
+        before = {k: v.copy() for k, v in a.params_.items()}
+        a.continue_fit(seqs, y, epochs=1, learning_rate=1e-3, trainable=heads)
+    changed = 0
+    for k, v in a.params_.items():
+        if k in heads:
+            changed += int(not np.array_equal(v, before[k]))
+        else:
+            assert np.array_equal(v, before[k]), k
+    assert changed > 0
+
+
+def test_fast_and_generic_epochs_agree(cuda_ok):
+    rng = np.random.default_rng(23)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=96))
+    y = rng.uniform(0.1, 0.9, size=96)
+    res = {}
+    for path in (1, 2):
+        with train_path(path):
+            res[path] = make(epochs=2, batch_size=16, loss="ranking", seed=8).fit(seqs, y)
+    np.testing.assert_allclose([c[0] for c in res[1].train_curve_],
+                               [c[0] for c in res[2].train_curve_], rtol=1e-4)
+    for k in res[1].params_:
+        a, b = res[1].params_[k], res[2].params_[k]
+        assert np.linalg.norm(a - b) <= 1e-3 * max(np.linalg.norm(a), 1e-12), k
