@@ -281,8 +281,11 @@ def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam):
         jobs = ""
         if mk[20] and mk[30]:
             jobs = (f" | job CTA: start-after-cta0-bwd={(mk[20] - mk[30]) / 1e3:.2f}us "
-                    f"jobs={(mk[21] - mk[20]) / 1e3:.2f}us")
-        print(f"step {probe}: cta0 {(mk[last] - mk[0]) / 1965.0:.2f}us | " + " ".join(row) + jobs,
+                    f"stage={(mk[22] - mk[20]) / 1e3:.2f} compute={(mk[23] - mk[22]) / 1e3:.2f} "
+                    f"adam+signal={(mk[21] - mk[23]) / 1e3:.2f}us")
+        proj = " proj=" + ",".join(f"{(mk[25 + l] - mk[1 + l] if l == 0 else mk[25 + l] - mk[1 + l]) / 1965.0:.2f}"
+                                  for l in range(3) if mk[25 + l])
+        print(f"step {probe}: cta0 {(mk[last] - mk[0]) / 1965.0:.2f}us | " + " ".join(row) + proj + jobs,
               flush=True)
     lib.tt_debug_profile_step(-1)
 

@@ -33,15 +33,20 @@ namespace tt {
 
 constexpr int kFH = 32, kFD = 64, kFG = 128;  // hidden, 2H, 4H
 constexpr int kLdA = 65;                       // staged attention weights row stride
+constexpr int kMaxFastB = 160;                 // minibatch limit of the latency path
+
+__host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
 
 // ------------------------------------------------------------ layouts --
 struct FastSmem {  // float offsets in dynamic shared memory (sample role)
-  int64_t S, gc, cs, xz, hb, K, V, alpha, pin, q, mix, pool, zb, a1, red, lb, dS, dS2, dZ, dK,
+  int64_t x0, lbn, S, gc, cs, xz, hb, gex, K, V, alpha, pin, q, mix, pool, zb, a1, red, lb, dS, dS2, dZ, dK,
       dV, dlg, dmix, dq, dpool, da1, W, total;
 };
 
-struct FastXch {  // float offsets inside one exchange slot
-  int64_t S, dZ, dK, dV, pin, mix, dpool, dq, z, a1, da1, dl, total;
+struct FastXch {  // float offsets in the (stacked) exchange region
+  int64_t Rmax;
+  int w0, zw;
+  int64_t x0, H, cst, S, dZ, dK, dV, pin, mix, dpool, dq, z, a1, da1, dl, total;
 };
 
 inline FastSmem make_fast_smem(const TDims& d, int B) {
@@ -53,11 +58,14 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
     return at;
   };
   const int TM = d.Tmax;
+  s.x0 = seg((int64_t)TM * round4(d.d0));
+  s.lbn = seg(B);
   s.S = seg((int64_t)d.L * TM * kFD);
   s.gc = seg((int64_t)d.L * 2 * TM * kFG);
   s.cs = seg((int64_t)d.L * 2 * TM * kFH);
   s.xz = seg((int64_t)2 * TM * kFG);  // also the dX partials [4][TM][64]
-  s.hb = seg(2 * 2 * kFH);
+  s.hb = seg(2 * 2 * 2 * kFH);   // [dir][warp copy][parity][32] hidden state
+  s.gex = seg(2 * 2 * 2 * 2 * kFH);  // [dir][warp][parity][64] gate / dh exchange
   s.K = seg((int64_t)TM * kFD);
   s.V = seg((int64_t)TM * kFD);
   s.alpha = seg((int64_t)d.U * d.heads * TM);
@@ -67,7 +75,7 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   s.pool = seg(kFD);
   s.zb = seg(kFD + d.C);
   s.a1 = seg(kHeadHidden);
-  s.red = seg(kThreads);
+  s.red = seg(std::max(kThreads, 2 * B));
   s.lb = seg((int64_t)3 * B);
   s.dS = seg((int64_t)TM * kFD);
   s.dS2 = seg((int64_t)TM * kFD);
@@ -85,7 +93,11 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   return s;
 }
 
-inline FastXch make_fast_xch(const TDims& d) {
+// The exchange is STACKED by minibatch row: sample k's step rows occupy rows
+// [rs_k, rs_k + T_k) of every per-step matrix (rs_k = sum of the earlier
+// samples' step counts), its per-sample vectors row k (or k*U + u).  A
+// gradient job then stages each operand with one flat copy loop.
+inline FastXch make_fast_xch(const TDims& d, int B) {
   FastXch x{};
   int64_t o = 0;
   auto seg = [&](int64_t n) {
@@ -93,19 +105,25 @@ inline FastXch make_fast_xch(const TDims& d) {
     o += pad4(n);
     return at;
   };
-  const int TM = d.Tmax;
-  x.S = seg((int64_t)d.L * TM * kFD);
-  x.dZ = seg((int64_t)d.L * 2 * TM * kFG);
-  x.dK = seg((int64_t)TM * kFD);
-  x.dV = seg((int64_t)TM * kFD);
-  x.pin = seg((int64_t)d.U * kFD);
-  x.mix = seg((int64_t)d.U * kFD);
-  x.dpool = seg((int64_t)d.U * kFD);
-  x.dq = seg((int64_t)d.U * kFD);
-  x.z = seg(kFD + d.C);
-  x.a1 = seg(kHeadHidden);
-  x.da1 = seg(kHeadHidden);
-  x.dl = seg(1);
+  x.Rmax = (int64_t)B * d.Tmax;
+  x.w0 = round4(d.d0);
+  x.zw = round4(kFD + d.C);
+  const int64_t R = x.Rmax;
+  x.x0 = seg(R * x.w0);                       // raw step rows, zero padded
+  x.S = seg((int64_t)d.L * R * kFD);          // layer outputs
+  x.H = seg((int64_t)d.L * 2 * R * kFH);      // h_prev per direction (0 at its first step)
+  x.dZ = seg((int64_t)d.L * 2 * R * kFG);     // gate pre-activation gradients
+  x.dK = seg(R * kFD);
+  x.dV = seg(R * kFD);
+  x.pin = seg((int64_t)B * d.U * kFD);
+  x.mix = seg((int64_t)B * d.U * kFD);
+  x.dpool = seg((int64_t)B * d.U * kFD);
+  x.dq = seg((int64_t)B * d.U * kFD);
+  x.z = seg((int64_t)B * x.zw);               // [pooled | ctx], zero padded
+  x.a1 = seg((int64_t)B * kHeadHidden);
+  x.da1 = seg((int64_t)B * kHeadHidden);
+  x.dl = seg((int64_t)B * 4);                 // [dl, 0, 0, 0]
+  x.cst = seg(8);                             // [0 0 0 0 | 1 0 0 0]
   x.total = o;
   return x;
 }
@@ -137,18 +155,45 @@ __host__ __device__ inline FastJob fast_job(const TDims& d, int j) {
   return FastJob{FJ_W2, 0, 0, 0, 1};
 }
 
-// A-operand width of a job (including the ones column when the slice has a bias)
-__device__ inline int fast_job_ka(const TDims& d, const FastJob& jb, bool& has_bias) {
-  switch (jb.kind) {
-    case FJ_LSTM: has_bias = true; return (jb.l == 0 ? d.d0 : kFD) + kFH + 1;
-    case FJ_WQ: case FJ_WO: has_bias = true; return kFD + 1;
-    case FJ_WK: case FJ_WV: has_bias = false; return kFD;
-    case FJ_W1: has_bias = true; return kFD + d.C + 1;
-    default: has_bias = true; return kHeadHidden + 1;  // W2 | b2
-  }
-}
+// A-operand geometry of a job: segment 1 (n1 real columns padded to w1),
+// optional segment 2 (n2 columns: the LSTM h_prev rows), then the ones column
+// when the slice has a bias.  A column k maps to parameter row
+//   k < n1 -> k ;  w1 <= k < w1 + n2 -> n1 + k - w1 ;  k == w1 + n2 -> bias
+// (the LSTM block [Wx; Wh; b] is contiguous in the parameter layout).
+struct JobGeo {
+  int n1, w1, n2, ka, kap, nbp, maxr;
+  bool bias;
+  int64_t base, ldp, bptr;
+};
 
-__host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
+__device__ inline JobGeo job_geo(const TDims& d, const FastJob& jb) {
+  JobGeo g{};
+  g.n2 = 0;
+  g.bias = true;
+  g.ldp = kFD;
+  g.maxr = 1;
+  switch (jb.kind) {
+    case FJ_LSTM:
+      g.n1 = jb.l == 0 ? d.d0 : kFD;
+      g.n2 = kFH;
+      g.base = d.wx[jb.l][jb.dir];
+      g.ldp = kFG;
+      g.bptr = d.bb[jb.l][jb.dir];
+      g.maxr = d.Tmax;
+      break;
+    case FJ_WQ: g.n1 = kFD; g.base = d.Wq; g.bptr = d.bq; g.maxr = d.U; break;
+    case FJ_WO: g.n1 = kFD; g.base = d.Wo; g.bptr = d.bo; g.maxr = d.U; break;
+    case FJ_WK: g.n1 = kFD; g.base = d.Wk; g.bias = false; g.bptr = -1; g.maxr = d.Tmax; break;
+    case FJ_WV: g.n1 = kFD; g.base = d.Wv; g.bias = false; g.bptr = -1; g.maxr = d.Tmax; break;
+    case FJ_W1: g.n1 = kFD + d.C; g.base = d.W1; g.ldp = kHeadHidden; g.bptr = d.b1; break;
+    default: g.n1 = kHeadHidden; g.base = d.W2; g.ldp = 1; g.bptr = d.b2; break;
+  }
+  g.w1 = round4(g.n1);
+  g.ka = g.w1 + g.n2 + (g.bias ? 1 : 0);
+  g.kap = round4(g.ka);
+  g.nbp = round4(jb.nb);
+  return g;
+}
 
 // smem floats a job needs for `rows` staged rows (plus the reduction area)
 __host__ __device__ inline int64_t fast_job_smem(int kap, int nbp, int rows) {
@@ -179,8 +224,8 @@ struct FastArgs {
   float* step_loss;
   float* grad_out;
   int32_t* status;
-  float* xch;          // [B][xl.total]
-  int64_t* meta;       // [B][2]: row offset, steps
+  float* xch;          // stacked exchange (FastXch)
+  int64_t* meta;       // [B]: steps of each minibatch slot
   float* yhat_buf;     // [B]
   unsigned int* ctr;   // [0] fwd, [1] bwd, [2] adam (monotone)
   int n_jobs;
@@ -208,7 +253,7 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void wait_counter(const unsigned* ctr, unsigned target, bool sleep) {
   if (threadIdx.x == 0) {
     while (ld_acquire(ctr) < target) {
-      if (sleep) __nanosleep(64);
+      if (sleep) __nanosleep(100);
     }
   }
   __syncthreads();
@@ -227,93 +272,134 @@ __device__ __forceinline__ void cp_async4(float* s, const float* g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(g) : "memory");
 }
 __device__ __forceinline__ void cp_async16(float* s, const float* g) {
+#ifdef TT_SYNC_STAGE
+  *reinterpret_cast<float4*>(s) = __ldcg(reinterpret_cast<const float4*>(g));
+#else
   const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ------------------------------------------------------ recurrences --
-// Forward recurrence of one direction on one warp.  Lane j: hidden unit j,
-// gate columns {j, 32+j, 64+j, 96+j} of Wh in registers (128 floats).
-// xz: [2][TM][128] input projections (bias included).  Writes the layer
-// output rows S[t][dir*32 + j] (smem + exchange), gates and cell state.
-__device__ __forceinline__ void fast_rec_fwd(int dir, int T, int TM, const float* __restrict__ Wh,
-                                             const float* xz, float* S, float* Sg, float* gc,
-                                             float* cs, float* hb) {
+// Each direction's recurrence runs on a PAIR of warps (dir d: warps 2d and
+// 2d+1, one per SM sub-partition); warp `sub` of the pair owns gate blocks
+// {2 sub, 2 sub + 1} ([i|f] or [g|o]), i.e. 64 of the 128 columns, so a
+// lane keeps 64 weights in registers.  One named barrier (id 2 + d, 64
+// threads) per time step exchanges the gate values (forward) or the dh
+// partial sums (backward); buffers alternate by step parity.
+using WReg = float[64];
+
+// Lane j of warp `sub`: Wh[k][(2 sub + q)*32 + j] -> w[q*32 + k].
+__device__ __forceinline__ void load_wh_cols(WReg& w, const float* __restrict__ Wh, int sub) {
   const int j = threadIdx.x & 31;
-  float w[4][kFH];
 #pragma unroll
   for (int k = 0; k < kFH; ++k)
 #pragma unroll
-    for (int g = 0; g < 4; ++g) w[g][k] = __ldcg(Wh + k * kFG + g * kFH + j);
-  float c = 0.f;
-  float* h0 = hb + dir * 2 * kFH;
-  h0[j] = 0.f;
-  __syncwarp();
-  int cur = 0;
-  for (int s = 0; s < T; ++s) {
-    const int t = dir == 0 ? s : T - 1 - s;
-    const float* xr = xz + ((int64_t)dir * TM + t) * kFG;
-    float a[4][2];
+    for (int q = 0; q < 2; ++q) w[q * kFH + k] = __ldcg(Wh + k * kFG + (2 * sub + q) * kFH + j);
+}
+
+// Lane j of warp `sub`: Wh[j][sub*64 + c] for c < 64 (half of row j).
+__device__ __forceinline__ void load_wh_row(WReg& w, const float* __restrict__ Wh, int sub) {
+  const int j = threadIdx.x & 31;
+  const float4* w4 = reinterpret_cast<const float4*>(Wh + (int64_t)j * kFG + sub * 64);
 #pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      a[g][0] = xr[g * kFH + j];
-      a[g][1] = 0.f;
-    }
-    const float4* h4 = reinterpret_cast<const float4*>(h0 + cur * kFH);
-#pragma unroll
-    for (int m = 0; m < kFH / 4; ++m) {
-      const float4 hv = h4[m];
-#pragma unroll
-      for (int g = 0; g < 4; ++g) {
-        a[g][m & 1] = fmaf(hv.x, w[g][4 * m + 0], a[g][m & 1]);
-        a[g][m & 1] = fmaf(hv.y, w[g][4 * m + 1], a[g][m & 1]);
-        a[g][m & 1] = fmaf(hv.z, w[g][4 * m + 2], a[g][m & 1]);
-        a[g][m & 1] = fmaf(hv.w, w[g][4 * m + 3], a[g][m & 1]);
-      }
-    }
-    const float gi = Act<float>::sigmoid(a[0][0] + a[0][1]);
-    const float gf = Act<float>::sigmoid(a[1][0] + a[1][1]);
-    const float gg = Act<float>::tanh(a[2][0] + a[2][1]);
-    const float go = Act<float>::sigmoid(a[3][0] + a[3][1]);
-    c = gf * c + gi * gg;
-    const float h = go * Act<float>::tanh(c);
-    h0[(cur ^ 1) * kFH + j] = h;
-    S[(int64_t)t * kFD + dir * kFH + j] = h;
-    Sg[(int64_t)t * kFD + dir * kFH + j] = h;
-    float* gr = gc + ((int64_t)dir * TM + t) * kFG;
-    gr[j] = gi;
-    gr[kFH + j] = gf;
-    gr[2 * kFH + j] = gg;
-    gr[3 * kFH + j] = go;
-    cs[((int64_t)dir * TM + t) * kFH + j] = c;
-    __syncwarp();
-    cur ^= 1;
+  for (int m = 0; m < 16; ++m) {
+    const float4 v = __ldcg(w4 + m);
+    w[4 * m + 0] = v.x;
+    w[4 * m + 1] = v.y;
+    w[4 * m + 2] = v.z;
+    w[4 * m + 3] = v.w;
   }
 }
 
-// BPTT of one direction on one warp (tuner.py:113-148 restricted to the
-// valid steps).  Lane j owns row j of Wh (128 floats) for dh = dZ Wh^T.
-// dS: [TM][64] upstream gradient of this layer's output.  Writes dZ rows
-// (smem [2][TM][128] and the exchange slot).
-__device__ __forceinline__ void fast_rec_bwd(int dir, int T, int TM, const float* __restrict__ Wh,
-                                             const float* gc, const float* cs, const float* dS,
-                                             float* dZ, float* dZg) {
+// Forward recurrence, warp `sub` of direction `dir`.  xz: [2][TM][128]
+// input projections (bias included).  Both warps form c and h identically
+// (each keeps its own copy of h for its next matvec); warp 0 of the pair
+// writes the layer output row S[t][dir*32 + j] (smem + exchange) and the
+// cell state, each warp its two gate blocks.
+__device__ __forceinline__ void fast_rec_fwd(const WReg& w, int dir, int sub, int T, int TM,
+                                             const float* xz, float* S, float* Sg, float* Hg,
+                                             float* gc, float* cs, float* hb, float* gex) {
   const int j = threadIdx.x & 31;
-  float wr[kFG];
-  const float4* w4 = reinterpret_cast<const float4*>(Wh + (int64_t)j * kFG);
+  float c = 0.f;
+  float* hm = hb + (dir * 2 + sub) * 2 * kFH;          // [parity][32]
+  float* gx_me = gex + (dir * 2 + sub) * 2 * 2 * kFH;  // [parity][64]
+  const float* gx_ot = gex + (dir * 2 + (sub ^ 1)) * 2 * 2 * kFH;
+  hm[j] = 0.f;
+  __syncwarp();
+  for (int s = 0; s < T; ++s) {
+    const int par = s & 1;
+    const int t = dir == 0 ? s : T - 1 - s;
+    const float* xr = xz + ((int64_t)dir * TM + t) * kFG + 2 * sub * kFH;
+    float a00 = xr[j], a01 = 0.f, a10 = xr[kFH + j], a11 = 0.f;
+    const float4* h4 = reinterpret_cast<const float4*>(hm + par * kFH);
 #pragma unroll
-  for (int m = 0; m < kFG / 4; ++m) {
-    const float4 v = __ldcg(w4 + m);
-    wr[4 * m + 0] = v.x;
-    wr[4 * m + 1] = v.y;
-    wr[4 * m + 2] = v.z;
-    wr[4 * m + 3] = v.w;
+    for (int m = 0; m < kFH / 4; m += 2) {
+      const float4 u = h4[m], v = h4[m + 1];
+      a00 = fmaf(u.x, w[4 * m + 0], a00);
+      a10 = fmaf(u.x, w[kFH + 4 * m + 0], a10);
+      a01 = fmaf(v.x, w[4 * m + 4], a01);
+      a11 = fmaf(v.x, w[kFH + 4 * m + 4], a11);
+      a00 = fmaf(u.y, w[4 * m + 1], a00);
+      a10 = fmaf(u.y, w[kFH + 4 * m + 1], a10);
+      a01 = fmaf(v.y, w[4 * m + 5], a01);
+      a11 = fmaf(v.y, w[kFH + 4 * m + 5], a11);
+      a00 = fmaf(u.z, w[4 * m + 2], a00);
+      a10 = fmaf(u.z, w[kFH + 4 * m + 2], a10);
+      a01 = fmaf(v.z, w[4 * m + 6], a01);
+      a11 = fmaf(v.z, w[kFH + 4 * m + 6], a11);
+      a00 = fmaf(u.w, w[4 * m + 3], a00);
+      a10 = fmaf(u.w, w[kFH + 4 * m + 3], a10);
+      a01 = fmaf(v.w, w[4 * m + 7], a01);
+      a11 = fmaf(v.w, w[kFH + 4 * m + 7], a11);
+    }
+    const float z0 = a00 + a01, z1 = a10 + a11;
+    // sub 0: (i, f) = sigmoid; sub 1: g = tanh, o = sigmoid
+    const float v0 = sub == 0 ? Act<float>::sigmoid(z0) : Act<float>::tanh(z0);
+    const float v1 = Act<float>::sigmoid(z1);
+    float* gr = gc + ((int64_t)dir * TM + t) * kFG + 2 * sub * kFH;
+    gr[j] = v0;
+    gr[kFH + j] = v1;
+    gx_me[par * 2 * kFH + j] = v0;
+    gx_me[par * 2 * kFH + kFH + j] = v1;
+    named_barrier(2 + dir, 64);
+    const float o0 = gx_ot[par * 2 * kFH + j], o1 = gx_ot[par * 2 * kFH + kFH + j];
+    const float gi = sub == 0 ? v0 : o0, gf = sub == 0 ? v1 : o1;
+    const float gg = sub == 0 ? o0 : v0, go = sub == 0 ? o1 : v1;
+    c = gf * c + gi * gg;
+    const float h = go * Act<float>::tanh(c);
+    hm[(par ^ 1) * kFH + j] = h;
+    if (sub == 0) {
+      S[(int64_t)t * kFD + dir * kFH + j] = h;
+      Sg[(int64_t)t * kFD + dir * kFH + j] = h;
+      cs[((int64_t)dir * TM + t) * kFH + j] = c;
+    } else {
+      // h_prev rows of the stacked exchange, in the direction's order
+      if (s == 0) Hg[(int64_t)t * kFH + j] = 0.f;
+      if (s + 1 < T) Hg[(int64_t)(dir == 0 ? t + 1 : t - 1) * kFH + j] = h;
+    }
+    __syncwarp();
   }
+}
+
+// BPTT (tuner.py:113-148 restricted to the valid steps), warp `sub` of
+// direction `dir`: both warps form the elementwise gate gradients
+// identically; warp `sub` publishes dZ for its gate blocks and the partial
+// dh_j = sum_{c in its half} Wh[j][c] dz[c]; the two partials are summed in
+// fixed order after the step's named barrier.  dS: [TM][64] upstream
+// gradient of this layer's output.
+__device__ __forceinline__ void fast_rec_bwd(const WReg& wr, int dir, int sub, int T, int TM,
+                                             const float* gc, const float* cs, const float* dS,
+                                             float* dZ, float* dZg, float* gex) {
+  // dZg: this direction's stacked dZ rows of the sample (row t at t*128)
+  const int j = threadIdx.x & 31;
+  float* px = gex + dir * 2 * 2 * kFH;  // [warp][parity][32]
   float dh = 0.f, dc = 0.f;
   for (int s = 0; s < T; ++s) {
+    const int par = s & 1;
     // reverse of the direction's forward order
     const int t = dir == 0 ? T - 1 - s : s;
     const bool has_prev = s < T - 1;
@@ -326,42 +412,55 @@ __device__ __forceinline__ void fast_rec_bwd(int dir, int T, int TM, const float
     const float dht = dS[(int64_t)t * kFD + dir * kFH + j] + dh;
     const float dO = dht * tc;
     const float dcr = dc + dht * go * (1.f - tc * tc);
-    const float dzi = dcr * gg * gi * (1.f - gi);
-    const float dzf = dcr * cp * gf * (1.f - gf);
-    const float dzg = dcr * gi * (1.f - gg * gg);
-    const float dzo = dO * go * (1.f - go);
+    const float d0 = sub == 0 ? dcr * gg * gi * (1.f - gi) : dcr * gi * (1.f - gg * gg);
+    const float d1 = sub == 0 ? dcr * cp * gf * (1.f - gf) : dO * go * (1.f - go);
     dc = dcr * gf;
-    float* zr = dZ + ((int64_t)dir * TM + t) * kFG;
-    float* zg = dZg + ((int64_t)dir * TM + t) * kFG;
-    zr[j] = dzi;
-    zr[kFH + j] = dzf;
-    zr[2 * kFH + j] = dzg;
-    zr[3 * kFH + j] = dzo;
-    zg[j] = dzi;
-    zg[kFH + j] = dzf;
-    zg[2 * kFH + j] = dzg;
-    zg[3 * kFH + j] = dzo;
-    __syncwarp();
+    float* zr = dZ + ((int64_t)dir * TM + t) * kFG + 2 * sub * kFH;
+    float* zg = dZg + (int64_t)t * kFG + 2 * sub * kFH;
+    zr[j] = d0;
+    zr[kFH + j] = d1;
+    zg[j] = d0;
+    zg[kFH + j] = d1;
     if (has_prev) {
+      __syncwarp();
       const float4* z4 = reinterpret_cast<const float4*>(zr);
       float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-      for (int m = 0; m < kFG / 4; ++m) {
+      for (int m = 0; m < 16; ++m) {
         const float4 zv = z4[m];
         a0 = fmaf(zv.x, wr[4 * m + 0], a0);
         a1 = fmaf(zv.y, wr[4 * m + 1], a1);
         a2 = fmaf(zv.z, wr[4 * m + 2], a2);
         a3 = fmaf(zv.w, wr[4 * m + 3], a3);
       }
-      dh = (a0 + a1) + (a2 + a3);
+      px[(sub * 2 + par) * kFH + j] = (a0 + a1) + (a2 + a3);
+      named_barrier(2 + dir, 64);
+      dh = px[(0 * 2 + par) * kFH + j] + px[(1 * 2 + par) * kFH + j];
     }
   }
 }
 
+// dot(x[0:64], w[OFF:OFF+64]) with x a 16-B aligned smem row
+template <int OFF>
+__device__ __forceinline__ float dot64(const float* __restrict__ x, const float (&w)[64 + OFF]) {
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const float4 v = x4[k];
+    a0 = fmaf(v.x, w[OFF + 4 * k + 0], a0);
+    a1 = fmaf(v.y, w[OFF + 4 * k + 1], a1);
+    a2 = fmaf(v.z, w[OFF + 4 * k + 2], a2);
+    a3 = fmaf(v.w, w[OFF + 4 * k + 3], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
 // ------------------------------------------------- sample forward --
 // All 256 threads.  Returns yhat (valid in every thread after the call).
-__device__ float fast_sample_fwd(const FastArgs& a, float* sm, float* xs, int64_t r0, int T,
-                                 int64_t idx, int step) {
+// rs: this sample's first row in the stacked exchange; slot: its minibatch slot.
+__device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int slot, int64_t r0,
+                                 int T, int64_t idx, int step) {
   const TDims& dm = a.dm;
   const FastSmem& L = a.sl;
   const FastXch& X = a.xl;
@@ -372,71 +471,84 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, float* xs, int64_
   float* W = sm + L.W;
   float* W1s = W + (4 * kFD + 2) * kLdA;
   for (int l = 0; l < dm.L; ++l) {
-    // ---- input projection xz[dir][t][c] = b[c] + x_t Wx[:, c]
+    // ---- warps 0..3 fetch their Wh gate columns for this layer, then all
+    //      threads form the input projection xz[dir][t][c] = b[c] + x_t Wx[:, c]
+    //      (thread = column), overlapping the two L2 round trips.
     {
+      // ---- input projection xz[dir][t][c] = b[c] + x_t Wx[:, c], thread = column
       const int dir = tid >> 7, c = tid & 127;
-      const float* Wx = a.prm + dm.wx[l][dir];
+      const float* Wx = a.prm + dm.wx[l][dir] + c;
       const float bc = __ldcg(a.prm + dm.bb[l][dir] + c);
       float* xzr = xz + (int64_t)dir * TM * kFG + c;
       if (l == 0) {
-        const float* x0 = a.steps + r0 * dm.d0;
-        for (int t = 0; t < T; ++t) xzr[(int64_t)t * kFG] = bc;
-        for (int k0 = 0; k0 < dm.d0; k0 += 8) {
+        // raw rows staged in smem at the step start (zero padded to w0)
+        const int w0 = round4(dm.d0);
+        const float* x0 = sm + L.x0;
+        for (int k0 = 0; k0 < w0; k0 += 8) {
           float wk[8];
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            wk[kk] = k0 + kk < dm.d0 ? __ldcg(Wx + (int64_t)(k0 + kk) * kFG + c) : 0.f;
+            wk[kk] = k0 + kk < dm.d0 ? __ldcg(Wx + (int64_t)(k0 + kk) * kFG) : 0.f;
           for (int t = 0; t < T; ++t) {
-            float acc = xzr[(int64_t)t * kFG];
+            float acc = k0 == 0 ? bc : xzr[(int64_t)t * kFG];
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)
-              if (k0 + kk < dm.d0) acc = fmaf(__ldg(x0 + (int64_t)t * dm.d0 + k0 + kk), wk[kk], acc);
+              if (k0 + kk < w0) acc = fmaf(x0[t * w0 + k0 + kk], wk[kk], acc);
             xzr[(int64_t)t * kFG] = acc;
           }
         }
       } else {
-        float wk[kFD];
+        float wx[kFD];
 #pragma unroll
-        for (int k = 0; k < kFD; ++k) wk[k] = __ldcg(Wx + (int64_t)k * kFG + c);
+        for (int k = 0; k < kFD; ++k) wx[k] = __ldcg(Wx + (int64_t)k * kFG);
         const float* xin = S + (int64_t)(l - 1) * TM * kFD;
-        for (int t = 0; t < T; ++t) xzr[(int64_t)t * kFG] = dot_reg<kFD>(xin + (int64_t)t * kFD, wk) + bc;
+        for (int t = 0; t < T; ++t) xzr[(int64_t)t * kFG] = dot64<0>(xin + (int64_t)t * kFD, wx) + bc;
       }
     }
-    __syncthreads();
-    if (warp < 2) {
-      fast_rec_fwd(warp, T, TM, a.prm + dm.wh[l][warp], xz, S + (int64_t)l * TM * kFD,
-                   xs + X.S + (int64_t)l * TM * kFD, sm + L.gc + (int64_t)l * 2 * TM * kFG,
-                   sm + L.cs + (int64_t)l * 2 * TM * kFH, sm + L.hb);
+    if (warp < 4) {
+      WReg wh;
+      load_wh_cols(wh, a.prm + dm.wh[l][warp >> 1], warp & 1);
+      named_barrier(1, kThreads);  // projection done
+      if (warp == 0) phase_mark(step, 25 + l);
+      const int dir = warp >> 1;
+      fast_rec_fwd(wh, dir, warp & 1, T, TM, xz, S + (int64_t)l * TM * kFD,
+                   a.xch + X.S + ((int64_t)l * X.Rmax + rs) * kFD,
+                   a.xch + X.H + (((int64_t)l * 2 + dir) * X.Rmax + rs) * kFH,
+                   sm + L.gc + (int64_t)l * 2 * TM * kFG, sm + L.cs + (int64_t)l * 2 * TM * kFH,
+                   sm + L.hb, sm + L.gex);
       if (warp == 0) phase_mark(step, 2 + l);
-    } else if (l == 0) {
-      // idle warps stage the attention/head weights (changed by the last Adam step)
-      const int t2 = tid - 64, n2 = kThreads - 64;
+    } else {
+      named_barrier(1, kThreads);
+      if (l == 0) {
+        // idle warps stage the attention/head weights (changed by the last Adam step)
+      const int t2 = tid - 128, n2 = kThreads - 128;
       const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
       const float* src1 = a.prm + dm.Wq;
       const float* src2 = a.prm + dm.W1;
       const int tot1 = rows1 * (kFD / 4), tot2 = rows2 * (kHeadHidden / 4);
-      for (int i0 = t2; i0 < tot1 + tot2; i0 += 4 * n2) {
-        float4 v[4];
+      for (int i0 = t2; i0 < tot1 + tot2; i0 += 8 * n2) {
+        float4 v[8];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u * n2;
-          if (i < tot1)
-            v[u] = __ldcg(reinterpret_cast<const float4*>(src1) + i);
-          else if (i < tot1 + tot2)
-            v[u] = __ldcg(reinterpret_cast<const float4*>(src2) + (i - tot1));
+        for (int u = 0; u < 8; ++u) {
+          const int ii = i0 + u * n2;
+          if (ii < tot1)
+            v[u] = __ldcg(reinterpret_cast<const float4*>(src1) + ii);
+          else if (ii < tot1 + tot2)
+            v[u] = __ldcg(reinterpret_cast<const float4*>(src2) + (ii - tot1));
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int i = i0 + u * n2;
-          if (i < tot1) {
-            float* d = W + (i >> 4) * kLdA + (i & 15) * 4;
+        for (int u = 0; u < 8; ++u) {
+          const int ii = i0 + u * n2;
+          if (ii < tot1) {
+            float* d = W + (ii >> 4) * kLdA + (ii & 15) * 4;
             d[0] = v[u].x, d[1] = v[u].y, d[2] = v[u].z, d[3] = v[u].w;
-          } else if (i < tot1 + tot2) {
-            const int ii = i - tot1;
-            float* d = W1s + (ii >> 4) * kLdA + (ii & 15) * 4;
+          } else if (ii < tot1 + tot2) {
+            const int i2 = ii - tot1;
+            float* d = W1s + (i2 >> 4) * kLdA + (i2 & 15) * 4;
             d[0] = v[u].x, d[1] = v[u].y, d[2] = v[u].z, d[3] = v[u].w;
           }
         }
+      }
       }
     }
     __syncthreads();
@@ -474,13 +586,14 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, float* xs, int64_
   }
   __syncthreads();
   const float sq = sqrtf((float)dh);
-  float* xsg = xs;
+  float* const xpin = a.xch + X.pin + (int64_t)slot * U * kFD;
+  float* const xmix = a.xch + X.mix + (int64_t)slot * U * kFD;
   for (int u = 0; u < U; ++u) {
     float* q = sm + L.q + u * kFD;
     bmv_col<float>(pool, Wq, kLdA, kFD, kFD, bq, q, red);
     if (tid < kFD) {
       sm[L.pin + u * kFD + tid] = pool[tid];
-      xsg[X.pin + u * kFD + tid] = pool[tid];
+      xpin[u * kFD + tid] = pool[tid];
     }
     float* al = sm + L.alpha + (int64_t)u * heads * TM;
     for (int h = warp; h < heads; h += kThreads / 32) {
@@ -512,16 +625,16 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, float* xs, int64_
       float acc = 0.f;
       for (int t = 0; t < T; ++t) acc += ar[t] * V[(int64_t)t * kFD + tid];
       mix[tid] = acc;
-      xsg[X.mix + u * kFD + tid] = acc;
+      xmix[u * kFD + tid] = acc;
     }
     __syncthreads();
     bmv_col<float>(mix, Wo, kLdA, kFD, kFD, bo, pool, red);
   }
   float* zb = sm + L.zb;
-  for (int i = tid; i < Z; i += kThreads) {
-    const float vz = i < kFD ? pool[i] : __ldg(a.ctx + idx * dm.C + (i - kFD));
-    zb[i] = vz;
-    xsg[X.z + i] = vz;
+  for (int i = tid; i < round4(Z); i += kThreads) {
+    const float vz = i < kFD ? pool[i] : (i < Z ? __ldg(a.ctx + idx * dm.C + (i - kFD)) : 0.f);
+    if (i < Z) zb[i] = vz;
+    a.xch[X.z + (int64_t)slot * X.zw + i] = vz;
   }
   __syncthreads();
   float* a1 = sm + L.a1;
@@ -532,7 +645,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, float* xs, int64_
     for (int c = lane; c < kHeadHidden; c += 32) {
       const float av = Act<float>::tanh(a1[c]);
       a1[c] = av;
-      xsg[X.a1 + c] = av;
+      a.xch[X.a1 + (int64_t)slot * kHeadHidden + c] = av;
       acc += av * W2[c];
     }
     acc = warp_sum(acc);
@@ -544,9 +657,43 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, float* xs, int64_
   return yh;
 }
 
+// Next-minibatch metadata of this CTA (kernel-wide shared state).
+__shared__ int64_t s_nmeta[3];
+__shared__ int s_pref;
+__shared__ int s_T[kMaxFastB], s_Tn[kMaxFastB];
+
+// Warp 7 during the first BPTT layer: fetch the next minibatch's step counts,
+// labels and this CTA's slot metadata into shared memory (none depends on
+// the parameters) and warm L2 with the next program's step rows and context,
+// so the next forward does not start with dependent DRAM round trips.
+__device__ __forceinline__ void prefetch_next_sample(const FastArgs& a, int step, float* lbn) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nb0 = (int64_t)(step + 1) * a.B;
+  if (step + 1 >= a.n_steps || nb0 + blockIdx.x >= a.n_order) return;
+  const int bnn = (int)(a.n_order - nb0 < (int64_t)a.B ? a.n_order - nb0 : (int64_t)a.B);
+  for (int i = lane; i < bnn; i += 32) {
+    const int64_t idx = a.order[nb0 + i];
+    const int64_t r0 = a.rowoff[idx], r1 = a.rowoff[idx + 1];
+    lbn[i] = a.y[idx];
+    s_Tn[i] = (int)(r1 - r0);
+    if (i == (int)blockIdx.x) {
+      s_nmeta[0] = idx;
+      s_nmeta[1] = r0;
+      s_nmeta[2] = r1 - r0;
+      const char* p0 = reinterpret_cast<const char*>(a.steps + r0 * a.dm.d0);
+      const char* p1 = reinterpret_cast<const char*>(a.steps + r1 * a.dm.d0);
+      for (const char* p = p0; p < p1; p += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+      const char* c0 = reinterpret_cast<const char*>(a.ctx + idx * a.dm.C);
+      for (int o = 0; o < a.dm.C * 4; o += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(c0 + o));
+    }
+  }
+  __syncwarp();
+  if (lane == 0) s_pref = step + 1;
+}
+
 // ------------------------------------------------ sample backward --
-__device__ void fast_sample_bwd(const FastArgs& a, float* sm, float* xs, int T, float dy,
-                                float yh, int step) {
+__device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int slot, int T,
+                                float dy, float yh, int step) {
   const TDims& dm = a.dm;
   const FastSmem& L = a.sl;
   const FastXch& X = a.xl;
@@ -576,15 +723,15 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, float* xs, int T, 
     const float av = sm[L.a1 + tid];
     const float d = dl * W2[tid] * (1.f - av * av);
     da1[tid] = d;
-    xs[X.da1 + tid] = d;
+    a.xch[X.da1 + (int64_t)slot * kHeadHidden + tid] = d;
   }
-  if (tid == 0) xs[X.dl] = dl;
+  if (tid < 4) a.xch[X.dl + (int64_t)slot * 4 + tid] = tid == 0 ? dl : 0.f;
   __syncthreads();
   bmv_row<float>(W1s, kLdA, da1, kHeadHidden, kFD, dpool, red);
   // ---- attention passes in reverse (tuner.py:310-328)
   const float sq = sqrtf((float)dh);
   for (int u = U - 1; u >= 0; --u) {
-    if (tid < kFD) xs[X.dpool + u * kFD + tid] = dpool[tid];
+    if (tid < kFD) a.xch[X.dpool + ((int64_t)slot * U + u) * kFD + tid] = dpool[tid];
     bmv_row<float>(Wo, kLdA, dpool, kFD, kFD, dmix, red);
     const float* al = sm + L.alpha + (int64_t)u * heads * TM;
     const float* qv = sm + L.q + u * kFD;
@@ -617,7 +764,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, float* xs, int T, 
       float acc = 0.f;
       for (int t = 0; t < T; ++t) acc += dlg[h * TM + t] * K[(int64_t)t * kFD + tid];
       dq[tid] = acc / sq;
-      xs[X.dq + u * kFD + tid] = acc / sq;
+      a.xch[X.dq + ((int64_t)slot * U + u) * kFD + tid] = acc / sq;
     }
     __syncthreads();
     bmv_row<float>(Wq, kLdA, dq, kFD, kFD, dpool, red);
@@ -637,47 +784,54 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, float* xs, int T, 
       s1 = fmaf(dvr[c], wv[c], s1);
     }
     dS[i] = (dpool[k] / denom + s0) + s1;
-    xs[X.dK + i] = dK[i];
-    xs[X.dV + i] = dV[i];
+    a.xch[X.dK + rs * kFD + i] = dK[i];
+    a.xch[X.dV + rs * kFD + i] = dV[i];
   }
   __syncthreads();
   phase_mark(step, 10);
-  // ---- LSTM stack in reverse (tuner.py:340-359)
+  // ---- LSTM stack in reverse (tuner.py:340-359).  Warps 0..3 run the two
+  //      BPTT recurrences (a warp pair per direction); every thread holds a
+  //      64-column slice of one Wx row for dX, fetched before the BPTT so the
+  //      load overlaps it.
   float* dSa = dS;
   float* dSb = sm + L.dS2;
   float* dZ = sm + L.dZ;
   float* part = sm + L.xz;  // [4][TM][64] dX partials (xz is dead)
+  const int xk = tid & 63, xq = tid >> 6, xdir = xq >> 1, xhalf = xq & 1;
   for (int l = dm.L - 1; l >= 0; --l) {
-    if (warp < 2)
-      fast_rec_bwd(warp, T, TM, a.prm + dm.wh[l][warp], sm + L.gc + (int64_t)l * 2 * TM * kFG,
-                   sm + L.cs + (int64_t)l * 2 * TM * kFH, dSa, dZ,
-                   xs + X.dZ + (int64_t)l * 2 * TM * kFG);
-    if (warp == 0) phase_mark(step, 11 + (dm.L - 1 - l) * 2);
-    if (l == 0) break;
-    // dX partials need this layer's Wx rows: load them while the BPTT warps run
-    const int pq = tid >> 6, kk = tid & 63, dir = pq >> 1, cb = (pq & 1) * 64;
-    float wr[64];
-    {
-      const float4* w4 = reinterpret_cast<const float4*>(a.prm + dm.wx[l][dir] + (int64_t)kk * kFG + cb);
+    WReg whr;
+    float wx[64];
+    if (warp < 4) load_wh_row(whr, a.prm + dm.wh[l][warp >> 1], warp & 1);
+    if (l > 0) {
+      const float4* w4 =
+          reinterpret_cast<const float4*>(a.prm + dm.wx[l][xdir] + (int64_t)xk * kFG + xhalf * 64);
 #pragma unroll
       for (int m = 0; m < 16; ++m) {
         const float4 v = __ldcg(w4 + m);
-        wr[4 * m + 0] = v.x;
-        wr[4 * m + 1] = v.y;
-        wr[4 * m + 2] = v.z;
-        wr[4 * m + 3] = v.w;
+        wx[4 * m + 0] = v.x;
+        wx[4 * m + 1] = v.y;
+        wx[4 * m + 2] = v.z;
+        wx[4 * m + 3] = v.w;
       }
     }
+    if (warp < 4) {
+      fast_rec_bwd(whr, warp >> 1, warp & 1, T, TM, sm + L.gc + (int64_t)l * 2 * TM * kFG,
+                   sm + L.cs + (int64_t)l * 2 * TM * kFH, dSa, dZ,
+                   a.xch + X.dZ + (((int64_t)l * 2 + (warp >> 1)) * X.Rmax + rs) * kFG,
+                   sm + L.gex);
+      if (warp == 0) phase_mark(step, 11 + (dm.L - 1 - l) * 2);
+    } else if (warp == 7 && l == dm.L - 1) {
+      prefetch_next_sample(a, step, sm + L.lbn);
+    }
     __syncthreads();
+    if (l == 0) break;
     for (int t = 0; t < T; ++t)
-      part[((int64_t)pq * TM + t) * kFD + kk] =
-          dot_reg<64>(dZ + ((int64_t)dir * TM + t) * kFG + cb, wr);
+      part[((int64_t)xq * TM + t) * kFD + xk] =
+          dot64<0>(dZ + ((int64_t)xdir * TM + t) * kFG + xhalf * 64, wx);
     __syncthreads();
     for (int i = tid; i < T * kFD; i += kThreads) {
-      const int t = i / kFD, k = i % kFD;
-      const float p0 = part[((int64_t)0 * TM + t) * kFD + k], p1 = part[((int64_t)1 * TM + t) * kFD + k];
-      const float p2 = part[((int64_t)2 * TM + t) * kFD + k], p3 = part[((int64_t)3 * TM + t) * kFD + k];
-      dSb[i] = (p0 + p1) + (p2 + p3);  // dX_fw + dX_bw (tuner.py:359)
+      const int64_t o = (int64_t)TM * kFD;
+      dSb[i] = (part[i] + part[o + i]) + (part[2 * o + i] + part[3 * o + i]);  // dX_fw + dX_bw
     }
     __syncthreads();
     phase_mark(step, 12 + (dm.L - 1 - l) * 2);
@@ -689,129 +843,105 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, float* xs, int T, 
 }
 
 // ------------------------------------------------------ job runner --
-// Stage the rows of job `jb` for minibatch slots [k0, k1) into smem:
-// A rows [rows][kap] (ones column appended when the slice has a bias),
-// B rows [rows][nbp].  Returns the number of staged rows.
-__device__ int fast_job_stage(const FastArgs& a, const FastJob& jb, int k0, int k1, int ka,
-                              bool has_bias, int kap, int nbp, float* As, float* Bs) {
+// Stage operand rows [r0, r1) of job `jb` into shared memory: A rows
+// [n][kap] = [segment 1 (w1) | h_prev (32, LSTM) | ones/pad chunk], B rows
+// [n][nbp] = the job's column slice.  The exchange is stacked by row, so
+// every operand is one flat loop of 16-B cp.async.cg copies (L2 -> smem).
+__device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGeo& g, int64_t r0,
+                               int64_t r1, float* As, float* Bs) {
   const TDims& dm = a.dm;
   const FastXch& X = a.xl;
   const int tid = threadIdx.x;
-  const int TM = dm.Tmax;
-  int rows = 0;
-  for (int k = k0; k < k1; ++k) {
-    const float* xs = a.xch + (int64_t)k * X.total;
-    const int T = (int)__ldcg(a.meta + 2 * k + 1);
-    int nr;
-    switch (jb.kind) {
-      case FJ_LSTM:
-      case FJ_WK:
-      case FJ_WV: nr = T; break;
-      case FJ_WQ:
-      case FJ_WO: nr = dm.U; break;
-      default: nr = 1;
-    }
-    float* Ar = As + (int64_t)rows * kap;
-    float* Br = Bs + (int64_t)rows * nbp;
-    if (jb.kind == FJ_LSTM) {
-      const int l = jb.l, dir = jb.dir;
-      const int din = l == 0 ? dm.d0 : kFD;
-      const float* Sl = xs + X.S + (int64_t)l * TM * kFD;
-      const float* dZ = xs + X.dZ + ((int64_t)l * 2 + dir) * TM * kFG + jb.c0;
-      if (l == 0) {
-        const int64_t r0 = __ldcg(a.meta + 2 * k);
-        const float* x0 = a.steps + r0 * dm.d0;
-        for (int i = tid; i < T * din; i += kThreads) cp_async4(Ar + (i / din) * kap + (i % din), x0 + i);
+  const int kap = g.kap, nbp = g.nbp, nq = jb.nb / 4 > 0 ? jb.nb / 4 : 1;
+  const int q1 = g.w1 / 4;
+  const int n = (int)(r1 - r0);
+  const float* A1;
+  const float* A2 = nullptr;
+  const float* B1;
+  int lda1, ldb1;
+  const float* xc = a.xch;
+  switch (jb.kind) {
+    case FJ_LSTM:
+      if (jb.l == 0) {
+        A1 = xc + X.x0;
+        lda1 = X.w0;
       } else {
-        const float* Sp = xs + X.S + (int64_t)(l - 1) * TM * kFD;
-        for (int i = tid; i < T * 16; i += kThreads)
-          cp_async16(Ar + (i >> 4) * kap + (i & 15) * 4, Sp + (int64_t)(i >> 4) * kFD + (i & 15) * 4);
+        A1 = xc + X.S + (int64_t)(jb.l - 1) * X.Rmax * kFD;
+        lda1 = kFD;
       }
-      // h_prev in the direction's order (zero state at its first step)
-      for (int i = tid; i < T * 8; i += kThreads) {
-        const int t = i >> 3, q = i & 7;
-        const int tp = dir == 0 ? t - 1 : t + 1;
-        float* d = Ar + t * kap + din + q * 4;
-        if (tp >= 0 && tp < T) {
-          const float* src = Sl + (int64_t)tp * kFD + dir * kFH + q * 4;
-          if (din & 3) {
-            cp_async4(d, src), cp_async4(d + 1, src + 1), cp_async4(d + 2, src + 2), cp_async4(d + 3, src + 3);
-          } else {
-            cp_async16(d, src);
-          }
-        } else
-          d[0] = d[1] = d[2] = d[3] = 0.f;
-      }
-      for (int i = tid; i < T * (jb.nb / 4); i += kThreads) {
-        const int t = i / (jb.nb / 4), q = i % (jb.nb / 4);
-        cp_async16(Br + t * nbp + q * 4, dZ + (int64_t)t * kFG + q * 4);
-      }
-    } else if (jb.kind == FJ_WK || jb.kind == FJ_WV) {
-      const float* Sl = xs + X.S + (int64_t)(dm.L - 1) * TM * kFD;
-      const float* G = xs + (jb.kind == FJ_WK ? X.dK : X.dV) + jb.c0;
-      for (int i = tid; i < T * 16; i += kThreads)
-        cp_async16(Ar + (i >> 4) * kap + (i & 15) * 4, Sl + (int64_t)(i >> 4) * kFD + (i & 15) * 4);
-      for (int i = tid; i < T * (jb.nb / 4); i += kThreads) {
-        const int t = i / (jb.nb / 4), q = i % (jb.nb / 4);
-        cp_async16(Br + t * nbp + q * 4, G + (int64_t)t * kFD + q * 4);
-      }
-    } else if (jb.kind == FJ_WQ || jb.kind == FJ_WO) {
-      const float* Av = xs + (jb.kind == FJ_WQ ? X.pin : X.mix);
-      const float* G = xs + (jb.kind == FJ_WQ ? X.dq : X.dpool) + jb.c0;
-      for (int i = tid; i < dm.U * 16; i += kThreads)
-        cp_async16(Ar + (i >> 4) * kap + (i & 15) * 4, Av + (int64_t)(i >> 4) * kFD + (i & 15) * 4);
-      for (int i = tid; i < dm.U * (jb.nb / 4); i += kThreads) {
-        const int u = i / (jb.nb / 4), q = i % (jb.nb / 4);
-        cp_async16(Br + u * nbp + q * 4, G + (int64_t)u * kFD + q * 4);
-      }
-    } else if (jb.kind == FJ_W1) {
-      const int Z = kFD + dm.C;
-      for (int i = tid; i < Z; i += kThreads) cp_async4(Ar + i, xs + X.z + i);
-      for (int i = tid; i < jb.nb / 4; i += kThreads) cp_async16(Br + i * 4, xs + X.da1 + jb.c0 + i * 4);
-    } else {  // W2 | b2: A = a1, B = dl
-      for (int i = tid; i < kHeadHidden / 4; i += kThreads) cp_async16(Ar + i * 4, xs + X.a1 + i * 4);
-      if (tid == 0) {
-        cp_async4(Br, xs + X.dl);
-        Br[1] = Br[2] = Br[3] = 0.f;
-      }
+      A2 = xc + X.H + ((int64_t)jb.l * 2 + jb.dir) * X.Rmax * kFH;
+      B1 = xc + X.dZ + ((int64_t)jb.l * 2 + jb.dir) * X.Rmax * kFG + jb.c0;
+      ldb1 = kFG;
+      break;
+    case FJ_WK:
+    case FJ_WV:
+      A1 = xc + X.S + (int64_t)(dm.L - 1) * X.Rmax * kFD;
+      lda1 = kFD;
+      B1 = xc + (jb.kind == FJ_WK ? X.dK : X.dV) + jb.c0;
+      ldb1 = kFD;
+      break;
+    case FJ_WQ:
+    case FJ_WO:
+      A1 = xc + (jb.kind == FJ_WQ ? X.pin : X.mix);
+      lda1 = kFD;
+      B1 = xc + (jb.kind == FJ_WQ ? X.dq : X.dpool) + jb.c0;
+      ldb1 = kFD;
+      break;
+    case FJ_W1:
+      A1 = xc + X.z;
+      lda1 = X.zw;
+      B1 = xc + X.da1 + jb.c0;
+      ldb1 = kHeadHidden;
+      break;
+    default:
+      A1 = xc + X.a1;
+      lda1 = kHeadHidden;
+      B1 = xc + X.dl;
+      ldb1 = 4;
+  }
+  A1 += r0 * lda1;
+  B1 += r0 * ldb1;
+  for (int e = tid; e < n * q1; e += kThreads) {
+    const int r = e / q1, q = e - r * q1;
+    cp_async16(As + r * kap + q * 4, A1 + (int64_t)r * lda1 + q * 4);
+  }
+  if (A2) {
+    A2 += r0 * kFH;
+    for (int e = tid; e < n * 8; e += kThreads) {
+      const int r = e >> 3, q = e & 7;
+      cp_async16(As + r * kap + g.w1 + q * 4, A2 + (int64_t)r * kFH + q * 4);
     }
-    // ones column (bias) and zero padding of A; zero padding of B
-    const int ka_w = has_bias ? ka - 1 : ka;
-    for (int i = tid; i < nr * (kap - ka_w); i += kThreads) {
-      const int r = i / (kap - ka_w), cix = ka_w + i % (kap - ka_w);
-      Ar[r * kap + cix] = (has_bias && cix == ka_w) ? 1.f : 0.f;
-    }
-    if (jb.nb < nbp && jb.kind != FJ_W2)
-      for (int i = tid; i < nr * (nbp - jb.nb); i += kThreads) {
-        const int r = i / (nbp - jb.nb);
-        Br[r * nbp + jb.nb + i % (nbp - jb.nb)] = 0.f;
-      }
-    rows += nr;
+  }
+  const int c0 = g.w1 + g.n2;
+  if (kap > c0) {  // ones column (bias) + zero padding, from the constant chunk
+    const float* src = xc + X.cst + (g.bias ? 4 : 0);
+    for (int r = tid; r < n; r += kThreads) cp_async16(As + r * kap + c0, src);
+  }
+  for (int e = tid; e < n * nq; e += kThreads) {
+    const int r = e / nq, q = e - r * nq;
+    cp_async16(Bs + r * nbp + q * 4, B1 + (int64_t)r * ldb1 + q * 4);
   }
   cp_async_wait_all();
   __syncthreads();
-  return rows;
 }
 
-__device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int step, float* sm) {
+// R: stacked step rows of the minibatch; bn: samples.
+__device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64_t R, int step,
+                             float* sm) {
   const TDims& dm = a.dm;
   const int tid = threadIdx.x;
-  bool has_bias = false;
-  const int ka = fast_job_ka(dm, jb, has_bias);
-  const int kap = round4(ka), nbp = round4(jb.nb);
+  const JobGeo geo = job_geo(dm, jb);
+  const int kap = geo.kap, nbp = geo.nbp, maxr = geo.maxr;
   const int nkb = kap / 4, ncb = nbp / 4, nblk = nkb * ncb;
   const int RG = nblk >= kThreads ? 1 : kThreads / nblk;
-  const int TM = dm.Tmax;
-  int maxr;
-  switch (jb.kind) {
-    case FJ_LSTM: case FJ_WK: case FJ_WV: maxr = TM; break;
-    case FJ_WQ: case FJ_WO: maxr = dm.U; break;
-    default: maxr = 1;
-  }
-  const int per_chunk = (int)(a.rch / maxr > 1 ? a.rch / maxr : 1);  // samples per staging chunk
+  (void)maxr;
+  const int64_t nrows = jb.kind == FJ_LSTM || jb.kind == FJ_WK || jb.kind == FJ_WV
+                            ? R
+                            : (jb.kind == FJ_WQ || jb.kind == FJ_WO ? (int64_t)bn * dm.U : bn);
+  const int64_t rch = a.rch;  // rows per staging chunk
   float* As = sm;
-  float* Bs = As + (int64_t)per_chunk * maxr * kap;
-  float* redb = Bs + (int64_t)per_chunk * maxr * nbp;   // [RG][nblk][16]
+  float* Bs = As + rch * kap;
+  float* redb = Bs + rch * nbp;                         // [RG][nblk][16]
   float* gout = redb + (int64_t)kThreads * 16;          // [kap][nbp]
   // thread -> (row group g, 4x4 output block blk); nblk <= 256 (fast_plan)
   float acc[4][4];
@@ -822,12 +952,14 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int s
   const int g = tid / nblk, blk = tid % nblk;
   const bool active = tid < RG * nblk;
   const int kb = blk / ncb, cb = blk % ncb;
-  for (int k0 = 0; k0 < bn; k0 += per_chunk) {
-    const int k1 = min(bn, k0 + per_chunk);
+  for (int64_t c0 = 0; c0 < nrows; c0 += rch) {
+    const int64_t c1 = c0 + rch < nrows ? c0 + rch : nrows;
     __syncthreads();
-    const int R = fast_job_stage(a, jb, k0, k1, ka, has_bias, kap, nbp, As, Bs);
+    fast_job_stage(a, jb, geo, c0, c1, As, Bs);
+    if (blockIdx.x == (unsigned)(a.B % gridDim.x)) phase_mark_any(step, 22);
+    const int n = (int)(c1 - c0);
     if (active) {
-      for (int rr = g; rr < R; rr += RG) {
+      for (int rr = g; rr < n; rr += RG) {
         const float4 av = *reinterpret_cast<const float4*>(As + (int64_t)rr * kap + kb * 4);
         const float4 bv = *reinterpret_cast<const float4*>(Bs + (int64_t)rr * nbp + cb * 4);
         const float ax[4] = {av.x, av.y, av.z, av.w}, bx[4] = {bv.x, bv.y, bv.z, bv.w};
@@ -850,23 +982,22 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int s
     gout[((b / ncb) * 4 + (e >> 2)) * nbp + (b % ncb) * 4 + (e & 3)] = s;
   }
   __syncthreads();
+  if (blockIdx.x == (unsigned)(a.B % gridDim.x)) phase_mark_any(step, 23);
   // parameter addresses of the slice and the fused Adam update
-  int64_t base, ldp, bias;
-  switch (jb.kind) {
-    case FJ_LSTM: base = dm.wx[jb.l][jb.dir]; ldp = kFG; bias = dm.bb[jb.l][jb.dir]; break;
-    case FJ_WQ: base = dm.Wq; ldp = kFD; bias = dm.bq; break;
-    case FJ_WK: base = dm.Wk; ldp = kFD; bias = -1; break;
-    case FJ_WV: base = dm.Wv; ldp = kFD; bias = -1; break;
-    case FJ_WO: base = dm.Wo; ldp = kFD; bias = dm.bo; break;
-    case FJ_W1: base = dm.W1; ldp = kHeadHidden; bias = dm.b1; break;
-    default: base = dm.W2; ldp = 1; bias = dm.b2; break;
-  }
-  const int ka_w = has_bias ? ka - 1 : ka;
   const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
   const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
-  for (int i = tid; i < ka * jb.nb; i += kThreads) {
-    const int k = i / jb.nb, c = i % jb.nb;
-    const int64_t p = k < ka_w ? base + (int64_t)k * ldp + jb.c0 + c : bias + jb.c0 + c;
+  const int nb = jb.nb;
+  for (int i = tid; i < geo.ka * nb; i += kThreads) {
+    const int k = i / nb, c = i % nb;
+    int64_t p;
+    if (k < geo.n1)
+      p = geo.base + (int64_t)k * geo.ldp + jb.c0 + c;
+    else if (k < geo.w1)
+      continue;  // zero padding column
+    else if (k < geo.w1 + geo.n2)
+      p = geo.base + (int64_t)(geo.n1 + k - geo.w1) * geo.ldp + jb.c0 + c;
+    else
+      p = geo.bptr + jb.c0 + c;
     const float gv = gout[k * nbp + c];
     if (a.mode == TT_MODE_GRAD) {
       a.grad_out[p] = gv;
@@ -880,13 +1011,64 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int s
   }
 }
 
+// Pairwise logistic loss over the minibatch (mlp.py:25-35), all threads:
+// warp w owns rows k = w, w+8, ..; lanes sweep j.  Same per-pair terms as
+// rank_loss_block; per-row sums by warp shuffles, the row totals summed in
+// fixed order.  red needs 2n floats.  Returns the loss in every thread.
+__device__ float fast_rank_loss(const float* y, const float* s, int n, float* dscore, float* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < n; k += kThreads / 32) {
+    const float yk = y[k], sk = s[k];
+    float d = 0.f, part = 0.f, pairs = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float yj = y[j], sj = s[j];
+      if (yj > yk) d += 1.f / (1.f + Act<float>::exp(sj - sk));
+      if (yk > yj) {
+        const float mg = sk - sj;
+        d -= 1.f / (1.f + Act<float>::exp(mg));
+        part += Act<float>::softplus(-mg);
+        pairs += 1.f;
+      }
+    }
+    d = warp_sum(d);
+    part = warp_sum(part);
+    pairs = warp_sum(pairs);
+    if (lane == 0) {
+      dscore[k] = d;
+      red[k] = part;
+      red[n + k] = pairs;
+    }
+  }
+  __syncthreads();
+  __shared__ float s_tot[2];
+  if (threadIdx.x == 0) {
+    float tot = 0.f, np = 0.f;
+    for (int k = 0; k < n; ++k) {
+      tot += red[k];
+      np += red[n + k];
+    }
+    s_tot[0] = tot;
+    s_tot[1] = np;
+  }
+  __syncthreads();
+  const float np = s_tot[1];
+  for (int k = threadIdx.x; k < n; k += kThreads) dscore[k] = np == 0.f ? 0.f : dscore[k] / np;
+  const float loss = np == 0.f ? 0.f : s_tot[0] / np;
+  __syncthreads();
+  return loss;
+}
+
 // ------------------------------------------------------------ kernel --
 __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* sm = reinterpret_cast<float*>(smem_raw);
-  __shared__ int64_t s_meta[3];
+  __shared__ int s_jT[kMaxFastB];
+  __shared__ int64_t s_R;
   __shared__ int s_stop;
   const TDims& dm = a.dm;
+  if (threadIdx.x == 0) s_pref = -1;
+  if (blockIdx.x == 0 && threadIdx.x < 8)  // constant chunks [0 0 0 0 | 1 0 0 0] for job staging
+    a.xch[a.xl.cst + threadIdx.x] = threadIdx.x == 4 ? 1.f : 0.f;
   const int tid = threadIdx.x;
   const int G = gridDim.x, r = blockIdx.x;
   const bool sampler = r < a.B;
@@ -903,21 +1085,47 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       if (step > 0) wait_counter(a.ctr + 2, (unsigned)(step * a.n_jobs), false);
       phase_mark(step, 1);
       if (r == 0) phase_mark_any(step, 31);
-      if (tid == 0) {
-        const int64_t idx = a.order[b0 + r];
-        const int64_t r0 = a.rowoff[idx];
-        s_meta[0] = idx;
-        s_meta[1] = r0;
-        s_meta[2] = a.rowoff[idx + 1] - r0;
-        a.meta[2 * r] = r0;
-        a.meta[2 * r + 1] = s_meta[2];
+      // step counts, labels and slot metadata: prefetched into smem during the
+      // previous step's backward (prefetch_next_sample), else loaded here
+      if (s_pref != step) {
+        for (int i = tid; i < bn; i += kThreads) {
+          const int64_t idx = a.order[b0 + i];
+          const int64_t r0 = a.rowoff[idx], r1 = a.rowoff[idx + 1];
+          lb[i] = a.y[idx];
+          s_T[i] = (int)(r1 - r0);
+          if (i == r) {
+            s_nmeta[0] = idx;
+            s_nmeta[1] = r0;
+            s_nmeta[2] = r1 - r0;
+          }
+        }
+      } else {
+        for (int i = tid; i < bn; i += kThreads) {
+          lb[i] = sm[a.sl.lbn + i];
+          s_T[i] = s_Tn[i];
+        }
       }
-      for (int i = tid; i < bn; i += kThreads) lb[i] = a.y[a.order[b0 + i]];
       __syncthreads();
-      const int64_t idx = s_meta[0], r0 = s_meta[1];
-      const int T = (int)s_meta[2];
-      float* xs = a.xch + (int64_t)r * a.xl.total;
-      const float yh = fast_sample_fwd(a, sm, xs, r0, T, idx, step);
+      const int64_t idx = s_nmeta[0], r0 = s_nmeta[1];
+      const int T = (int)s_nmeta[2];
+      int64_t rs = 0;  // first stacked row of this sample
+      for (int i = 0; i < r; ++i) rs += s_T[i];
+      if (tid == 0) a.meta[r] = T;
+      {
+        // raw step rows -> smem (layer-0 projection) and the stacked exchange
+        // (layer-0 weight gradient), zero padded to 16 B rows
+        const int w0 = a.xl.w0;
+        const float* x0 = a.steps + r0 * dm.d0;
+        float* xg = a.xch + a.xl.x0 + rs * w0;
+        for (int i = tid; i < T * w0; i += kThreads) {
+          const int t = i / w0, k = i - t * w0;
+          const float v = k < dm.d0 ? __ldg(x0 + (int64_t)t * dm.d0 + k) : 0.f;
+          sm[a.sl.x0 + i] = v;
+          xg[i] = v;
+        }
+      }
+      __syncthreads();
+      const float yh = fast_sample_fwd(a, sm, rs, r, r0, T, idx, step);
       phase_mark(step, 5);
       if (tid == 0) a.yhat_buf[r] = yh;
       signal_counter(a.ctr + 0, 1);
@@ -926,7 +1134,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       for (int i = tid; i < bn; i += kThreads) lb[bn + i] = __ldcg(a.yhat_buf + i);
       __syncthreads();
       const float loss = a.loss_kind == TT_LOSS_RANK
-                             ? rank_loss_block<float>(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red)
+                             ? fast_rank_loss(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red)
                              : mse_block<float>(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red);
       if (tid == 0) {
         s_stop = !isfinite(loss);
@@ -937,7 +1145,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       }
       __syncthreads();
       phase_mark(step, 7);
-      if (!s_stop) fast_sample_bwd(a, sm, xs, T, lb[2 * bn + r], yh, step);
+      if (!s_stop) fast_sample_bwd(a, sm, rs, r, T, lb[2 * bn + r], yh, step);
       phase_mark(step, 16);
       if (r == 0) phase_mark_any(step, 30);
       signal_counter(a.ctr + 1, 1);
@@ -950,9 +1158,18 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     wait_counter(a.ctr + 1, cum, !sampler);
     if (r == a.B % G) phase_mark_any(step, 20);
     if (tid == 0) s_stop = __ldcg(a.status) >= 0;
+    for (int i = tid; i < bn; i += kThreads) s_jT[i] = (int)__ldcg(a.meta + i);
     __syncthreads();
+    if (tid == 0) {
+      int64_t R = 0;
+      for (int i = 0; i < bn; ++i) R += s_jT[i];
+      s_R = R;
+    }
+    __syncthreads();
+    if (r == a.B % G) phase_mark_any(step, 17);
     if (s_stop) break;
-    for (int j = first_job; j < a.n_jobs; j += G) fast_run_job(a, fast_job(dm, j), bn, step, sm);
+    for (int j = first_job; j < a.n_jobs; j += G)
+      fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm);
     signal_counter(a.ctr + 2, (unsigned)my_jobs);
     if (r == a.B % G) phase_mark_any(step, 21);
   }
@@ -968,30 +1185,30 @@ struct FastPlan {
 };
 
 inline size_t fast_ws_bytes(const TDims& dm, int B) {
-  const FastXch xl = make_fast_xch(dm);
-  return align_up((size_t)B * xl.total * sizeof(float), 256) + align_up((size_t)B * 2 * 8, 256) +
+  const FastXch xl = make_fast_xch(dm, B);
+  return align_up((size_t)xl.total * sizeof(float), 256) + align_up((size_t)B * 8, 256) +
          align_up((size_t)B * sizeof(float), 256) + 256;
 }
 
 // Eligible: fp32, hidden 32, one sample per CTA, every per-sample cache in
 // shared memory.  Returns false (generic kernel) otherwise.
 inline bool fast_plan(const TDims& dm, int B, int grid, FastPlan& p) {
-  if (dm.H != kFH || B > grid || B < 1 || dm.Tmax > 32 || dm.heads < 1) return false;
+  if (dm.H != kFH || B > grid || B > kMaxFastB || B < 1 || dm.Tmax > 32 || dm.heads < 1)
+    return false;
   int dev = 0, optin = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
     return false;
   p.sl = make_fast_smem(dm, B);
-  p.xl = make_fast_xch(dm);
+  p.xl = make_fast_xch(dm, B);
   p.n_jobs = fast_n_jobs(dm);
   const size_t static_smem = 64;
   const size_t budget = (size_t)optin - static_smem - 1024;
   size_t need = (size_t)p.sl.total * sizeof(float);
   if (need > budget) return false;
   // job staging: at least Tmax rows of the widest job
-  const int kap_max = round4(std::max(dm.d0, kFD) + kFH + 1 > kFD + dm.C + 1
-                                 ? std::max(dm.d0, kFD) + kFH + 1
-                                 : kFD + dm.C + 1);
+  const int kap_max = std::max(round4(round4(std::max(dm.d0, kFD)) + kFH + 1),
+                               round4(round4(kFD + dm.C) + 1));
   const int nbp = 16;
   const int64_t job_fixed = fast_job_smem(kap_max, nbp, 0);
   const size_t avail = std::max(need, (size_t)budget);
@@ -1012,9 +1229,9 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   a.n_jobs = p.n_jobs;
   a.rch = p.rch;
   a.xch = reinterpret_cast<float*>(w);
-  w += align_up((size_t)a.B * p.xl.total * sizeof(float), 256);
+  w += align_up((size_t)p.xl.total * sizeof(float), 256);
   a.meta = reinterpret_cast<int64_t*>(w);
-  w += align_up((size_t)a.B * 2 * 8, 256);
+  w += align_up((size_t)a.B * 8, 256);
   a.yhat_buf = reinterpret_cast<float*>(w);
   w += align_up((size_t)a.B * sizeof(float), 256);
   a.ctr = reinterpret_cast<unsigned int*>(w);
