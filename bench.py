@@ -255,8 +255,9 @@ def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam):
     from paper_2304_05430_b200.estimators import _bias_corrections
 
     lib = _lib.load()
-    names = {0: "start", 1: "adam_wait", 2: "fwd_l0", 3: "fwd_l1", 4: "fwd_l2", 5: "attn_fwd",
-             6: "yhat_xchg", 7: "loss", 10: "attn_bwd+dS", 11: "bptt_l2", 12: "dX_l2",
+    names = {0: "start", 1: "adam_wait", 2: "fwd_l0", 3: "fwd_l1", 4: "fwd_l2", 8: "attn_kv",
+             9: "attn_p0", 17: "attn_p1", 5: "head", 6: "yhat_xchg", 7: "loss", 18: "head_bwd",
+             19: "attn_bwd_p1", 24: "attn_bwd_p0", 10: "dS", 11: "bptt_l2", 12: "dX_l2",
              13: "bptt_l1", 14: "dX_l1", 15: "bptt_l0", 16: "bwd_end"}
     for probe in (40, 41, 42):
         lib.tt_debug_profile_step(probe)
@@ -272,12 +273,12 @@ def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam):
         mk = list(buf)
         prev = mk[0]
         row = []
-        for i in sorted(names):
-            if i == 0 or mk[i] == 0 or mk[i] < prev:
+        for i in sorted(names, key=lambda i: mk[i] if mk[i] else 0):
+            if i == 0 or mk[i] == 0 or mk[i] < mk[0]:
                 continue
             row.append(f"{names[i]}={(mk[i] - prev) / 1965.0:.2f}")
             prev = mk[i]
-        last = max(i for i in names if mk[i] >= mk[0] and mk[i] != 0)
+        last = max((i for i in names if mk[i] >= mk[0] and mk[i] != 0), key=lambda i: mk[i])
         jobs = ""
         if mk[20] and mk[30]:
             jobs = (f" | job CTA: start-after-cta0-bwd={(mk[20] - mk[30]) / 1e3:.2f}us "

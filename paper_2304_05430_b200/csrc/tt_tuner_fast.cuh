@@ -32,7 +32,7 @@
 namespace tt {
 
 constexpr int kFH = 32, kFD = 64, kFG = 128;  // hidden, 2H, 4H
-constexpr int kLdA = 65;                       // staged attention weights row stride
+constexpr int kLdA = 68;  // staged attention weights row stride (16-B rows, see frow_mv)
 constexpr int kMaxFastB = 160;                 // minibatch limit of the latency path
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
@@ -87,7 +87,7 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   s.dq = seg(kFD);
   s.dpool = seg(kFD);
   s.da1 = seg(kHeadHidden);
-  // attention + head weights, row stride 65: [Wq|Wk|Wv|Wo|bq|bo] then [W1|b1|W2]
+  // attention + head weights, row stride 68: [Wq|Wk|Wv|Wo|bq|bo] then [W1|b1|W2]
   s.W = seg((int64_t)(4 * kFD + 2) * kLdA + (int64_t)(kFD + d.C + 2) * kLdA);
   s.total = o;
   return s;
@@ -456,6 +456,28 @@ __device__ __forceinline__ float dot64(const float* __restrict__ x, const float 
   return (a0 + a1) + (a2 + a3);
 }
 
+// out[k] = sum_{c < 64} W[k*kLdA + c] v[c] for k < 64 (v @ W^T), all threads:
+// thread (k, part) reads its 16-column row segment as float4 (conflict-free
+// at the 16-B row stride), partials combined in fixed order.  Ends synced.
+__device__ __forceinline__ void frow_mv(const float* W, const float* v, float* out, float* red) {
+  const int k = threadIdx.x & 63, part = threadIdx.x >> 6;
+  const float4* w4 = reinterpret_cast<const float4*>(W + k * kLdA + part * 16);
+  const float4* v4 = reinterpret_cast<const float4*>(v + part * 16);
+  float acc = 0.f;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const float4 w = w4[m], x = v4[m];
+    acc = fmaf(w.x, x.x, acc);
+    acc = fmaf(w.y, x.y, acc);
+    acc = fmaf(w.z, x.z, acc);
+    acc = fmaf(w.w, x.w, acc);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < 64) out[threadIdx.x] = (red[k] + red[64 + k]) + (red[128 + k] + red[192 + k]);
+  __syncthreads();
+}
+
 // ------------------------------------------------- sample forward --
 // All 256 threads.  Returns yhat (valid in every thread after the call).
 // rs: this sample's first row in the stacked exchange; slot: its minibatch slot.
@@ -520,36 +542,22 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     } else {
       named_barrier(1, kThreads);
       if (l == 0) {
-        // idle warps stage the attention/head weights (changed by the last Adam step)
-      const int t2 = tid - 128, n2 = kThreads - 128;
-      const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
-      const float* src1 = a.prm + dm.Wq;
-      const float* src2 = a.prm + dm.W1;
-      const int tot1 = rows1 * (kFD / 4), tot2 = rows2 * (kHeadHidden / 4);
-      for (int i0 = t2; i0 < tot1 + tot2; i0 += 8 * n2) {
-        float4 v[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int ii = i0 + u * n2;
-          if (ii < tot1)
-            v[u] = __ldcg(reinterpret_cast<const float4*>(src1) + ii);
-          else if (ii < tot1 + tot2)
-            v[u] = __ldcg(reinterpret_cast<const float4*>(src2) + (ii - tot1));
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int ii = i0 + u * n2;
-          if (ii < tot1) {
-            float* d = W + (ii >> 4) * kLdA + (ii & 15) * 4;
-            d[0] = v[u].x, d[1] = v[u].y, d[2] = v[u].z, d[3] = v[u].w;
-          } else if (ii < tot1 + tot2) {
-            const int i2 = ii - tot1;
-            float* d = W1s + (i2 >> 4) * kLdA + (i2 & 15) * 4;
-            d[0] = v[u].x, d[1] = v[u].y, d[2] = v[u].z, d[3] = v[u].w;
-          }
+        // idle warps start the async copy of the attention/head weights (changed
+        // by the last Adam step) into 16-B rows of stride 68; waited for before
+        // the attention phase
+        const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
+        const float* src1 = a.prm + dm.Wq;
+        const float* src2 = a.prm + dm.W1;
+        const int tot = (rows1 + rows2) * 16;
+        for (int e = tid - 128; e < tot; e += kThreads - 128) {
+          const int row = e >> 4, q = e & 15;
+          if (row < rows1)
+            cp_async16(W + row * kLdA + q * 4, src1 + e * 4);
+          else
+            cp_async16(W1s + (row - rows1) * kLdA + q * 4, src2 + (e - rows1 * 16) * 4);
         }
       }
-      }
+      if (l == dm.L - 1) cp_async_wait_all();
     }
     __syncthreads();
   }
@@ -585,6 +593,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     for (int t = grp; t < T; t += 2) dst[(int64_t)t * kFD + col] = dot_reg<kFD>(Sl + (int64_t)t * kFD, wc);
   }
   __syncthreads();
+  phase_mark(step, 8);
   const float sq = sqrtf((float)dh);
   float* const xpin = a.xch + X.pin + (int64_t)slot * U * kFD;
   float* const xmix = a.xch + X.mix + (int64_t)slot * U * kFD;
@@ -629,6 +638,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     }
     __syncthreads();
     bmv_col<float>(mix, Wo, kLdA, kFD, kFD, bo, pool, red);
+    phase_mark(step, u == 0 ? 9 : 17);
   }
   float* zb = sm + L.zb;
   for (int i = tid; i < round4(Z); i += kThreads) {
@@ -727,12 +737,13 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
   }
   if (tid < 4) a.xch[X.dl + (int64_t)slot * 4 + tid] = tid == 0 ? dl : 0.f;
   __syncthreads();
-  bmv_row<float>(W1s, kLdA, da1, kHeadHidden, kFD, dpool, red);
+  frow_mv(W1s, da1, dpool, red);
+  phase_mark(step, 18);
   // ---- attention passes in reverse (tuner.py:310-328)
   const float sq = sqrtf((float)dh);
   for (int u = U - 1; u >= 0; --u) {
     if (tid < kFD) a.xch[X.dpool + ((int64_t)slot * U + u) * kFD + tid] = dpool[tid];
-    bmv_row<float>(Wo, kLdA, dpool, kFD, kFD, dmix, red);
+    frow_mv(Wo, dpool, dmix, red);
     const float* al = sm + L.alpha + (int64_t)u * heads * TM;
     const float* qv = sm + L.q + u * kFD;
     for (int h = warp; h < heads; h += kThreads / 32) {
@@ -767,21 +778,30 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
       a.xch[X.dq + ((int64_t)slot * U + u) * kFD + tid] = acc / sq;
     }
     __syncthreads();
-    bmv_row<float>(Wq, kLdA, dq, kFD, kFD, dpool, red);
+    frow_mv(Wq, dq, dpool, red);
+    phase_mark(step, u == U - 1 ? 19 : 24);
   }
   // ---- dS = dpool/denom + dK Wk^T + dV Wv^T (tuner.py:331-338)
   float* dS = sm + L.dS;
   const float denom = (float)(T > 1 ? T : 1);
   for (int i = tid; i < T * kFD; i += kThreads) {
     const int t = i / kFD, k = i % kFD;
-    const float* wk = Wk + k * kLdA;
-    const float* wv = Wv + k * kLdA;
-    const float* dkr = dK + (int64_t)t * kFD;
-    const float* dvr = dV + (int64_t)t * kFD;
+    const float4* wk = reinterpret_cast<const float4*>(Wk + k * kLdA);
+    const float4* wv = reinterpret_cast<const float4*>(Wv + k * kLdA);
+    const float4* dkr = reinterpret_cast<const float4*>(dK + (int64_t)t * kFD);
+    const float4* dvr = reinterpret_cast<const float4*>(dV + (int64_t)t * kFD);
     float s0 = 0.f, s1 = 0.f;
-    for (int c = 0; c < kFD; ++c) {
-      s0 = fmaf(dkr[c], wk[c], s0);
-      s1 = fmaf(dvr[c], wv[c], s1);
+#pragma unroll 4
+    for (int m = 0; m < kFD / 4; ++m) {
+      const float4 a4 = dkr[m], b4 = wk[m], c4 = dvr[m], d4 = wv[m];
+      s0 = fmaf(a4.x, b4.x, s0);
+      s1 = fmaf(c4.x, d4.x, s1);
+      s0 = fmaf(a4.y, b4.y, s0);
+      s1 = fmaf(c4.y, d4.y, s1);
+      s0 = fmaf(a4.z, b4.z, s0);
+      s1 = fmaf(c4.z, d4.z, s1);
+      s0 = fmaf(a4.w, b4.w, s0);
+      s1 = fmaf(c4.w, d4.w, s1);
     }
     dS[i] = (dpool[k] / denom + s0) + s1;
     a.xch[X.dK + rs * kFD + i] = dK[i];
@@ -1166,7 +1186,6 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       s_R = R;
     }
     __syncthreads();
-    if (r == a.B % G) phase_mark_any(step, 17);
     if (s_stop) break;
     for (int j = first_job; j < a.n_jobs; j += G)
       fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm);
