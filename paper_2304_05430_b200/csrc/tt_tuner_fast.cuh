@@ -33,7 +33,8 @@ namespace tt {
 
 constexpr int kFH = 32, kFD = 64, kFG = 128;  // hidden, 2H, 4H
 constexpr int kLdA = 68;  // staged attention weights row stride (16-B rows, see frow_mv)
-constexpr int kMaxFastB = 160;                 // minibatch limit of the latency path
+constexpr int kMaxFastB = 160;  // minibatch limit of the latency path
+constexpr int kLdK = 65;        // K/V row stride in smem (odd: lanes over steps hit distinct banks)
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
 
@@ -66,8 +67,8 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   s.xz = seg((int64_t)2 * TM * kFG);  // also the dX partials [4][TM][64]
   s.hb = seg(2 * 2 * 2 * kFH);   // [dir][warp copy][parity][32] hidden state
   s.gex = seg(2 * 2 * 2 * 2 * kFH);  // [dir][warp][parity][64] gate / dh exchange
-  s.K = seg((int64_t)TM * kFD);
-  s.V = seg((int64_t)TM * kFD);
+  s.K = seg((int64_t)TM * kLdK);
+  s.V = seg((int64_t)TM * kLdK);
   s.alpha = seg((int64_t)d.U * d.heads * TM);
   s.pin = seg((int64_t)d.U * kFD);
   s.q = seg((int64_t)d.U * kFD);
@@ -243,6 +244,24 @@ __device__ __forceinline__ void phase_mark_any(int step, int i) {
 }
 
 // ------------------------------------------------------------- sync --
+// Counter layout (monotone within a launch):
+//   ctr[0]             scores published (forward done), += 1 per sample
+//   ctr[1 + g]         backward operands of parameter group g published
+//   ctr[2 + L + g]     gradient jobs of group g done (parameters updated)
+// Groups: g < L = LSTM layer g (both directions), g = L = attention + head.
+// A gradient job waits only for its own group and the next minibatch's
+// forward waits per layer, so the Adam updates of the upper layers overlap
+// the next forward's first layers.
+__device__ __forceinline__ int ctr_bwd(int g) { return 1 + g; }
+__device__ __forceinline__ int ctr_adam(const TDims& d, int g) { return 2 + d.L + g; }
+__device__ __forceinline__ int jobs_per_layer() { return 2 * (kFG / kCwLstm); }
+__device__ __forceinline__ int job_group(const TDims& d, int j) {
+  return j < d.L * jobs_per_layer() ? j / jobs_per_layer() : d.L;
+}
+__device__ __forceinline__ int group_jobs(const TDims& d, int g) {
+  return g < d.L ? jobs_per_layer() : 4 * (kFD / kCwAttn) + kHeadHidden / kCwHead + 1;
+}
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -590,7 +609,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
 #pragma unroll
     for (int k = 0; k < kFD; ++k) wc[k] = wp[k * kLdA];
     float* dst = cc < kFD ? K : V;
-    for (int t = grp; t < T; t += 2) dst[(int64_t)t * kFD + col] = dot_reg<kFD>(Sl + (int64_t)t * kFD, wc);
+    for (int t = grp; t < T; t += 2) dst[(int64_t)t * kLdK + col] = dot_reg<kFD>(Sl + (int64_t)t * kFD, wc);
   }
   __syncthreads();
   phase_mark(step, 8);
@@ -610,7 +629,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
       float* ar = al + (int64_t)h * TM;
       float mx = -INFINITY;
       for (int t = lane; t < T; t += 32) {
-        const float* kr = K + (int64_t)t * kFD + h * dh;
+        const float* kr = K + (int64_t)t * kLdK + h * dh;
         float acc = 0.f;
         for (int d = 0; d < dh; ++d) acc += qh[d] * kr[d];
         acc = acc / sq;
@@ -632,7 +651,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     if (tid < kFD) {
       const float* ar = al + (int64_t)(tid / dh) * TM;
       float acc = 0.f;
-      for (int t = 0; t < T; ++t) acc += ar[t] * V[(int64_t)t * kFD + tid];
+      for (int t = 0; t < T; ++t) acc += ar[t] * V[(int64_t)t * kLdK + tid];
       mix[tid] = acc;
       xmix[u * kFD + tid] = acc;
     }
@@ -750,7 +769,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
       float sacc = 0.f;
       for (int t = lane; t < T; t += 32) {
         float da = 0.f;
-        for (int d = 0; d < dh; ++d) da += dmix[h * dh + d] * V[(int64_t)t * kFD + h * dh + d];
+        for (int d = 0; d < dh; ++d) da += dmix[h * dh + d] * V[(int64_t)t * kLdK + h * dh + d];
         dlg[h * TM + t] = da;
         sacc += da * al[h * TM + t];
       }
@@ -773,7 +792,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
     if (tid < kFD) {
       const int h = tid / dh;
       float acc = 0.f;
-      for (int t = 0; t < T; ++t) acc += dlg[h * TM + t] * K[(int64_t)t * kFD + tid];
+      for (int t = 0; t < T; ++t) acc += dlg[h * TM + t] * K[(int64_t)t * kLdK + tid];
       dq[tid] = acc / sq;
       a.xch[X.dq + ((int64_t)slot * U + u) * kFD + tid] = acc / sq;
     }
@@ -809,6 +828,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
   }
   __syncthreads();
   phase_mark(step, 10);
+  signal_counter(a.ctr + ctr_bwd(dm.L), 1);  // attention/head operands published
   // ---- LSTM stack in reverse (tuner.py:340-359).  Warps 0..3 run the two
   //      BPTT recurrences (a warp pair per direction); every thread holds a
   //      64-column slice of one Wx row for dX, fetched before the BPTT so the
@@ -844,6 +864,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
       prefetch_next_sample(a, step, sm + L.lbn);
     }
     __syncthreads();
+    signal_counter(a.ctr + ctr_bwd(l), 1);  // this layer's dZ published
     if (l == 0) break;
     for (int t = 0; t < T; ++t)
       part[((int64_t)xq * TM + t) * kFD + xk] =
@@ -1093,8 +1114,8 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
   const int G = gridDim.x, r = blockIdx.x;
   const bool sampler = r < a.B;
   const int first_job = (r - a.B + G) % G;
-  int my_jobs = 0;
-  for (int j = first_job; j < a.n_jobs; j += G) ++my_jobs;
+  int my_jobs = 0, last_job = -1;
+  for (int j = first_job; j < a.n_jobs; j += G) ++my_jobs, last_job = j;
   float* lb = sm + a.sl.lb;
   for (int step = 0; step < a.n_steps; ++step) {
     const int64_t b0 = (int64_t)step * a.B;
@@ -1102,7 +1123,11 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     const unsigned cum = (unsigned)(b0 + bn);
     if (sampler && r < bn) {
       phase_mark(step, 0);
-      if (step > 0) wait_counter(a.ctr + 2, (unsigned)(step * a.n_jobs), false);
+      if (step > 0) {
+        // layer 0 and the attention block (staged during layer 0) must be updated
+        wait_counter(a.ctr + ctr_adam(dm, dm.L), (unsigned)(step * group_jobs(dm, dm.L)), false);
+        wait_counter(a.ctr + ctr_adam(dm, 0), (unsigned)(step * group_jobs(dm, 0)), false);
+      }
       phase_mark(step, 1);
       if (r == 0) phase_mark_any(step, 31);
       // step counts, labels and slot metadata: prefetched into smem during the
@@ -1165,32 +1190,40 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       }
       __syncthreads();
       phase_mark(step, 7);
-      if (!s_stop) fast_sample_bwd(a, sm, rs, r, T, lb[2 * bn + r], yh, step);
+      if (!s_stop) {
+        fast_sample_bwd(a, sm, rs, r, T, lb[2 * bn + r], yh, step);
+      } else {
+        for (int g = 0; g <= dm.L; ++g) signal_counter(a.ctr + ctr_bwd(g), 1);  // wake the jobs
+      }
       phase_mark(step, 16);
       if (r == 0) phase_mark_any(step, 30);
-      signal_counter(a.ctr + 1, 1);
       if (s_stop) break;
     }
     if (my_jobs == 0) {
       if (!sampler) break;  // idle CTA
       continue;
     }
-    wait_counter(a.ctr + 1, cum, !sampler);
-    if (r == a.B % G) phase_mark_any(step, 20);
-    if (tid == 0) s_stop = __ldcg(a.status) >= 0;
-    for (int i = tid; i < bn; i += kThreads) s_jT[i] = (int)__ldcg(a.meta + i);
-    __syncthreads();
-    if (tid == 0) {
-      int64_t R = 0;
-      for (int i = 0; i < bn; ++i) R += s_jT[i];
-      s_R = R;
-    }
-    __syncthreads();
-    if (s_stop) break;
-    for (int j = first_job; j < a.n_jobs; j += G)
+    // this CTA's jobs, attention/head group first, then the LSTM layers top-down
+    // (the order in which the samples publish their backward operands)
+    for (int j = last_job; j >= 0; j -= G) {
+      const int g = job_group(dm, j);
+      wait_counter(a.ctr + ctr_bwd(g), cum, !sampler);
+      if (r == a.B % G) phase_mark_any(step, 20);
+      if (tid == 0) s_stop = __ldcg(a.status) >= 0;
+      for (int i = tid; i < bn; i += kThreads) s_jT[i] = (int)__ldcg(a.meta + i);
+      __syncthreads();
+      if (tid == 0) {
+        int64_t R = 0;
+        for (int i = 0; i < bn; ++i) R += s_jT[i];
+        s_R = R;
+      }
+      __syncthreads();
+      if (s_stop) break;
       fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm);
-    signal_counter(a.ctr + 2, (unsigned)my_jobs);
-    if (r == a.B % G) phase_mark_any(step, 21);
+      signal_counter(a.ctr + ctr_adam(dm, g), 1);
+      if (r == a.B % G) phase_mark_any(step, 21);
+    }
+    if (s_stop) break;
   }
 }
 
