@@ -197,8 +197,10 @@ __device__ inline JobGeo job_geo(const TDims& d, const FastJob& jb) {
 }
 
 // smem floats a job needs for `rows` staged rows (plus the reduction area)
+// (the last term: the persistent parameter/moment cache of a job CTA)
 __host__ __device__ inline int64_t fast_job_smem(int kap, int nbp, int rows) {
-  return (int64_t)rows * (kap + nbp) + (int64_t)kThreads * 16 + (int64_t)kap * nbp + 64;
+  return (int64_t)rows * (kap + nbp) + (int64_t)kThreads * 16 + (int64_t)kap * nbp + 64 +
+         (int64_t)4 * kap * nbp;
 }
 
 // ------------------------------------------------------------- args --
@@ -231,6 +233,8 @@ struct FastArgs {
   unsigned int* ctr;   // [0] fwd, [1] bwd, [2] adam (monotone)
   int n_jobs;
   int64_t rch;         // job staging rows per chunk
+  int64_t pc_off;      // smem float offset of a job CTA's parameter cache [4][pc_n]
+  int pc_n;            // floats per cache array (kap_max * 16)
 };
 
 // phase mark from any CTA (the first job CTA records the job timeline)
@@ -967,8 +971,12 @@ __device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGe
 }
 
 // R: stacked step rows of the minibatch; bn: samples.
+// keep: this CTA owns the slice for the whole launch (not a sampler), so the
+// parameters, Adam moments and trainable mask of the slice stay in shared
+// memory across minibatches (loaded at the first step, moments written back
+// at the last); otherwise they are read from and written to global memory.
 __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64_t R, int step,
-                             float* sm) {
+                             float* sm, bool keep) {
   const TDims& dm = a.dm;
   const int tid = threadIdx.x;
   const JobGeo geo = job_geo(dm, jb);
@@ -1042,6 +1050,32 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64
     const float gv = gout[k * nbp + c];
     if (a.mode == TT_MODE_GRAD) {
       a.grad_out[p] = gv;
+    } else if (keep) {
+      float* pc = sm + a.pc_off + k * nbp + c;
+      float pp, mm, vv, tr;
+      if (step == 0) {
+        pp = __ldcg(a.prm + p);
+        mm = a.m[p];
+        vv = a.v[p];
+        tr = (!a.trainable || a.trainable[p]) ? 1.f : 0.f;
+        pc[3 * a.pc_n] = tr;
+      } else {
+        pp = pc[0];
+        mm = pc[a.pc_n];
+        vv = pc[2 * a.pc_n];
+        tr = pc[3 * a.pc_n];
+      }
+      if (tr != 0.f) {
+        adam_update<float>(pp, gv, mm, vv, a.hyp, c1, c2);
+        a.prm[p] = pp;
+        if (step == a.n_steps - 1) {
+          a.m[p] = mm;
+          a.v[p] = vv;
+        }
+      }
+      pc[0] = pp;
+      pc[a.pc_n] = mm;
+      pc[2 * a.pc_n] = vv;
     } else if (!a.trainable || a.trainable[p]) {
       float pp = __ldcg(a.prm + p), mm = a.m[p], vv = a.v[p];
       adam_update<float>(pp, gv, mm, vv, a.hyp, c1, c2);
@@ -1103,7 +1137,6 @@ __device__ float fast_rank_loss(const float* y, const float* s, int n, float* ds
 __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* sm = reinterpret_cast<float*>(smem_raw);
-  __shared__ int s_jT[kMaxFastB];
   __shared__ int64_t s_R;
   __shared__ int s_stop;
   const TDims& dm = a.dm;
@@ -1203,6 +1236,14 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       if (!sampler) break;  // idle CTA
       continue;
     }
+    // minibatch row count: every sample CTA published its step count before
+    // signalling the forward counter, so this read is off the critical path
+    wait_counter(a.ctr + 0, cum, !sampler);
+    if (tid == 0) {
+      int64_t R = 0;
+      for (int i = 0; i < bn; ++i) R += __ldcg(a.meta + i);
+      s_R = R;
+    }
     // this CTA's jobs, attention/head group first, then the LSTM layers top-down
     // (the order in which the samples publish their backward operands)
     for (int j = last_job; j >= 0; j -= G) {
@@ -1210,16 +1251,9 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       wait_counter(a.ctr + ctr_bwd(g), cum, !sampler);
       if (r == a.B % G) phase_mark_any(step, 20);
       if (tid == 0) s_stop = __ldcg(a.status) >= 0;
-      for (int i = tid; i < bn; i += kThreads) s_jT[i] = (int)__ldcg(a.meta + i);
-      __syncthreads();
-      if (tid == 0) {
-        int64_t R = 0;
-        for (int i = 0; i < bn; ++i) R += s_jT[i];
-        s_R = R;
-      }
       __syncthreads();
       if (s_stop) break;
-      fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm);
+      fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm, !sampler && my_jobs == 1);
       signal_counter(a.ctr + ctr_adam(dm, g), 1);
       if (r == a.B % G) phase_mark_any(step, 21);
     }
@@ -1232,7 +1266,8 @@ struct FastPlan {
   FastSmem sl;
   FastXch xl;
   size_t smem;
-  int64_t rch;
+  int64_t rch, pc_off;
+  int pc_n;
   int n_jobs;
 };
 
@@ -1254,8 +1289,9 @@ inline bool fast_plan(const TDims& dm, int B, int grid, FastPlan& p) {
   p.sl = make_fast_smem(dm, B);
   p.xl = make_fast_xch(dm, B);
   p.n_jobs = fast_n_jobs(dm);
-  const size_t static_smem = 64;
-  const size_t budget = (size_t)optin - static_smem - 1024;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, tuner_train_fast_kernel) != cudaSuccess) return false;
+  const size_t budget = (size_t)optin - fa.sharedSizeBytes - 256;
   size_t need = (size_t)p.sl.total * sizeof(float);
   if (need > budget) return false;
   // job staging: at least Tmax rows of the widest job
@@ -1271,6 +1307,8 @@ inline bool fast_plan(const TDims& dm, int B, int grid, FastPlan& p) {
   if (p.rch > all_rows) p.rch = all_rows;
   need = std::max(need, (size_t)(job_fixed + p.rch * (kap_max + nbp)) * sizeof(float));
   p.smem = need;
+  p.pc_n = kap_max * nbp;
+  p.pc_off = (int64_t)(need / sizeof(float)) - 4 * (int64_t)p.pc_n;
   return true;
 }
 
@@ -1280,6 +1318,8 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   a.xl = p.xl;
   a.n_jobs = p.n_jobs;
   a.rch = p.rch;
+  a.pc_off = p.pc_off;
+  a.pc_n = p.pc_n;
   a.xch = reinterpret_cast<float*>(w);
   w += align_up((size_t)p.xl.total * sizeof(float), 256);
   a.meta = reinterpret_cast<int64_t*>(w);
