@@ -892,8 +892,10 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
 // [n][kap] = [segment 1 (w1) | h_prev (32, LSTM) | ones/pad chunk], B rows
 // [n][nbp] = the job's column slice.  The exchange is stacked by row, so
 // every operand is one flat loop of 16-B cp.async.cg copies (L2 -> smem).
+// what: 1 = A operand only (forward data: may be staged before the
+// backward of the minibatch is done), 2 = B operand only, 3 = both.
 __device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGeo& g, int64_t r0,
-                               int64_t r1, float* As, float* Bs) {
+                               int64_t r1, float* As, float* Bs, int what = 3) {
   const TDims& dm = a.dm;
   const FastXch& X = a.xl;
   const int tid = threadIdx.x;
@@ -946,6 +948,7 @@ __device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGe
   }
   A1 += r0 * lda1;
   B1 += r0 * ldb1;
+  if (what & 1) {
   for (int e = tid; e < n * q1; e += kThreads) {
     const int r = e / q1, q = e - r * q1;
     cp_async16(As + r * kap + q * 4, A1 + (int64_t)r * lda1 + q * 4);
@@ -962,10 +965,12 @@ __device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGe
     const float* src = xc + X.cst + (g.bias ? 4 : 0);
     for (int r = tid; r < n; r += kThreads) cp_async16(As + r * kap + c0, src);
   }
-  for (int e = tid; e < n * nq; e += kThreads) {
-    const int r = e / nq, q = e - r * nq;
-    cp_async16(Bs + r * nbp + q * 4, B1 + (int64_t)r * ldb1 + q * 4);
   }
+  if (what & 2)
+    for (int e = tid; e < n * nq; e += kThreads) {
+      const int r = e / nq, q = e - r * nq;
+      cp_async16(Bs + r * nbp + q * 4, B1 + (int64_t)r * ldb1 + q * 4);
+    }
   cp_async_wait_all();
   __syncthreads();
 }
@@ -975,8 +980,15 @@ __device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGe
 // parameters, Adam moments and trainable mask of the slice stay in shared
 // memory across minibatches (loaded at the first step, moments written back
 // at the last); otherwise they are read from and written to global memory.
+__device__ __forceinline__ int64_t job_rows(const TDims& dm, const FastJob& jb, int bn, int64_t R) {
+  return jb.kind == FJ_LSTM || jb.kind == FJ_WK || jb.kind == FJ_WV
+             ? R
+             : (jb.kind == FJ_WQ || jb.kind == FJ_WO ? (int64_t)bn * dm.U : bn);
+}
+
+// a_staged: the A operand of all rows was staged by the caller (single chunk).
 __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64_t R, int step,
-                             float* sm, bool keep) {
+                             float* sm, bool keep, bool a_staged) {
   const TDims& dm = a.dm;
   const int tid = threadIdx.x;
   const JobGeo geo = job_geo(dm, jb);
@@ -984,9 +996,7 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64
   const int nkb = kap / 4, ncb = nbp / 4, nblk = nkb * ncb;
   const int RG = nblk >= kThreads ? 1 : kThreads / nblk;
   (void)maxr;
-  const int64_t nrows = jb.kind == FJ_LSTM || jb.kind == FJ_WK || jb.kind == FJ_WV
-                            ? R
-                            : (jb.kind == FJ_WQ || jb.kind == FJ_WO ? (int64_t)bn * dm.U : bn);
+  const int64_t nrows = job_rows(dm, jb, bn, R);
   const int64_t rch = a.rch;  // rows per staging chunk
   float* As = sm;
   float* Bs = As + rch * kap;
@@ -1004,7 +1014,7 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64
   for (int64_t c0 = 0; c0 < nrows; c0 += rch) {
     const int64_t c1 = c0 + rch < nrows ? c0 + rch : nrows;
     __syncthreads();
-    fast_job_stage(a, jb, geo, c0, c1, As, Bs);
+    fast_job_stage(a, jb, geo, c0, c1, As, Bs, a_staged ? 2 : 3);
     if (blockIdx.x == (unsigned)(a.B % gridDim.x)) phase_mark_any(step, 22);
     const int n = (int)(c1 - c0);
     if (active) {
@@ -1246,6 +1256,20 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     }
     // this CTA's jobs, attention/head group first, then the LSTM layers top-down
     // (the order in which the samples publish their backward operands)
+    const bool keep = !sampler && my_jobs == 1;
+    bool a_staged = false;
+    if (keep) {
+      // single job: stage its A operand (forward data) while the samples run
+      // their backward, so only the B operand waits for the backward counter
+      __syncthreads();
+      const FastJob jb = fast_job(dm, last_job);
+      const int64_t nr = job_rows(dm, jb, bn, s_R);
+      if (nr <= a.rch) {
+        const JobGeo geo = job_geo(dm, jb);
+        fast_job_stage(a, jb, geo, 0, nr, sm, sm + a.rch * geo.kap, 1);
+        a_staged = true;
+      }
+    }
     for (int j = last_job; j >= 0; j -= G) {
       const int g = job_group(dm, j);
       wait_counter(a.ctr + ctr_bwd(g), cum, !sampler);
@@ -1253,7 +1277,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       if (tid == 0) s_stop = __ldcg(a.status) >= 0;
       __syncthreads();
       if (s_stop) break;
-      fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm, !sampler && my_jobs == 1);
+      fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm, keep, a_staged);
       signal_counter(a.ctr + ctr_adam(dm, g), 1);
       if (r == a.B % G) phase_mark_any(step, 21);
     }
