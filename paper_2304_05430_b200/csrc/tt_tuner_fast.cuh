@@ -40,7 +40,7 @@ __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
 
 // ------------------------------------------------------------ layouts --
 struct FastSmem {  // float offsets in dynamic shared memory (sample role)
-  int64_t x0, lbn, S, gc, cs, xz, hb, gex, K, V, alpha, pin, q, mix, pool, zb, a1, red, lb, dS, dS2, dZ, dK,
+  int64_t x0, lbn, ctxs, S, gc, cs, xz, hb, gex, K, V, alpha, pin, q, mix, pool, zb, a1, red, lb, dS, dS2, dZ, dK,
       dV, dlg, dmix, dq, dpool, da1, W, total;
 };
 
@@ -61,6 +61,7 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   const int TM = d.Tmax;
   s.x0 = seg((int64_t)TM * round4(d.d0));
   s.lbn = seg(B);
+  s.ctxs = seg(d.C);
   s.S = seg((int64_t)d.L * TM * kFD);
   s.gc = seg((int64_t)d.L * 2 * TM * kFG);
   s.cs = seg((int64_t)d.L * 2 * TM * kFH);
@@ -89,7 +90,7 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   s.dpool = seg(kFD);
   s.da1 = seg(kHeadHidden);
   // attention + head weights, row stride 68: [Wq|Wk|Wv|Wo|bq|bo] then [W1|b1|W2]
-  s.W = seg((int64_t)(4 * kFD + 2) * kLdA + (int64_t)(kFD + d.C + 2) * kLdA);
+  s.W = seg((int64_t)(4 * kFD + 2) * kLdA + (int64_t)(kFD + d.C + 3) * kLdA);  // + b2 row
   s.total = o;
   return s;
 }
@@ -237,10 +238,17 @@ struct FastArgs {
   int pc_n;            // floats per cache array (kap_max * 16)
 };
 
-// phase mark from any CTA (the first job CTA records the job timeline)
-// (%globaltimer, ns: comparable across SMs, unlike clock64)
-__device__ __forceinline__ void phase_mark_any(int step, int i) {
-  if (threadIdx.x == 0 && step == g_prof_step) {
+// Phase marks (debug, tt_debug_profile_step).  The profiled step is read
+// from global memory ONCE per launch into shared memory: a global read per
+// mark would cost an L2 round trip after every fence (they invalidate L1).
+__shared__ int s_prof;
+// CTA 0, clock64 (cycles)
+__device__ __forceinline__ void fmark(int step, int i) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && step == s_prof) g_phase[i] = clock64();
+}
+// any CTA, %globaltimer (ns: comparable across SMs, unlike clock64)
+__device__ __forceinline__ void fmark_any(int step, int i) {
+  if (threadIdx.x == 0 && step == s_prof) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     g_phase[i] = (long long)t;
@@ -501,6 +509,68 @@ __device__ __forceinline__ void frow_mv(const float* W, const float* v, float* o
   __syncthreads();
 }
 
+// out[c] = bias[c] + sum_{k < K} v[k] W[k*kLdA + c] for c < 64, all threads:
+// thread (c, part) sums rows k in [part*KQ, part*KQ + KQ) with four
+// independent accumulators (latency-bound otherwise); the four partials are
+// combined in fixed order.  Ends synced.
+__device__ __forceinline__ void fcol_mv(const float* v, const float* W, int K, const float* bias,
+                                        float* out, float* red) {
+  const int c = threadIdx.x & 63, part = threadIdx.x >> 6;
+  const int KQ = (K + 3) >> 2;
+  const int k0 = part * KQ, k1 = min(K, k0 + KQ);
+  const float* w = W + c;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    a0 = fmaf(v[k], w[k * kLdA], a0);
+    a1 = fmaf(v[k + 1], w[(k + 1) * kLdA], a1);
+    a2 = fmaf(v[k + 2], w[(k + 2) * kLdA], a2);
+    a3 = fmaf(v[k + 3], w[(k + 3) * kLdA], a3);
+  }
+  for (; k < k1; ++k) a0 = fmaf(v[k], w[k * kLdA], a0);
+  red[threadIdx.x] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (threadIdx.x < 64)
+    out[c] = bias[c] + ((red[c] + red[64 + c]) + (red[128 + c] + red[192 + c]));
+  __syncthreads();
+}
+
+// dot(a[0:n], b[0:n]) of two smem rows, four accumulators (n % 4 == 0)
+__device__ __forceinline__ float fdot4(const float* a, const float* b, int n) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  for (int d = 0; d < n; d += 4) {
+    a0 = fmaf(a[d], b[d], a0);
+    a1 = fmaf(a[d + 1], b[d + 1], a1);
+    a2 = fmaf(a[d + 2], b[d + 2], a2);
+    a3 = fmaf(a[d + 3], b[d + 3], a3);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+// out[c] = scale * sum_{t < T} w[h(c)][t] M[t*kLdK + c] for c < 64 (h(c) = c / dh,
+// w rows of stride TM), all threads: thread (c, part) sums t = part, part+4,
+// ...; partials combined in fixed order.  Optional copy to `out2`.  Ends synced.
+__device__ __forceinline__ void fmix(const float* w, int TM, int dh, const float* M, int T,
+                                     float scale, float* out, float* out2, float* red) {
+  const int c = threadIdx.x & 63, part = threadIdx.x >> 6;
+  const float* wr = w + (c / dh) * TM;
+  float a0 = 0.f, a1 = 0.f;
+  int t = part;
+  for (; t + 4 < T; t += 8) {
+    a0 = fmaf(wr[t], M[t * kLdK + c], a0);
+    a1 = fmaf(wr[t + 4], M[(t + 4) * kLdK + c], a1);
+  }
+  if (t < T) a0 = fmaf(wr[t], M[t * kLdK + c], a0);
+  red[threadIdx.x] = a0 + a1;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const float r = ((red[c] + red[64 + c]) + (red[128 + c] + red[192 + c])) * scale;
+    out[c] = r;
+    if (out2) out2[c] = r;
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------- sample forward --
 // All 256 threads.  Returns yhat (valid in every thread after the call).
 // rs: this sample's first row in the stacked exchange; slot: its minibatch slot.
@@ -554,14 +624,14 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
       WReg wh;
       load_wh_cols(wh, a.prm + dm.wh[l][warp >> 1], warp & 1);
       named_barrier(1, kThreads);  // projection done
-      if (warp == 0) phase_mark(step, 25 + l);
+      if (warp == 0) fmark(step, 25 + l);
       const int dir = warp >> 1;
       fast_rec_fwd(wh, dir, warp & 1, T, TM, xz, S + (int64_t)l * TM * kFD,
                    a.xch + X.S + ((int64_t)l * X.Rmax + rs) * kFD,
                    a.xch + X.H + (((int64_t)l * 2 + dir) * X.Rmax + rs) * kFH,
                    sm + L.gc + (int64_t)l * 2 * TM * kFG, sm + L.cs + (int64_t)l * 2 * TM * kFH,
                    sm + L.hb, sm + L.gex);
-      if (warp == 0) phase_mark(step, 2 + l);
+      if (warp == 0) fmark(step, 2 + l);
     } else {
       named_barrier(1, kThreads);
       if (l == 0) {
@@ -571,13 +641,15 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
         const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
         const float* src1 = a.prm + dm.Wq;
         const float* src2 = a.prm + dm.W1;
-        const int tot = (rows1 + rows2) * 16;
+        const int tot = (rows1 + rows2) * 16 + 1;  // + the chunk holding b2
         for (int e = tid - 128; e < tot; e += kThreads - 128) {
           const int row = e >> 4, q = e & 15;
           if (row < rows1)
             cp_async16(W + row * kLdA + q * 4, src1 + e * 4);
-          else
+          else if (e + 1 < tot)
             cp_async16(W1s + (row - rows1) * kLdA + q * 4, src2 + (e - rows1 * 16) * 4);
+          else  // b2 is the last parameter: a 4-byte copy stays inside the buffer
+            cp_async4(W1s + (int64_t)rows2 * kLdA, src2 + (int64_t)rows2 * 64);
         }
       }
       if (l == dm.L - 1) cp_async_wait_all();
@@ -600,11 +672,16 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
   const int Z = kFD + dm.C;
   const float* b1 = W1s + (int64_t)Z * kLdA;
   const float* W2 = W1s + (int64_t)(Z + 1) * kLdA;
-  const float b2 = __ldcg(a.prm + dm.b2);
+  const float b2 = W1s[(int64_t)(Z + 2) * kLdA];  // staged with the head block
   if (tid < kFD) {
-    float acc = 0.f;
-    for (int t = 0; t < T; ++t) acc += Sl[(int64_t)t * kFD + tid];
-    pool[tid] = acc / (float)(T > 1 ? T : 1);
+    float a0 = 0.f, a1 = 0.f;
+    int t = 0;
+    for (; t + 1 < T; t += 2) {
+      a0 += Sl[(int64_t)t * kFD + tid];
+      a1 += Sl[(int64_t)(t + 1) * kFD + tid];
+    }
+    if (t < T) a0 += Sl[(int64_t)t * kFD + tid];
+    pool[tid] = (a0 + a1) / (float)(T > 1 ? T : 1);
   }
   {
     const int cc = tid & 127, grp = tid >> 7, col = cc & 63;
@@ -616,27 +693,24 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     for (int t = grp; t < T; t += 2) dst[(int64_t)t * kLdK + col] = dot_reg<kFD>(Sl + (int64_t)t * kFD, wc);
   }
   __syncthreads();
-  phase_mark(step, 8);
+  fmark(step, 8);
   const float sq = sqrtf((float)dh);
   float* const xpin = a.xch + X.pin + (int64_t)slot * U * kFD;
   float* const xmix = a.xch + X.mix + (int64_t)slot * U * kFD;
   for (int u = 0; u < U; ++u) {
     float* q = sm + L.q + u * kFD;
-    bmv_col<float>(pool, Wq, kLdA, kFD, kFD, bq, q, red);
     if (tid < kFD) {
       sm[L.pin + u * kFD + tid] = pool[tid];
       xpin[u * kFD + tid] = pool[tid];
     }
+    fcol_mv(pool, Wq, kFD, bq, q, red);
     float* al = sm + L.alpha + (int64_t)u * heads * TM;
     for (int h = warp; h < heads; h += kThreads / 32) {
       const float* qh = q + h * dh;
       float* ar = al + (int64_t)h * TM;
       float mx = -INFINITY;
       for (int t = lane; t < T; t += 32) {
-        const float* kr = K + (int64_t)t * kLdK + h * dh;
-        float acc = 0.f;
-        for (int d = 0; d < dh; ++d) acc += qh[d] * kr[d];
-        acc = acc / sq;
+        const float acc = fdot4(qh, K + (int64_t)t * kLdK + h * dh, dh) / sq;
         ar[t] = acc;
         mx = fmaxf(mx, acc);
       }
@@ -652,26 +726,19 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     }
     __syncthreads();
     float* mix = sm + L.mix + u * kFD;
-    if (tid < kFD) {
-      const float* ar = al + (int64_t)(tid / dh) * TM;
-      float acc = 0.f;
-      for (int t = 0; t < T; ++t) acc += ar[t] * V[(int64_t)t * kLdK + tid];
-      mix[tid] = acc;
-      xmix[u * kFD + tid] = acc;
-    }
-    __syncthreads();
-    bmv_col<float>(mix, Wo, kLdA, kFD, kFD, bo, pool, red);
-    phase_mark(step, u == 0 ? 9 : 17);
+    fmix(al, TM, dh, V, T, 1.f, mix, xmix + u * kFD, red);
+    fcol_mv(mix, Wo, kFD, bo, pool, red);
+    fmark(step, u == 0 ? 9 : 17);
   }
   float* zb = sm + L.zb;
   for (int i = tid; i < round4(Z); i += kThreads) {
-    const float vz = i < kFD ? pool[i] : (i < Z ? __ldg(a.ctx + idx * dm.C + (i - kFD)) : 0.f);
+    const float vz = i < kFD ? pool[i] : (i < Z ? sm[L.ctxs + (i - kFD)] : 0.f);
     if (i < Z) zb[i] = vz;
     a.xch[X.z + (int64_t)slot * X.zw + i] = vz;
   }
   __syncthreads();
   float* a1 = sm + L.a1;
-  bmv_col<float>(zb, W1s, kLdA, Z, kHeadHidden, b1, a1, red);
+  fcol_mv(zb, W1s, Z, b1, a1, red);
   float yh = 0.f;
   if (warp == 0) {
     float acc = 0.f;
@@ -761,7 +828,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
   if (tid < 4) a.xch[X.dl + (int64_t)slot * 4 + tid] = tid == 0 ? dl : 0.f;
   __syncthreads();
   frow_mv(W1s, da1, dpool, red);
-  phase_mark(step, 18);
+  fmark(step, 18);
   // ---- attention passes in reverse (tuner.py:310-328)
   const float sq = sqrtf((float)dh);
   for (int u = U - 1; u >= 0; --u) {
@@ -772,8 +839,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
     for (int h = warp; h < heads; h += kThreads / 32) {
       float sacc = 0.f;
       for (int t = lane; t < T; t += 32) {
-        float da = 0.f;
-        for (int d = 0; d < dh; ++d) da += dmix[h * dh + d] * V[(int64_t)t * kLdK + h * dh + d];
+        const float da = fdot4(dmix + h * dh, V + (int64_t)t * kLdK + h * dh, dh);
         dlg[h * TM + t] = da;
         sacc += da * al[h * TM + t];
       }
@@ -793,16 +859,9 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
         dK[i] += dk;
       }
     }
-    if (tid < kFD) {
-      const int h = tid / dh;
-      float acc = 0.f;
-      for (int t = 0; t < T; ++t) acc += dlg[h * TM + t] * K[(int64_t)t * kLdK + tid];
-      dq[tid] = acc / sq;
-      a.xch[X.dq + ((int64_t)slot * U + u) * kFD + tid] = acc / sq;
-    }
-    __syncthreads();
+    fmix(dlg, TM, dh, K, T, 1.f / sq, dq, a.xch + X.dq + ((int64_t)slot * U + u) * kFD, red);
     frow_mv(Wq, dq, dpool, red);
-    phase_mark(step, u == U - 1 ? 19 : 24);
+    fmark(step, u == U - 1 ? 19 : 24);
   }
   // ---- dS = dpool/denom + dK Wk^T + dV Wv^T (tuner.py:331-338)
   float* dS = sm + L.dS;
@@ -831,7 +890,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
     a.xch[X.dV + rs * kFD + i] = dV[i];
   }
   __syncthreads();
-  phase_mark(step, 10);
+  fmark(step, 10);
   signal_counter(a.ctr + ctr_bwd(dm.L), 1);  // attention/head operands published
   // ---- LSTM stack in reverse (tuner.py:340-359).  Warps 0..3 run the two
   //      BPTT recurrences (a warp pair per direction); every thread holds a
@@ -863,7 +922,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
                    sm + L.cs + (int64_t)l * 2 * TM * kFH, dSa, dZ,
                    a.xch + X.dZ + (((int64_t)l * 2 + (warp >> 1)) * X.Rmax + rs) * kFG,
                    sm + L.gex);
-      if (warp == 0) phase_mark(step, 11 + (dm.L - 1 - l) * 2);
+      if (warp == 0) fmark(step, 11 + (dm.L - 1 - l) * 2);
     } else if (warp == 7 && l == dm.L - 1) {
       prefetch_next_sample(a, step, sm + L.lbn);
     }
@@ -879,7 +938,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
       dSb[i] = (part[i] + part[o + i]) + (part[2 * o + i] + part[3 * o + i]);  // dX_fw + dX_bw
     }
     __syncthreads();
-    phase_mark(step, 12 + (dm.L - 1 - l) * 2);
+    fmark(step, 12 + (dm.L - 1 - l) * 2);
     float* tmp = dSa;
     dSa = dSb;
     dSb = tmp;
@@ -1015,7 +1074,7 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64
     const int64_t c1 = c0 + rch < nrows ? c0 + rch : nrows;
     __syncthreads();
     fast_job_stage(a, jb, geo, c0, c1, As, Bs, a_staged ? 2 : 3);
-    if (blockIdx.x == (unsigned)(a.B % gridDim.x)) phase_mark_any(step, 22);
+    if (blockIdx.x == (unsigned)(a.B % gridDim.x)) fmark_any(step, 22);
     const int n = (int)(c1 - c0);
     if (active) {
       for (int rr = g; rr < n; rr += RG) {
@@ -1041,7 +1100,7 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64
     gout[((b / ncb) * 4 + (e >> 2)) * nbp + (b % ncb) * 4 + (e & 3)] = s;
   }
   __syncthreads();
-  if (blockIdx.x == (unsigned)(a.B % gridDim.x)) phase_mark_any(step, 23);
+  if (blockIdx.x == (unsigned)(a.B % gridDim.x)) fmark_any(step, 23);
   // parameter addresses of the slice and the fused Adam update
   const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
   const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
@@ -1150,7 +1209,10 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
   __shared__ int64_t s_R;
   __shared__ int s_stop;
   const TDims& dm = a.dm;
-  if (threadIdx.x == 0) s_pref = -1;
+  if (threadIdx.x == 0) {
+    s_pref = -1;
+    s_prof = g_prof_step;
+  }
   if (blockIdx.x == 0 && threadIdx.x < 8)  // constant chunks [0 0 0 0 | 1 0 0 0] for job staging
     a.xch[a.xl.cst + threadIdx.x] = threadIdx.x == 4 ? 1.f : 0.f;
   const int tid = threadIdx.x;
@@ -1165,14 +1227,14 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
     const unsigned cum = (unsigned)(b0 + bn);
     if (sampler && r < bn) {
-      phase_mark(step, 0);
+      fmark(step, 0);
       if (step > 0) {
         // layer 0 and the attention block (staged during layer 0) must be updated
         wait_counter(a.ctr + ctr_adam(dm, dm.L), (unsigned)(step * group_jobs(dm, dm.L)), false);
         wait_counter(a.ctr + ctr_adam(dm, 0), (unsigned)(step * group_jobs(dm, 0)), false);
       }
-      phase_mark(step, 1);
-      if (r == 0) phase_mark_any(step, 31);
+      fmark(step, 1);
+      if (r == 0) fmark_any(step, 31);
       // step counts, labels and slot metadata: prefetched into smem during the
       // previous step's backward (prefetch_next_sample), else loaded here
       if (s_pref != step) {
@@ -1211,14 +1273,15 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
           sm[a.sl.x0 + i] = v;
           xg[i] = v;
         }
+        for (int i = tid; i < dm.C; i += kThreads) sm[a.sl.ctxs + i] = __ldg(a.ctx + idx * dm.C + i);
       }
       __syncthreads();
       const float yh = fast_sample_fwd(a, sm, rs, r, r0, T, idx, step);
-      phase_mark(step, 5);
+      fmark(step, 5);
       if (tid == 0) a.yhat_buf[r] = yh;
       signal_counter(a.ctr + 0, 1);
       wait_counter(a.ctr + 0, cum, false);
-      phase_mark(step, 6);
+      fmark(step, 6);
       for (int i = tid; i < bn; i += kThreads) lb[bn + i] = __ldcg(a.yhat_buf + i);
       __syncthreads();
       const float loss = a.loss_kind == TT_LOSS_RANK
@@ -1232,14 +1295,14 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
         }
       }
       __syncthreads();
-      phase_mark(step, 7);
+      fmark(step, 7);
       if (!s_stop) {
         fast_sample_bwd(a, sm, rs, r, T, lb[2 * bn + r], yh, step);
       } else {
         for (int g = 0; g <= dm.L; ++g) signal_counter(a.ctr + ctr_bwd(g), 1);  // wake the jobs
       }
-      phase_mark(step, 16);
-      if (r == 0) phase_mark_any(step, 30);
+      fmark(step, 16);
+      if (r == 0) fmark_any(step, 30);
       if (s_stop) break;
     }
     if (my_jobs == 0) {
@@ -1273,13 +1336,13 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     for (int j = last_job; j >= 0; j -= G) {
       const int g = job_group(dm, j);
       wait_counter(a.ctr + ctr_bwd(g), cum, !sampler);
-      if (r == a.B % G) phase_mark_any(step, 20);
+      if (r == a.B % G) fmark_any(step, 20);
       if (tid == 0) s_stop = __ldcg(a.status) >= 0;
       __syncthreads();
       if (s_stop) break;
       fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm, keep, a_staged);
       signal_counter(a.ctr + ctr_adam(dm, g), 1);
-      if (r == a.B % G) phase_mark_any(step, 21);
+      if (r == a.B % G) fmark_any(step, 21);
     }
     if (s_stop) break;
   }
@@ -1304,7 +1367,8 @@ inline size_t fast_ws_bytes(const TDims& dm, int B) {
 // Eligible: fp32, hidden 32, one sample per CTA, every per-sample cache in
 // shared memory.  Returns false (generic kernel) otherwise.
 inline bool fast_plan(const TDims& dm, int B, int grid, FastPlan& p) {
-  if (dm.H != kFH || B > grid || B > kMaxFastB || B < 1 || dm.Tmax > 32 || dm.heads < 1)
+  if (dm.H != kFH || B > grid || B > kMaxFastB || B < 1 || dm.Tmax > 32 || dm.heads < 1 ||
+      kFD % (4 * dm.heads) != 0)
     return false;
   int dev = 0, optin = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
