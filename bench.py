@@ -399,7 +399,10 @@ def run_b200(args, world, rank):
     achieved = flops / t_mean / 1e12
     roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": traffic,
-            "kernel": "tuner_train_kernel<float,32> (one launch = one epoch)",
+            "kernel": "tuner_train_fast_kernel (latency path, one launch = one epoch)",
+            "note": "B=16 minibatches are a sequential chain of 16,384 dependent Adam steps; the kernel "
+                    "is bound by the per-step critical path (recurrences, barriers, L2 hand-offs), "
+                    "not by tensor or HBM throughput (DESIGN.md section 3)",
             "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback"}
 
     # ---- e2e through the public API (host step sequences -> fit epoch)

@@ -40,6 +40,39 @@ class HostPrograms:
 def pack_sequences(seqs, step_width: int | None = None, ctx_len: int | None = None) -> HostPrograms:
     if len(seqs) == 0:
         raise DataValidationError("empty sequence batch")
+    fast = _pack_fast(seqs, step_width, ctx_len)
+    if fast is not None:
+        return fast
+    return _pack_checked(seqs, step_width, ctx_len)
+
+
+def _pack_fast(seqs, step_width, ctx_len) -> HostPrograms | None:
+    """Vectorised packing for well-formed input (numpy does the shape checks);
+    None sends malformed input to the per-item path for the exact message."""
+    n = len(seqs)
+    try:
+        st = [s.steps for s in seqs]
+        cx = [s.context for s in seqs]
+        lens = np.fromiter(map(len, st), dtype=np.int64, count=n)
+        clens = np.fromiter(map(len, cx), dtype=np.int64, count=n)
+        steps = np.concatenate(st, axis=0, dtype=np.float64)
+        ctx = np.concatenate(cx, axis=0, dtype=np.float64)
+    except (ValueError, TypeError, AttributeError):
+        return None
+    C = int(clens[0])
+    if (steps.ndim != 2 or ctx.ndim != 1 or lens.min() < 1 or steps.shape[0] != int(lens.sum())
+            or np.any(clens != C) or ctx.shape[0] != n * C):
+        return None
+    ctx = ctx.reshape(n, C)
+    if (step_width is not None and steps.shape[1] != step_width) or (
+            ctx_len is not None and ctx.shape[1] != ctx_len):
+        return None
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    return HostPrograms(steps, off, ctx)
+
+
+def _pack_checked(seqs, step_width, ctx_len) -> HostPrograms:
     steps = [np.asarray(s.steps, dtype=np.float64) for s in seqs]
     ctxs = [np.asarray(s.context, dtype=np.float64) for s in seqs]
     d0 = steps[0].shape[1] if steps[0].ndim == 2 else -1
