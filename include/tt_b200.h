@@ -111,6 +111,19 @@ int tt_tuner_predict_f64(const double *d_params, const double *d_steps,
                          int32_t step_width, int32_t ctx_len, int32_t max_steps,
                          double *d_yhat, void *d_ws, size_t ws_bytes, tt_stream_t stream);
 
+/* Tensor-core scoring (tcgen05 kind::tf32, csrc/tt_tuner_tc.cu): the same
+ * forward as tt_tuner_predict_f32 with every dense layer (LSTM gates, Wq,
+ * Wk, Wv, Wo, W1) as a 128-program GEMM tile; tf32 operands, fp32
+ * accumulation and activations ("tf32" precision mode, its own tolerance).
+ * Requires hidden = 32, heads in {1, 2}, step_width <= 32, ctx_len <= 64;
+ * TT_EINVAL otherwise.  d_ws: tt_tuner_predict_tf32_workspace_bytes(max_steps). */
+size_t tt_tuner_predict_tf32_workspace_bytes(int32_t max_steps);
+int tt_tuner_predict_tf32(const float *d_params, const float *d_steps,
+                          const int64_t *d_row_offsets, const float *d_ctx, int64_t n,
+                          int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                          int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                          float *d_yhat, void *d_ws, size_t ws_bytes, tt_stream_t stream);
+
 /* Training (tuner.py:427-466) / gradients (tuner.py:364-376).
  * d_order lists sample indices; minibatch k is d_order[k*B, min((k+1)*B, n_order)).
  * TT_MODE_TRAIN: every minibatch runs forward, loss, backward, a deterministic

@@ -258,6 +258,12 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
     def _dev_params(self, dims):
         return self._device_flat(dims["names"])
 
+    @staticmethod
+    def _tc_eligible(dims, prog) -> bool:
+        """Shapes the tcgen05 scoring kernel (csrc/tt_tuner_tc.cu) covers."""
+        return (dims["H"] == 32 and dims["heads"] in (1, 2) and dims["d0"] <= 32
+                and dims["C"] <= 64 and prog.max_steps <= 512)
+
     def _predict_programs(self, prog: DevicePrograms, dims, flat=None):
         t = _device.torch()
         prec = self._prec()
@@ -265,8 +271,12 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         flat = self._dev_params(dims) if flat is None else flat
         out = _device.empty(prog.n, _device.real_dtype(prec))
         lib = _lib.load()
-        nbytes = lib.tt_tuner_predict_workspace_bytes(int(prec == "fp64"), dims["L"], dims["H"],
-                                                      prog.max_steps)
+        if prec == "tf32" and self._tc_eligible(dims, prog):
+            fn = "tt_tuner_predict_tf32"  # tcgen05 tensor-core scoring
+            nbytes = lib.tt_tuner_predict_tf32_workspace_bytes(prog.max_steps)
+        else:
+            nbytes = lib.tt_tuner_predict_workspace_bytes(int(prec == "fp64"), dims["L"],
+                                                          dims["H"], prog.max_steps)
         ws = _device.workspace(nbytes, "tuner_predict")
         _lib.call(fn, flat.data_ptr(), prog.steps.data_ptr(), prog.offsets.data_ptr(),
                   prog.ctx.data_ptr(), prog.n, dims["L"], dims["H"], dims["heads"], dims["U"],
