@@ -165,6 +165,8 @@ int tt_tuner_train_set_path(int32_t path);
  * next tuner training launches (-1 = off) and read them back (host memory). */
 int tt_debug_profile_step(int32_t step);
 int tt_debug_phase_times(int64_t *h_out, int32_t n);
+/* Debug aid: clock64 marks of the tensor-core scoring kernel's first tile. */
+int tt_debug_tc_phase_times(int64_t *h_out, int32_t n);
 
 /* ------------------------------------------------------------ cost MLP --
  * replaces estimators/mlp.py CostMLP._forward/_backward/fit/predict

@@ -35,9 +35,19 @@ namespace tt {
 
 using namespace sm100;
 
+// clock64 marks of CTA 0 / row thread 0 on its first tile (debug aid,
+// tt_debug_tc_phase_times): 0 tile start, 1+l after LSTM layer l, 20 after
+// attention, 21 end; layer 1 step 1: 22 before A, 23 A arrived, 24 gates
+// ready, 25 epilogue done.
+static __device__ long long g_tc_phase[32];
+#define TC_MARK(cond, i) \
+  do {                   \
+    if (cond) g_tc_phase[i] = clock64(); \
+  } while (0)
+
 namespace sc {
 constexpr int kRows = 128;
-constexpr int kThreads = 160;
+constexpr int kThreads = 288;  // warp 0: MMA; warps 1..4 and 5..8: two row groups
 constexpr int kH = 32, kD = 64, kG = 128;
 constexpr uint32_t kColG = 0;    // G_fw [0,128) G_bw [128,256) ; attention D [0,128)
 constexpr uint32_t kColA = 256;  // A_fw [256,256+K) A_bw [256+K,256+2K) ; attention A [256,384)
@@ -54,11 +64,14 @@ struct ScArgs {
   int64_t n;
   float* yhat;
   float* scratch;       // per CTA: [2][128][Tmax][64] layer outputs (ping-pong)
+  const unsigned char* img;  // prepared B^T images (tuner_tc_prepare_kernel)
   int64_t scr_per_cta;  // floats
 };
 
 struct __align__(8) ScBars {
   uint64_t a_full, d_full;
+  uint64_t a_dir[2], d_dir[2];  // LSTM hand-offs per direction
+  uint64_t w_full;              // weight image landed
   uint32_t tmem_base;
   int tmax;
 };
@@ -75,12 +88,88 @@ __device__ void sc_stage(unsigned char* dst, int N, int kbase, int Kcnt, const f
   }
 }
 
+__host__ __device__ inline int sc_slot_floats(int Tmax) {
+  return 2 * sc::kD > Tmax * sc::kMaxHeads ? 2 * sc::kD : Tmax * sc::kMaxHeads;
+}
+
+__device__ __forceinline__ void cp_async16_cg(float* s, const float* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Byte sizes / offsets of the per-layer LSTM images ([Wx_d ; Wh_d]^T for
+// d = fw, bw) and of the attention/head image, all in the shared-memory
+// byte layout (1024-B aligned atoms, so the swizzle is position independent).
+__host__ __device__ inline uint32_t sc_lstm_image_bytes(int l) {
+  return 2u * (uint32_t)(((l == 0 ? 32 : 64) + 32) / 32) * (128u * 128u);
+}
+__host__ __device__ inline int64_t sc_lstm_image_off(int l) {
+  int64_t o = 0;
+  for (int i = 0; i < l; ++i) o += sc_lstm_image_bytes(i);
+  return o;
+}
+__host__ __device__ inline uint32_t sc_attn_image_bytes(const TDims& dm) {
+  const int NK = dm.heads * 64, Zp = (64 + dm.C + 31) & ~31;
+  return (uint32_t)(2 * 64 * 128 + 2 * NK * 128 + (NK / 32) * 64 * 128 + 2 * 64 * 128 +
+                    (Zp / 32) * 64 * 128);
+}
+__host__ __device__ inline int64_t sc_attn_image_off(const TDims& dm) { return sc_lstm_image_off(dm.L); }
+
 // D[tmem] = A[tmem](128 x K) . B (N rows K-major SW128 at b_smem); one lane.
 __device__ __forceinline__ void sc_issue(uint32_t d, uint32_t a, uint32_t b_smem, int N, int K) {
   const uint32_t idesc = idesc_tf32(sc::kRows, N);
   for (int kk = 0; kk < K / 8; ++kk) {
     const uint64_t bd = sw128_desc(b_smem + (kk >> 2) * (N * 128) + (kk & 3) * 32);
     mma_tf32_ts(d, a + kk * 8, bd, idesc, kk != 0);
+  }
+}
+
+// Attention/head B^T image at `base` (smem or global).  All threads.
+__device__ void sc_stage_attn(unsigned char* base, const TDims& dm, const float* __restrict__ prm) {
+  using namespace sc;
+  const int heads = dm.heads, dh = dm.dh, C = dm.C;
+  const int Z = kD + C, Zp = (Z + 31) & ~31;
+  const int NK = heads * kD;
+  unsigned char* bq_t = base;
+  unsigned char* bk_t = bq_t + 2 * (kD * 128);
+  unsigned char* bv_t = bk_t + 2 * (NK * 128);
+  unsigned char* bo_t = bv_t + (NK / 32) * (kD * 128);
+  unsigned char* b1_t = bo_t + 2 * (kD * 128);
+  sc_stage(bq_t, kD, 0, kD, prm + dm.Wq, kD, kD);
+  sc_stage(bo_t, kD, 0, kD, prm + dm.Wo, kD, kD);
+  sc_stage(b1_t, kD, 0, Zp, prm + dm.W1, kHeadHidden, Z);
+  // Bk^T[h*64 + k][c] = Wk[k][c] for c in head h ; Bv^T[c][h*64 + k] = Wv[k][c] for c in head h
+  for (int i = threadIdx.x; i < NK * kD; i += blockDim.x) {
+    const int nrow = i % NK, c = i / NK;
+    const int h = nrow / kD, k = nrow % kD;
+    const float v = (c / dh == h) ? __ldg(prm + dm.Wk + (int64_t)k * kD + c) : 0.f;
+    *reinterpret_cast<float*>(bk_t + (c >> 5) * (NK * 128) + sw128_offset(nrow, c & 31)) = v;
+  }
+  for (int i = threadIdx.x; i < kD * NK; i += blockDim.x) {
+    const int c = i % kD, kk = i / kD;
+    const int h = kk / kD, k = kk % kD;
+    const float v = (c / dh == h) ? __ldg(prm + dm.Wv + (int64_t)k * kD + c) : 0.f;
+    *reinterpret_cast<float*>(bv_t + (kk >> 5) * (kD * 128) + sw128_offset(c, kk & 31)) = v;
+  }
+}
+
+// Builds the B^T images of every LSTM layer (block l < L) and of the
+// attention/head block (block L) in global memory, once per scoring call.
+__global__ void __launch_bounds__(256) tuner_tc_prepare_kernel(TDims dm, const float* __restrict__ prm,
+                                                                unsigned char* img) {
+  using namespace sc;
+  const int l = blockIdx.x;
+  if (l < dm.L) {
+    const int din = l == 0 ? dm.d0 : kD, kx = l == 0 ? 32 : kD, nat = (kx + kH) / 32;
+    unsigned char* base = img + sc_lstm_image_off(l);
+    for (int d = 0; d < 2; ++d) {
+      unsigned char* bd = base + d * nat * (kG * 128);
+      sc_stage(bd, kG, 0, kx, prm + dm.wx[l][d], kG, din);
+      sc_stage(bd, kG, kx, kH, prm + dm.wh[l][d], kG, kH);
+    }
+  } else {
+    sc_stage_attn(img + sc_attn_image_off(dm), dm, prm);
   }
 }
 
@@ -91,11 +180,15 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* Bs = base;                                         // B operands (128 KB)
   float* sbias = reinterpret_cast<float*>(base + kBBytes);          // 512 floats
-  float* slog = sbias + 512;                                        // [128][Tmax*heads] logits
-  ScBars* bars = reinterpret_cast<ScBars*>(slog + (int64_t)kRows * a.dm.Tmax * kMaxHeads);
+  // LSTM: per-row x slots [128][2][64]; attention: per-row logits [128][Tmax][2] (aliased)
+  float* sxs = sbias + 512;
+  float* slog = sxs;
+  ScBars* bars = reinterpret_cast<ScBars*>(sxs + (int64_t)kRows * sc_slot_floats(a.dm.Tmax));
   const TDims& dm = a.dm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool rowt = warp >= 1;
+  const int grp = (warp - 1) >> 2;           // row group (LSTM direction)
+  const bool att = rowt && grp == 0;         // attention/head row threads
   const int row = ((warp & 3) << 5) | lane;  // TMEM lane quarter = warp % 4
   const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
   const int TM = dm.Tmax, heads = dm.heads, dh = dm.dh, C = dm.C;
@@ -103,8 +196,13 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
   const uint32_t bs_addr = smem_u32(Bs);
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars->a_full, kRows);
+    mbar_init(&bars->a_full, 2 * kRows);  // both row groups arrive
     mbar_init(&bars->d_full, 1);
+    for (int d = 0; d < 2; ++d) {
+      mbar_init(&bars->a_dir[d], kRows);
+      mbar_init(&bars->d_dir[d], 1);
+    }
+    mbar_init(&bars->w_full, 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(&bars->tmem_base);
@@ -113,6 +211,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
   uint32_t ph = 0;
+  uint32_t pd[2] = {0, 0};  // phase bits of the per-direction LSTM hand-offs
   float* scr0 = a.scratch + (int64_t)blockIdx.x * a.scr_per_cta;
 
   // one GEMM hand-off: row threads have written A; the MMA lane issues.
@@ -134,6 +233,19 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
     ph ^= 1;
   };
 
+  // bulk-copy a prepared B^T image into Bs (all threads; previous readers done)
+  uint32_t pw = 0;
+  auto load_image = [&](const unsigned char* src, uint32_t bytes) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bars->w_full, bytes);
+      for (uint32_t off = 0; off < bytes; off += 32768)
+        bulk_g2s(Bs + off, src + off, bytes - off < 32768 ? bytes - off : 32768, &bars->w_full);
+    }
+    mbar_wait(&bars->w_full, pw);
+    pw ^= 1;
+  };
+
   const int64_t n_tiles = (a.n + kRows - 1) / kRows;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t p = tile * kRows + row;
@@ -149,149 +261,166 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
     if (live) atomicMax(&bars->tmax, T);
     __syncthreads();
     const int Tt = bars->tmax;
+    const bool pm = blockIdx.x == 0 && threadIdx.x == 32 && tile == blockIdx.x;
+    TC_MARK(pm, 0);
 
     // ================================================================ LSTM
-    float c_fw[kH], c_bw[kH];
+    // Per direction d its own hand-off pair (a_full[d] / d_full[d], phase
+    // bit ph_d): the MMA of one direction runs while the row threads do the
+    // other direction's epilogue, and the next step's x rows are loaded at
+    // the start of an epilogue so their L2 latency hides behind it.
+    // cell state lives in TMEM columns [448, 512) (c_fw | c_bw), not registers
+    const uint32_t Cst = tmem + lane_off + 448;
     for (int l = 0; l < dm.L; ++l) {
       const int din = l == 0 ? dm.d0 : kD;
       const int kx = l == 0 ? 32 : kD;
       const int K = kx + kH;
       const int nat = K / 32;
-      // ---- stage [Wx_d ; Wh_d]^T for both directions (+ biases)
-      __syncthreads();  // previous users of Bs are done
-      for (int d = 0; d < 2; ++d) {
-        unsigned char* bd = Bs + d * nat * (kG * 128);
-        sc_stage(bd, kG, 0, kx, a.prm + dm.wx[l][d], kG, din);
-        sc_stage(bd, kG, kx, kH, a.prm + dm.wh[l][d], kG, kH);
+      // ---- [Wx_d ; Wh_d]^T of both directions: one bulk copy of the image
+      load_image(a.img + sc_lstm_image_off(l), sc_lstm_image_bytes(l));
+      for (int d = 0; d < 2; ++d)
         for (int i = threadIdx.x; i < kG; i += blockDim.x) sbias[d * kG + i] = __ldg(a.prm + dm.bb[l][d] + i);
-      }
-      fence_proxy_async_smem();
       __syncthreads();
       const float* xin = scr0 + (int64_t)((l - 1) & 1) * kRows * TM * kD + (int64_t)row * TM * kD;
       float* xout = scr0 + (int64_t)(l & 1) * kRows * TM * kD + (int64_t)row * TM * kD;
+      // x row of direction d at step s (zeros past the program's end):
+      // layer 0 reads the raw step row into registers; layers >= 1 copy the
+      // previous layer's output row into this thread's shared-memory slot
+      // with async 16-B copies (issued one half-step ahead, no registers).
+      float* xslot = sxs + (int64_t)row * 2 * kD;
+      auto fetch_x = [&](int d, int s) {
+        if (l == 0) return;
+        const bool ok = live && s < T;
+        float* dst = xslot + d * kD;
+        if (ok) {
+          const float* src = xin + (int64_t)(d == 0 ? s : T - 1 - s) * kD;
 #pragma unroll
-      for (int j = 0; j < kH; ++j) c_fw[j] = c_bw[j] = 0.f;
-      const uint32_t Af = tmem + lane_off + kColA, Ab = Af + K;
-      const uint32_t Gf = tmem + lane_off + kColG, Gb = Gf + kG;
-      for (int s = 0; s < Tt; ++s) {
-        // tcgen05.ld/st are warp-collective: every row thread executes them;
-        // rows past their program's end compute on stale inputs (their state
-        // is dead for the rest of the layer) and never write the output.
-        const bool valid = live && s < T;
-        if (rowt) {
-          // A_d = [x_t | h] ; h is already in place from the previous step
+          for (int q = 0; q < 16; ++q) cp_async16_cg(dst + 4 * q, src + 4 * q);
+        } else {
 #pragma unroll
-          for (int d = 0; d < 2; ++d) {
-            const uint32_t Ad = d == 0 ? Af : Ab;
-            if (s == 0) {
-              float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+          for (int q = 0; q < 16; ++q) reinterpret_cast<float4*>(dst)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        cp_async_commit();
+      };
+      auto put_x = [&](int d, int s, uint32_t Ad) {
+        if (l == 0) {
+          const bool ok = live && s < T;
+          const float* xr = a.steps + (r0 + (ok ? (d == 0 ? s : T - 1 - s) : 0)) * dm.d0;
 #pragma unroll
-              for (int j0 = 0; j0 < kH; j0 += 8) tmem_st8(Ad + kx + j0, z);
+          for (int j0 = 0; j0 < 32; j0 += 16) {
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = (ok && j0 + i < din) ? __ldg(xr + j0 + i) : 0.f;
+            tmem_st16(Ad + j0, v);
+          }
+        } else {
+          cp_async_wait0();
+          const float4* x4 = reinterpret_cast<const float4*>(xslot + d * kD);
+#pragma unroll
+          for (int j0 = 0; j0 < kD; j0 += 16) {
+            float v[16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 f = x4[j0 / 4 + q];
+              v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
             }
-            const int t = d == 0 ? s : T - 1 - s;
-            if (l == 0) {
-              const float* xr = a.steps + (r0 + (valid ? t : 0)) * dm.d0;
-              for (int j0 = 0; j0 < kx; j0 += 8) {
-                float v[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[i] = (valid && j0 + i < din) ? __ldg(xr + j0 + i) : 0.f;
-                tmem_st8(Ad + j0, v);
-              }
-            } else {
-              const float4* xr = reinterpret_cast<const float4*>(xin + (int64_t)(valid ? t : 0) * kD);
-#pragma unroll
-              for (int j0 = 0; j0 < kD; j0 += 16) {
-                float v[16];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float4 f = valid ? __ldcg(xr + j0 / 4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-                  v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
-                }
-                tmem_st16(Ad + j0, v);
-              }
-            }
+            tmem_st16(Ad + j0, v);
           }
         }
-        // both directions' gates: one hand-off, two GEMMs
-        if (rowt) {
+      };
+      if (rowt) {
+        // row group `grp` runs direction d = grp: two independent recurrences,
+        // two warps per SM sub-partition, so one direction's activation math
+        // hides the other's latencies
+        const int d = grp;
+        const uint32_t Ad = tmem + lane_off + kColA + d * K;
+        const uint32_t Gd = tmem + lane_off + kColG + d * kG;
+        const uint32_t Cd = Cst + d * kH;
+        const float* bd = sbias + d * kG;
+        {
+          float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int j0 = 0; j0 < kH; j0 += 8) {
+            tmem_st8(Ad + kx + j0, z);
+            tmem_st8(Cd + j0, z);
+          }
+          fetch_x(d, 0);
+          put_x(d, 0, Ad);
           tmem_wait_st();
           tc_fence_before();
-          mbar_arrive(&bars->a_full);
-        } else if (lane == 0) {
-          mbar_wait(&bars->a_full, ph);
-          tc_fence_after();
-          sc_issue(tmem + kColG, tmem + kColA, bs_addr, kG, K);
-          sc_issue(tmem + kColG + kG, tmem + kColA + K, bs_addr + nat * (kG * 128), kG, K);
-          mma_commit(&bars->d_full);
+          mbar_arrive(&bars->a_dir[d]);
         }
-        if (rowt) {
-          mbar_wait(&bars->d_full, ph);
+        for (int s = 0; s < Tt; ++s) {
+          const bool valid = live && s < T;
+          const bool pms = pm && l == 1 && s == 1;
+          TC_MARK(pms, 22);
+          if (s + 1 < Tt) fetch_x(d, s + 1);  // in flight during the epilogue
+          mbar_wait(&bars->d_dir[d], pd[d]);
           tc_fence_after();
+          TC_MARK(pms, 24);
+          const int t = d == 0 ? s : T - 1 - s;
+          float* orow = xout + (int64_t)t * kD + d * kH;
 #pragma unroll
-          for (int d = 0; d < 2; ++d) {
-            const uint32_t Gd = d == 0 ? Gf : Gb;
-            const uint32_t Ad = d == 0 ? Af : Ab;
-            const float* bd = sbias + d * kG;
-            const int t = d == 0 ? s : T - 1 - s;
-            float* orow = xout + (int64_t)t * kD + d * kH;
+          for (int j0 = 0; j0 < kH; j0 += 8) {
+            float gi[8], gf[8], gg[8], go[8], cc[8], h[8];
+            tmem_ld8(Gd + j0, gi);
+            tmem_ld8(Gd + kH + j0, gf);
+            tmem_ld8(Gd + 2 * kH + j0, gg);
+            tmem_ld8(Gd + 3 * kH + j0, go);
+            tmem_ld8(Cd + j0, cc);
+            tmem_wait_ld();
 #pragma unroll
-            for (int j0 = 0; j0 < kH; j0 += 8) {
-              float gi[8], gf[8], gg[8], go[8], h[8];
-              tmem_ld8(Gd + j0, gi);
-              tmem_ld8(Gd + kH + j0, gf);
-              tmem_ld8(Gd + 2 * kH + j0, gg);
-              tmem_ld8(Gd + 3 * kH + j0, go);
-              tmem_wait_ld();
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const int j = j0 + i;
-                const float ig = Act<float>::sigmoid(gi[i] + bd[j]);
-                const float fg = Act<float>::sigmoid(gf[i] + bd[kH + j]);
-                const float cg = Act<float>::tanh(gg[i] + bd[2 * kH + j]);
-                const float og = Act<float>::sigmoid(go[i] + bd[3 * kH + j]);
-                float& cc = d == 0 ? c_fw[j] : c_bw[j];
-                cc = fg * cc + ig * cg;
-                h[i] = og * Act<float>::tanh(cc);
-              }
-              tmem_st8(Ad + kx + j0, h);
-              if (valid) {
-                reinterpret_cast<float4*>(orow + j0)[0] = make_float4(h[0], h[1], h[2], h[3]);
-                reinterpret_cast<float4*>(orow + j0)[1] = make_float4(h[4], h[5], h[6], h[7]);
-              }
+            for (int i = 0; i < 8; ++i) {
+              const int j = j0 + i;
+              const float ig = Act<float>::sigmoid(gi[i] + bd[j]);
+              const float fg = Act<float>::sigmoid(gf[i] + bd[kH + j]);
+              const float cg = Act<float>::tanh(gg[i] + bd[2 * kH + j]);
+              const float og = Act<float>::sigmoid(go[i] + bd[3 * kH + j]);
+              cc[i] = fg * cc[i] + ig * cg;
+              h[i] = og * Act<float>::tanh(cc[i]);
+            }
+            tmem_st8(Cd + j0, cc);
+            tmem_st8(Ad + kx + j0, h);
+            if (valid) {
+              reinterpret_cast<float4*>(orow + j0)[0] = make_float4(h[0], h[1], h[2], h[3]);
+              reinterpret_cast<float4*>(orow + j0)[1] = make_float4(h[4], h[5], h[6], h[7]);
             }
           }
+          if (s + 1 < Tt) {
+            put_x(d, s + 1, Ad);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&bars->a_dir[d]);
+          }
+          pd[d] ^= 1;
+          TC_MARK(pms, 25);
         }
-        ph ^= 1;
+      } else if (lane == 0) {
+        // MMA lane: both directions, step by step
+        for (int s = 0; s < Tt; ++s)
+          for (int d = 0; d < 2; ++d) {
+            mbar_wait(&bars->a_dir[d], pd[d]);
+            tc_fence_after();
+            sc_issue(tmem + kColG + d * kG, tmem + kColA + d * K, bs_addr + d * nat * (kG * 128), kG, K);
+            mma_commit(&bars->d_dir[d]);
+            pd[d] ^= 1;
+          }
       }
+      TC_MARK(pm, 1 + l);
     }
 
     // =========================================================== attention
     __syncthreads();
     const int L1 = (dm.L - 1) & 1;
     const float* Srow = scr0 + (int64_t)L1 * kRows * TM * kD + (int64_t)row * TM * kD;
-    // B layout: Wq^T | Bk^T | Bv^T | Wo^T | W1^T
+    // B layout: Wq^T | Bk^T | Bv^T | Wo^T | W1^T (image built by the prepare kernel)
     const int NK = heads * kD;  // r width and u width
     unsigned char* bq_t = Bs;
     unsigned char* bk_t = bq_t + 2 * (kD * 128);
     unsigned char* bv_t = bk_t + 2 * (NK * 128);
     unsigned char* bo_t = bv_t + (NK / 32) * (kD * 128);
     unsigned char* b1_t = bo_t + 2 * (kD * 128);
-    sc_stage(bq_t, kD, 0, kD, a.prm + dm.Wq, kD, kD);
-    sc_stage(bo_t, kD, 0, kD, a.prm + dm.Wo, kD, kD);
-    sc_stage(b1_t, kD, 0, Zp, a.prm + dm.W1, kHeadHidden, Z);
-    // Bk^T[h*64 + k][c] = Wk[k][c] for c in head h ; Bv^T[c][h*64 + k] = Wv[k][c] for c in head h
-    for (int i = threadIdx.x; i < NK * kD; i += blockDim.x) {
-      const int nrow = i % NK, c = i / NK;  // Bk^T row nrow, K index c
-      const int h = nrow / kD, k = nrow % kD;
-      const float v = (c / dh == h) ? __ldg(a.prm + dm.Wk + (int64_t)k * kD + c) : 0.f;
-      *reinterpret_cast<float*>(bk_t + (c >> 5) * (NK * 128) + sw128_offset(nrow, c & 31)) = v;
-    }
-    for (int i = threadIdx.x; i < kD * NK; i += blockDim.x) {
-      const int c = i % kD, kk = i / kD;  // Bv^T row c, K index kk = h*64 + k
-      const int h = kk / kD, k = kk % kD;
-      const float v = (c / dh == h) ? __ldg(a.prm + dm.Wv + (int64_t)k * kD + c) : 0.f;
-      *reinterpret_cast<float*>(bv_t + (kk >> 5) * (kD * 128) + sw128_offset(c, kk & 31)) = v;
-    }
+    load_image(a.img + sc_attn_image_off(dm), sc_attn_image_bytes(dm));
     for (int i = threadIdx.x; i < kD; i += blockDim.x) {
       sbias[i] = __ldg(a.prm + dm.bq + i);
       sbias[kD + i] = __ldg(a.prm + dm.bo + i);
@@ -303,38 +432,41 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
     if (threadIdx.x == 0) sbias[2 * kD + 2 * kHeadHidden] = __ldg(a.prm + dm.b2);
     fence_proxy_async_smem();
     __syncthreads();
+    TC_MARK(pm, 26);
     const uint32_t A0 = tmem + lane_off + kColA, D0 = tmem + lane_off + kColG;
-    float pool[kD];
-    if (live) {
+    // Row group g owns head g for the per-step work (logits, softmax, u_h);
+    // group 0 writes the other GEMM operands.  pooled never lives in
+    // registers: it is written straight into the next GEMM's A columns.
+    const bool hg = rowt && grp < heads;  // this thread owns head grp
+    if (att) {
+      float pool[kD];
 #pragma unroll
       for (int k = 0; k < kD; ++k) pool[k] = 0.f;
-      for (int t = 0; t < T; ++t) {
-        const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
+      if (live) {
+        for (int t = 0; t < T; ++t) {
+          const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const float4 f = __ldcg(sr + q);
-          pool[4 * q] += f.x, pool[4 * q + 1] += f.y, pool[4 * q + 2] += f.z, pool[4 * q + 3] += f.w;
+          for (int q = 0; q < 16; ++q) {
+            const float4 f = __ldcg(sr + q);
+            pool[4 * q] += f.x, pool[4 * q + 1] += f.y, pool[4 * q + 2] += f.z, pool[4 * q + 3] += f.w;
+          }
         }
       }
       const float inv = (float)(T > 1 ? T : 1);
 #pragma unroll
-      for (int k = 0; k < kD; ++k) pool[k] = pool[k] / inv;
+      for (int j0 = 0; j0 < kD; j0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = pool[j0 + i] / inv;
+        tmem_st16(A0 + j0, v);
+      }
     }
     const float sq = sqrtf((float)dh);
-    float* lg = slog + (int64_t)row * TM * kMaxHeads;
+    // logits as [t][head][row]: lanes (rows) hit consecutive banks
+    float* lg = slog + row;
     for (int u = 0; u < dm.U; ++u) {
-      // q = pooled Wq + bq
-      if (rowt) {
-#pragma unroll
-        for (int j0 = 0; j0 < kD; j0 += 16) {
-          float v[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = live ? pool[j0 + i] : 0.f;
-          tmem_st16(A0 + j0, v);
-        }
-      }
-      gemm(tmem + kColG, tmem + kColA, smem_u32(bq_t), kD, kD);
-      if (rowt) {  // q -> A (r = q Bk)
+      gemm(tmem + kColG, tmem + kColA, smem_u32(bq_t), kD, kD);  // q = pooled Wq
+      if (att) {  // q + bq -> A (r = q Bk)
 #pragma unroll
         for (int j0 = 0; j0 < kD; j0 += 16) {
           float v[16];
@@ -345,91 +477,69 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           tmem_st16(A0 + j0, v);
         }
       }
-      gemm(tmem + kColG, tmem + kColA, smem_u32(bk_t), NK, kD);
-      float uvec[kMaxHeads * kD];
+      gemm(tmem + kColG, tmem + kColA, smem_u32(bk_t), NK, kD);  // r_h = Wk[:, h] q_h
       if (rowt) {
-        float r[kMaxHeads * kD];
+        float r[kD], uvec[kD];
+        if (hg) {
 #pragma unroll
-        for (int j0 = 0; j0 < kMaxHeads * kD; j0 += 16) {
-          if (j0 < NK) {
+          for (int j0 = 0; j0 < kD; j0 += 16) {
             float v[16];
-            tmem_ld16(D0 + j0, v);
+            tmem_ld16(D0 + grp * kD + j0, v);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 16; ++i) r[j0 + i] = v[i];
-          } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) r[j0 + i] = 0.f;
           }
         }
-        float mx[kMaxHeads], sum[kMaxHeads];
-#pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h) mx[h] = -INFINITY, sum[h] = 0.f;
-        if (live) {
+        if (hg && live) {
+          float mx = -INFINITY, sum = 0.f;
           for (int t = 0; t < T; ++t) {
             const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
-            float acc[kMaxHeads];
-#pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) acc[h] = 0.f;
+            float a0 = 0.f, a1 = 0.f;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               const float4 f = __ldcg(sr + q);
-#pragma unroll
-              for (int h = 0; h < kMaxHeads; ++h) {
-                acc[h] = fmaf(f.x, r[h * kD + 4 * q], acc[h]);
-                acc[h] = fmaf(f.y, r[h * kD + 4 * q + 1], acc[h]);
-                acc[h] = fmaf(f.z, r[h * kD + 4 * q + 2], acc[h]);
-                acc[h] = fmaf(f.w, r[h * kD + 4 * q + 3], acc[h]);
-              }
+              a0 = fmaf(f.x, r[4 * q], a0);
+              a1 = fmaf(f.y, r[4 * q + 1], a1);
+              a0 = fmaf(f.z, r[4 * q + 2], a0);
+              a1 = fmaf(f.w, r[4 * q + 3], a1);
             }
-#pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) {
-              const float v = acc[h] / sq;
-              lg[t * kMaxHeads + h] = v;
-              mx[h] = fmaxf(mx[h], v);
-            }
+            const float v = (a0 + a1) / sq;
+            lg[(t * kMaxHeads + grp) * kRows] = v;
+            mx = fmaxf(mx, v);
           }
-          for (int t = 0; t < T; ++t)
-#pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) {
-              const float e = Act<float>::exp(lg[t * kMaxHeads + h] - mx[h]);
-              lg[t * kMaxHeads + h] = e;
-              sum[h] += e;
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < kMaxHeads * kD; ++k) uvec[k] = 0.f;
-        if (live) {
           for (int t = 0; t < T; ++t) {
-            float al[kMaxHeads];
+            const float e = Act<float>::exp(lg[(t * kMaxHeads + grp) * kRows] - mx);
+            lg[(t * kMaxHeads + grp) * kRows] = e;
+            sum += e;
+          }
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) al[h] = lg[t * kMaxHeads + h] / sum[h];
+          for (int k = 0; k < kD; ++k) uvec[k] = 0.f;
+          for (int t = 0; t < T; ++t) {
+            const float al = lg[(t * kMaxHeads + grp) * kRows] / sum;
             const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
               const float4 f = __ldcg(sr + q);
-#pragma unroll
-              for (int h = 0; h < kMaxHeads; ++h) {
-                uvec[h * kD + 4 * q] = fmaf(al[h], f.x, uvec[h * kD + 4 * q]);
-                uvec[h * kD + 4 * q + 1] = fmaf(al[h], f.y, uvec[h * kD + 4 * q + 1]);
-                uvec[h * kD + 4 * q + 2] = fmaf(al[h], f.z, uvec[h * kD + 4 * q + 2]);
-                uvec[h * kD + 4 * q + 3] = fmaf(al[h], f.w, uvec[h * kD + 4 * q + 3]);
-              }
+              uvec[4 * q] = fmaf(al, f.x, uvec[4 * q]);
+              uvec[4 * q + 1] = fmaf(al, f.y, uvec[4 * q + 1]);
+              uvec[4 * q + 2] = fmaf(al, f.z, uvec[4 * q + 2]);
+              uvec[4 * q + 3] = fmaf(al, f.w, uvec[4 * q + 3]);
             }
           }
         }
+        if (hg) {
+          const bool ok = live;
 #pragma unroll
-        for (int j0 = 0; j0 < kMaxHeads * kD; j0 += 16) {
-          if (j0 < NK) {
+          for (int j0 = 0; j0 < kD; j0 += 16) {
             float v[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = uvec[j0 + i];
-            tmem_st16(A0 + j0, v);
+            for (int i = 0; i < 16; ++i) v[i] = ok ? uvec[j0 + i] : 0.f;
+            tmem_st16(A0 + grp * kD + j0, v);
           }
         }
       }
-      gemm(tmem + kColG, tmem + kColA, smem_u32(bv_t), kD, NK);  // mix = u . blockdiag(Wv)
-      if (rowt) {
+      gemm(tmem + kColG, tmem + kColA, smem_u32(bv_t), kD, NK);  // mix = [u_h] blockdiag(Wv)
+      if (att) {
 #pragma unroll
         for (int j0 = 0; j0 < kD; j0 += 16) {
           float v[16];
@@ -439,26 +549,21 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
         }
       }
       gemm(tmem + kColG, tmem + kColA, smem_u32(bo_t), kD, kD);  // pooled = mix Wo + bo
-      if (rowt) {
+      if (att) {
 #pragma unroll
         for (int j0 = 0; j0 < kD; j0 += 16) {
           float v[16];
           tmem_ld16(D0 + j0, v);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) pool[j0 + i] = v[i] + sbias[kD + j0 + i];
+          for (int i = 0; i < 16; ++i) v[i] += sbias[kD + j0 + i];
+          tmem_st16(A0 + j0, v);  // next pass's query input / the head's z[0:64]
         }
       }
     }
+    TC_MARK(pm, 20);
     // ================================================================ head
-    if (rowt) {
-#pragma unroll
-      for (int j0 = 0; j0 < kD; j0 += 16) {
-        float v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = pool[j0 + i];
-        tmem_st16(A0 + j0, v);
-      }
+    if (att) {
       for (int j0 = kD; j0 < Zp; j0 += 8) {
         float v[8];
 #pragma unroll
@@ -467,7 +572,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
       }
     }
     gemm(tmem + kColG, tmem + kColA, smem_u32(b1_t), kHeadHidden, Zp);
-    if (rowt) {
+    if (att) {
       float acc = 0.f;
 #pragma unroll
       for (int j0 = 0; j0 < kHeadHidden; j0 += 16) {
@@ -481,6 +586,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
       }
       if (live) a.yhat[p] = Act<float>::sigmoid(acc + sbias[2 * kD + 2 * kHeadHidden]);
     }
+    TC_MARK(pm, 21);
   }
   tc_fence_before();
   __syncthreads();
@@ -491,12 +597,14 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
 }
 
 static size_t sc_smem_bytes(int Tmax) {
-  return 1024 + sc::kBBytes + 512 * 4 + (size_t)sc::kRows * Tmax * sc::kMaxHeads * 4 +
+  return 1024 + sc::kBBytes + 512 * 4 + (size_t)sc::kRows * sc_slot_floats(Tmax) * 4 +
          sizeof(ScBars) + 64;
 }
 
+constexpr size_t kScImageBytes = 1u << 20;  // >= every LSTM image (L <= 8) + the attention image
+
 size_t tuner_predict_tc_ws(int Tmax) {
-  return (size_t)sm_count() * 2 * sc::kRows * Tmax * sc::kD * sizeof(float);
+  return (size_t)sm_count() * 2 * sc::kRows * Tmax * sc::kD * sizeof(float) + kScImageBytes;
 }
 
 int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff, const float* ctx,
@@ -523,6 +631,12 @@ int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff
   a.yhat = yhat;
   a.scratch = static_cast<float*>(ws);
   a.scr_per_cta = (int64_t)2 * sc::kRows * Tmax * sc::kD;
+  unsigned char* img = static_cast<unsigned char*>(ws) +
+                       align_up((size_t)sm_count() * a.scr_per_cta * sizeof(float), 1024);
+  TT_REQUIRE(sc_attn_image_off(a.dm) + sc_attn_image_bytes(a.dm) <= (int64_t)kScImageBytes - 1024,
+             "tuner tf32 scoring: weight images exceed the workspace");
+  a.img = img;
+  tuner_tc_prepare_kernel<<<L + 1, 256, 0, st>>>(a.dm, prm, img);
   TT_CUDA(cudaFuncSetAttribute(tuner_predict_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   const int64_t tiles = (n + sc::kRows - 1) / sc::kRows;
@@ -534,6 +648,12 @@ int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff
 }  // namespace tt
 
 extern "C" {
+
+int tt_debug_tc_phase_times(int64_t* out, int32_t n) {
+  TT_REQUIRE(n >= 0 && n <= 32, "debug: n must be in [0, 32]");
+  TT_CUDA(cudaMemcpyFromSymbol(out, tt::g_tc_phase, sizeof(long long) * n));
+  return TT_OK;
+}
 
 size_t tt_tuner_predict_tf32_workspace_bytes(int32_t max_steps) {
   return tt::tuner_predict_tc_ws(max_steps);

@@ -262,7 +262,7 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
     def _tc_eligible(dims, prog) -> bool:
         """Shapes the tcgen05 scoring kernel (csrc/tt_tuner_tc.cu) covers."""
         return (dims["H"] == 32 and dims["heads"] in (1, 2) and dims["d0"] <= 32
-                and dims["C"] <= 64 and prog.max_steps <= 512)
+                and dims["C"] <= 64 and prog.max_steps <= 64)
 
     def _predict_programs(self, prog: DevicePrograms, dims, flat=None):
         t = _device.torch()

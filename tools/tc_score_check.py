@@ -35,3 +35,12 @@ for prec in ("fp32", "tf32"):
     e1.record(); torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 3 / 1e3
     print(f"{prec}: {n / t / 1e6:.2f} M programs/s ({t * 1e3:.2f} ms for {n})")
+
+import ctypes
+from paper_2304_05430_b200 import _lib
+buf = (ctypes.c_int64 * 32)()
+_lib.load().tt_debug_tc_phase_times(buf, 32)
+mk = list(buf)
+cyc = lambda a, b: (mk[b] - mk[a])
+print("tile:", " ".join(f"layer{l}={cyc(l, l + 1)}" for l in range(3)), f"attn-staging={cyc(3, 26)} attn={cyc(26, 20)} head={cyc(20, 21)} total={cyc(0, 21)} cycles")
+print(f"layer1 step1: writeA={cyc(22, 23)} mma(wait)={cyc(23, 24)} epilogue={cyc(24, 25)} cycles")
