@@ -443,6 +443,24 @@ def run_b200(args, world, rank):
         sc_t = s0.elapsed_time(s1) / 1e3
         extra["scoring_programs_per_s"] = n / sc_t
         extra["scoring_tflops"] = float(np.sum(134656.0 * lens + 45568.0)) / sc_t / 1e12
+        # the same scoring on the tensor cores (tcgen05 kind::tf32, "tf32" mode)
+        est.precision = "tf32"
+        for _ in range(2):
+            est._predict_programs(prog, dims, flat)
+        ts = []
+        for _ in range(3):
+            flush_l2(l2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            est._predict_programs(prog, dims, flat)
+            e1.record(stream)
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        tc_t = float(np.mean([a_.elapsed_time(b_) for a_, b_ in ts])) / 1e3
+        est.precision = "fp32"
+        extra["scoring_tc_tf32_programs_per_s"] = n / tc_t
+        extra["scoring_tc_tf32_tflops"] = float(np.sum(134656.0 * lens + 45568.0)) / tc_t / 1e12
         from paper_2304_05430_b200 import metrics as gm
 
         pred = est._predict_programs(prog, dims, flat).double()

@@ -95,6 +95,32 @@ __host__ __device__ inline int sc_slot_floats(int Tmax) {
 __device__ __forceinline__ void cp_async16_cg(float* s, const float* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(s)), "l"(g) : "memory");
 }
+// L2 evict_last cache-policy loads/stores for the layer-output scratch, so
+// the rows the next layer and the attention passes re-read stay in L2
+// instead of streaming out with the input programs.
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_keep(float* g, float4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(g), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ float4 ld_keep(const float* g, uint64_t pol) {
+  float4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(g), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void cp_async16_keep(float* s, const float* g, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(s)),
+               "l"(g), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
@@ -212,6 +238,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
   const uint32_t tmem = bars->tmem_base;
   uint32_t ph = 0;
   uint32_t pd[2] = {0, 0};  // phase bits of the per-direction LSTM hand-offs
+  const uint64_t pol_keep = l2_keep_policy();
   float* scr0 = a.scratch + (int64_t)blockIdx.x * a.scr_per_cta;
 
   // one GEMM hand-off: row threads have written A; the MMA lane issues.
@@ -295,7 +322,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
         if (ok) {
           const float* src = xin + (int64_t)(d == 0 ? s : T - 1 - s) * kD;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) cp_async16_cg(dst + 4 * q, src + 4 * q);
+          for (int q = 0; q < 16; ++q) cp_async16_keep(dst + 4 * q, src + 4 * q, pol_keep);
         } else {
 #pragma unroll
           for (int q = 0; q < 16; ++q) reinterpret_cast<float4*>(dst)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -382,8 +409,8 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
             tmem_st8(Cd + j0, cc);
             tmem_st8(Ad + kx + j0, h);
             if (valid) {
-              reinterpret_cast<float4*>(orow + j0)[0] = make_float4(h[0], h[1], h[2], h[3]);
-              reinterpret_cast<float4*>(orow + j0)[1] = make_float4(h[4], h[5], h[6], h[7]);
+              st_keep(orow + j0, make_float4(h[0], h[1], h[2], h[3]), pol_keep);
+              st_keep(orow + j0 + 4, make_float4(h[4], h[5], h[6], h[7]), pol_keep);
             }
           }
           if (s + 1 < Tt) {
@@ -447,7 +474,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float4 f = __ldcg(sr + q);
+            const float4 f = ld_keep(reinterpret_cast<const float*>(sr + q), pol_keep);
             pool[4 * q] += f.x, pool[4 * q + 1] += f.y, pool[4 * q + 2] += f.z, pool[4 * q + 3] += f.w;
           }
         }
@@ -461,6 +488,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
         tmem_st16(A0 + j0, v);
       }
     }
+    TC_MARK(pm, 27);
     const float sq = sqrtf((float)dh);
     // logits as [t][head][row]: lanes (rows) hit consecutive banks
     float* lg = slog + row;
@@ -478,6 +506,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
         }
       }
       gemm(tmem + kColG, tmem + kColA, smem_u32(bk_t), NK, kD);  // r_h = Wk[:, h] q_h
+      TC_MARK(pm && u == 0, 28);
       if (rowt) {
         float r[kD], uvec[kD];
         if (hg) {
@@ -497,7 +526,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-              const float4 f = __ldcg(sr + q);
+              const float4 f = ld_keep(reinterpret_cast<const float*>(sr + q), pol_keep);
               a0 = fmaf(f.x, r[4 * q], a0);
               a1 = fmaf(f.y, r[4 * q + 1], a1);
               a0 = fmaf(f.z, r[4 * q + 2], a0);
@@ -519,7 +548,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
             const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
-              const float4 f = __ldcg(sr + q);
+              const float4 f = ld_keep(reinterpret_cast<const float*>(sr + q), pol_keep);
               uvec[4 * q] = fmaf(al, f.x, uvec[4 * q]);
               uvec[4 * q + 1] = fmaf(al, f.y, uvec[4 * q + 1]);
               uvec[4 * q + 2] = fmaf(al, f.z, uvec[4 * q + 2]);
@@ -538,6 +567,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           }
         }
       }
+      TC_MARK(pm && u == 0, 29);
       gemm(tmem + kColG, tmem + kColA, smem_u32(bv_t), kD, NK);  // mix = [u_h] blockdiag(Wv)
       if (att) {
 #pragma unroll

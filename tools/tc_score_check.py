@@ -44,3 +44,4 @@ mk = list(buf)
 cyc = lambda a, b: (mk[b] - mk[a])
 print("tile:", " ".join(f"layer{l}={cyc(l, l + 1)}" for l in range(3)), f"attn-staging={cyc(3, 26)} attn={cyc(26, 20)} head={cyc(20, 21)} total={cyc(0, 21)} cycles")
 print(f"layer1 step1: writeA={cyc(22, 23)} mma(wait)={cyc(23, 24)} epilogue={cyc(24, 25)} cycles")
+print(f"attention: p0={cyc(26, 27)} pass0 q+r gemms={cyc(27, 28)} logits+softmax+u={cyc(28, 29)} rest={cyc(29, 20)}")
