@@ -45,6 +45,23 @@ static __device__ long long g_tc_phase[32];
     if (cond) g_tc_phase[i] = clock64(); \
   } while (0)
 
+// Activations for the tf32 scoring mode: ex2.approx.ftz / rcp.approx.ftz
+// (same MUFU ops as Act<float>, without the denormal-range fix-ups).
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rcpf(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sig_f(float x) { return rcpf(1.f + ex2f(-1.4426950408889634f * x)); }
+__device__ __forceinline__ float tanh_f(float x) {
+  return 1.f - 2.f * rcpf(ex2f(2.8853900817779268f * x) + 1.f);
+}
+
 namespace sc {
 constexpr int kRows = 128;
 constexpr int kThreads = 288;  // warp 0: MMA; warps 1..4 and 5..8: two row groups
@@ -205,9 +222,9 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* Bs = base;                                         // B operands (128 KB)
-  float* sbias = reinterpret_cast<float*>(base + kBBytes);          // 512 floats
+  __shared__ float sbias[512];  // biases / head vectors (static: LDS, not generic loads)
   // LSTM: per-row x slots [128][2][64]; attention: per-row logits [128][Tmax][2] (aliased)
-  float* sxs = sbias + 512;
+  float* sxs = reinterpret_cast<float*>(base + kBBytes);
   float* slog = sxs;
   ScBars* bars = reinterpret_cast<ScBars*>(sxs + (int64_t)kRows * sc_slot_floats(a.dm.Tmax));
   const TDims& dm = a.dm;
@@ -388,29 +405,31 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           const int t = d == 0 ? s : T - 1 - s;
           float* orow = xout + (int64_t)t * kD + d * kH;
 #pragma unroll
-          for (int j0 = 0; j0 < kH; j0 += 8) {
-            float gi[8], gf[8], gg[8], go[8], cc[8], h[8];
-            tmem_ld8(Gd + j0, gi);
-            tmem_ld8(Gd + kH + j0, gf);
-            tmem_ld8(Gd + 2 * kH + j0, gg);
-            tmem_ld8(Gd + 3 * kH + j0, go);
-            tmem_ld8(Cd + j0, cc);
+          for (int j0 = 0; j0 < kH; j0 += 16) {
+            float gi[16], gf[16], gg[16], go[16], cc[16], h[16];
+            tmem_ld16(Gd + j0, gi);
+            tmem_ld16(Gd + kH + j0, gf);
+            tmem_ld16(Gd + 2 * kH + j0, gg);
+            tmem_ld16(Gd + 3 * kH + j0, go);
+            tmem_ld16(Cd + j0, cc);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
+            for (int i = 0; i < 16; ++i) {
               const int j = j0 + i;
-              const float ig = Act<float>::sigmoid(gi[i] + bd[j]);
-              const float fg = Act<float>::sigmoid(gf[i] + bd[kH + j]);
-              const float cg = Act<float>::tanh(gg[i] + bd[2 * kH + j]);
-              const float og = Act<float>::sigmoid(go[i] + bd[3 * kH + j]);
+              const float ig = sig_f(gi[i] + bd[j]);
+              const float fg = sig_f(gf[i] + bd[kH + j]);
+              const float cg = tanh_f(gg[i] + bd[2 * kH + j]);
+              const float og = sig_f(go[i] + bd[3 * kH + j]);
               cc[i] = fg * cc[i] + ig * cg;
-              h[i] = og * Act<float>::tanh(cc[i]);
+              h[i] = og * tanh_f(cc[i]);
             }
-            tmem_st8(Cd + j0, cc);
-            tmem_st8(Ad + kx + j0, h);
+            tmem_st16(Cd + j0, cc);
+            tmem_st16(Ad + kx + j0, h);
             if (valid) {
-              st_keep(orow + j0, make_float4(h[0], h[1], h[2], h[3]), pol_keep);
-              st_keep(orow + j0 + 4, make_float4(h[4], h[5], h[6], h[7]), pol_keep);
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                st_keep(orow + j0 + 4 * q, make_float4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]),
+                        pol_keep);
             }
           }
           if (s + 1 < Tt) {
@@ -627,7 +646,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
 }
 
 static size_t sc_smem_bytes(int Tmax) {
-  return 1024 + sc::kBBytes + 512 * 4 + (size_t)sc::kRows * sc_slot_floats(Tmax) * 4 +
+  return 1024 + sc::kBBytes + (size_t)sc::kRows * sc_slot_floats(Tmax) * 4 +
          sizeof(ScBars) + 64;
 }
 
