@@ -132,24 +132,35 @@ inline FastXch make_fast_xch(const TDims& d, int B) {
 
 // ------------------------------------------------------ gradient jobs --
 enum FastJobKind { FJ_LSTM = 0, FJ_WQ, FJ_WK, FJ_WV, FJ_WO, FJ_W1, FJ_W2 };
-constexpr int kCwLstm = 8, kCwAttn = 16, kCwHead = 16;
+// Column-slice widths.  Layer 0's gradient jobs sit on the critical path
+// into the next minibatch (its forward needs them first), so they are cut
+// finest; the upper layers' jobs overlap that forward and are cut coarser
+// (same total job count, fewer CTAs per non-critical group).
+constexpr int kCwLstm0 = 4, kCwLstm = 16, kCwAttn = 16, kCwHead = 16;
+
+__host__ __device__ inline int lstm_cw(int l) { return l == 0 ? kCwLstm0 : kCwLstm; }
+__host__ __device__ inline int lstm_jobs(int l) { return 2 * (kFG / lstm_cw(l)); }
+__host__ __device__ inline int attn_jobs() { return 4 * (kFD / kCwAttn) + kHeadHidden / kCwHead + 1; }
 
 struct FastJob {
   int kind, l, dir, c0, nb;  // nb = slice width (columns)
 };
 
 __host__ __device__ inline int fast_n_jobs(const TDims& d) {
-  return d.L * 2 * (kFG / kCwLstm) + 4 * (kFD / kCwAttn) + kHeadHidden / kCwHead + 1;
+  int n = attn_jobs();
+  for (int l = 0; l < d.L; ++l) n += lstm_jobs(l);
+  return n;
 }
 
 __host__ __device__ inline FastJob fast_job(const TDims& d, int j) {
-  const int nl = d.L * 2 * (kFG / kCwLstm);
-  if (j < nl) {
-    const int per = kFG / kCwLstm;
-    const int ld = j / per;
-    return FastJob{FJ_LSTM, ld / 2, ld % 2, (j % per) * kCwLstm, kCwLstm};
+  for (int l = 0; l < d.L; ++l) {
+    const int nl = lstm_jobs(l);
+    if (j < nl) {
+      const int cw = lstm_cw(l), per = kFG / cw;
+      return FastJob{FJ_LSTM, l, j / per, (j % per) * cw, cw};
+    }
+    j -= nl;
   }
-  j -= nl;
   const int pa = kFD / kCwAttn;
   if (j < 4 * pa) return FastJob{FJ_WQ + j / pa, 0, 0, (j % pa) * kCwAttn, kCwAttn};
   j -= 4 * pa;
@@ -266,12 +277,15 @@ __device__ __forceinline__ void fmark_any(int step, int i) {
 // the next forward's first layers.
 __device__ __forceinline__ int ctr_bwd(int g) { return 1 + g; }
 __device__ __forceinline__ int ctr_adam(const TDims& d, int g) { return 2 + d.L + g; }
-__device__ __forceinline__ int jobs_per_layer() { return 2 * (kFG / kCwLstm); }
 __device__ __forceinline__ int job_group(const TDims& d, int j) {
-  return j < d.L * jobs_per_layer() ? j / jobs_per_layer() : d.L;
+  for (int l = 0; l < d.L; ++l) {
+    if (j < lstm_jobs(l)) return l;
+    j -= lstm_jobs(l);
+  }
+  return d.L;
 }
 __device__ __forceinline__ int group_jobs(const TDims& d, int g) {
-  return g < d.L ? jobs_per_layer() : 4 * (kFD / kCwAttn) + kHeadHidden / kCwHead + 1;
+  return g < d.L ? lstm_jobs(g) : attn_jobs();
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -312,6 +326,25 @@ __device__ __forceinline__ void cp_async16(float* s, const float* g) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// Recurrence activations: the same MUFU ops as Act<float> (ex2.approx +
+// rcp.approx) in their .ftz forms, which drop the denormal-range fix-up
+// instructions from the per-step critical path (results differ only where
+// exp underflows to a denormal).
+__device__ __forceinline__ float fx_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fx_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fsig(float x) { return fx_rcp(1.f + fx_ex2(-1.4426950408889634f * x)); }
+__device__ __forceinline__ float ftanh(float x) {
+  return 1.f - 2.f * fx_rcp(fx_ex2(2.8853900817779268f * x) + 1.f);
 }
 
 // ------------------------------------------------------ recurrences --
@@ -389,8 +422,8 @@ __device__ __forceinline__ void fast_rec_fwd(const WReg& w, int dir, int sub, in
     }
     const float z0 = a00 + a01, z1 = a10 + a11;
     // sub 0: (i, f) = sigmoid; sub 1: g = tanh, o = sigmoid
-    const float v0 = sub == 0 ? Act<float>::sigmoid(z0) : Act<float>::tanh(z0);
-    const float v1 = Act<float>::sigmoid(z1);
+    const float v0 = sub == 0 ? fsig(z0) : ftanh(z0);
+    const float v1 = fsig(z1);
     float* gr = gc + ((int64_t)dir * TM + t) * kFG + 2 * sub * kFH;
     gr[j] = v0;
     gr[kFH + j] = v1;
@@ -401,7 +434,7 @@ __device__ __forceinline__ void fast_rec_fwd(const WReg& w, int dir, int sub, in
     const float gi = sub == 0 ? v0 : o0, gf = sub == 0 ? v1 : o1;
     const float gg = sub == 0 ? o0 : v0, go = sub == 0 ? o1 : v1;
     c = gf * c + gi * gg;
-    const float h = go * Act<float>::tanh(c);
+    const float h = go * ftanh(c);
     hm[(par ^ 1) * kFH + j] = h;
     if (sub == 0) {
       S[(int64_t)t * kFD + dir * kFH + j] = h;
@@ -438,7 +471,7 @@ __device__ __forceinline__ void fast_rec_bwd(const WReg& wr, int dir, int sub, i
     const float* gr = gc + ((int64_t)dir * TM + t) * kFG;
     const float gi = gr[j], gf = gr[kFH + j], gg = gr[2 * kFH + j], go = gr[3 * kFH + j];
     const float cn = cs[((int64_t)dir * TM + t) * kFH + j];
-    const float tc = Act<float>::tanh(cn);
+    const float tc = ftanh(cn);
     const float cp = has_prev ? cs[((int64_t)dir * TM + tp) * kFH + j] : 0.f;
     const float dht = dS[(int64_t)t * kFD + dir * kFH + j] + dh;
     const float dO = dht * tc;
