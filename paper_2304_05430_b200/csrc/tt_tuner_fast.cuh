@@ -27,6 +27,7 @@
 // (~45 KB/sample at T = 10) instead of B partial 330 KB gradient vectors.
 #pragma once
 
+#include "tt_sm100.cuh"
 #include "tt_tuner_train.cuh"
 
 namespace tt {
@@ -90,7 +91,10 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   s.dpool = seg(kFD);
   s.da1 = seg(kHeadHidden);
   // attention + head weights, row stride 68: [Wq|Wk|Wv|Wo|bq|bo] then [W1|b1|W2]
-  s.W = seg((int64_t)(4 * kFD + 2) * kLdA + (int64_t)(kFD + d.C + 3) * kLdA);  // + b2 row
+  // attention/head weights (row stride 68, + b2 row) or one LSTM layer's two
+  // direction blocks [Wx | Wh | b] (128 columns)
+  s.W = seg(std::max<int64_t>((int64_t)(4 * kFD + 2) * kLdA + (int64_t)(kFD + d.C + 3) * kLdA,
+                              (int64_t)2 * (kFD + kFH + 1) * kFG));
   s.total = o;
   return s;
 }
@@ -253,6 +257,10 @@ struct FastArgs {
 // from global memory ONCE per launch into shared memory: a global read per
 // mark would cost an L2 round trip after every fence (they invalidate L1).
 __shared__ int s_prof;
+// Weight-prefetch barrier of a sample CTA (bulk copies into W) and its phase.
+__shared__ __align__(8) uint64_t s_wbar;
+__shared__ uint32_t s_wph;
+
 // CTA 0, clock64 (cycles)
 __device__ __forceinline__ void fmark(int step, int i) {
   if (blockIdx.x == 0 && threadIdx.x == 0 && step == s_prof) g_phase[i] = clock64();
@@ -618,17 +626,29 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
   float* xz = sm + L.xz;
   float* W = sm + L.W;
   float* W1s = W + (4 * kFD + 2) * kLdA;
+  // Weights of layer l >= 1 (per direction the contiguous parameter block
+  // [Wx (64 rows) | Wh (32 rows) | b] of 128 columns) and finally the
+  // attention/head block are copied into W by warps 4..7 with async 16-B
+  // copies DURING the previous layer's recurrence, after that group's Adam
+  // update of the previous minibatch is complete; layer 0 reads L2 directly
+  // (its update was awaited at the step start).
+  constexpr int kBlk = (kFD + kFH + 1) * kFG;  // floats per direction block
+  // Layers 1..L-2 read their block from W; layer 0 and the last layer read
+  // L2 directly, so the attention block can be prefetched during layer L-2
+  // (two recurrences to land).
+  const int att_l = dm.L >= 2 ? dm.L - 2 : 0;  // layer during which attention is prefetched
   for (int l = 0; l < dm.L; ++l) {
-    // ---- warps 0..3 fetch their Wh gate columns for this layer, then all
-    //      threads form the input projection xz[dir][t][c] = b[c] + x_t Wx[:, c]
-    //      (thread = column), overlapping the two L2 round trips.
+    const bool direct = l == 0 || l == dm.L - 1;
+    if (l > 0 && direct && step > 0)  // last layer: its update must be done
+      wait_counter(a.ctr + ctr_adam(dm, l), (unsigned)(step * group_jobs(dm, l)), false);
     {
       // ---- input projection xz[dir][t][c] = b[c] + x_t Wx[:, c], thread = column
       const int dir = tid >> 7, c = tid & 127;
-      const float* Wx = a.prm + dm.wx[l][dir] + c;
-      const float bc = __ldcg(a.prm + dm.bb[l][dir] + c);
       float* xzr = xz + (int64_t)dir * TM * kFG + c;
       if (l == 0) {
+        const float* Wx = a.prm + dm.wx[0][dir] + c;
+        const float bc = __ldcg(a.prm + dm.bb[0][dir] + c);
+        (void)direct;
         // raw rows staged in smem at the step start (zero padded to w0)
         const int w0 = round4(dm.d0);
         const float* x0 = sm + L.x0;
@@ -646,20 +666,38 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
           }
         }
       } else {
+        // prefetched block of this direction, or L2 for the last layer
+        const float* Wb = direct ? a.prm + dm.wx[l][dir] + c : W + dir * kBlk + c;
         float wx[kFD];
+        float bc;
+        if (direct) {
 #pragma unroll
-        for (int k = 0; k < kFD; ++k) wx[k] = __ldcg(Wx + (int64_t)k * kFG);
+          for (int k = 0; k < kFD; ++k) wx[k] = __ldcg(Wb + k * kFG);
+          bc = __ldcg(Wb + (kFD + kFH) * kFG);
+        } else {
+#pragma unroll
+          for (int k = 0; k < kFD; ++k) wx[k] = Wb[k * kFG];
+          bc = Wb[(kFD + kFH) * kFG];
+        }
         const float* xin = S + (int64_t)(l - 1) * TM * kFD;
         for (int t = 0; t < T; ++t) xzr[(int64_t)t * kFG] = dot64<0>(xin + (int64_t)t * kFD, wx) + bc;
       }
     }
     if (warp < 4) {
       WReg wh;
-      load_wh_cols(wh, a.prm + dm.wh[l][warp >> 1], warp & 1);
-      named_barrier(1, kThreads);  // projection done
+      const int dir = warp >> 1, sub = warp & 1;
+      if (direct) {
+        load_wh_cols(wh, a.prm + dm.wh[l][dir], sub);
+      } else {
+        const float* Wh = W + dir * kBlk + kFD * kFG + lane;
+#pragma unroll
+        for (int k = 0; k < kFH; ++k)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) wh[q * kFH + k] = Wh[k * kFG + (2 * sub + q) * kFH];
+      }
+      named_barrier(1, kThreads);  // projection done, W free
       if (warp == 0) fmark(step, 25 + l);
-      const int dir = warp >> 1;
-      fast_rec_fwd(wh, dir, warp & 1, T, TM, xz, S + (int64_t)l * TM * kFD,
+      fast_rec_fwd(wh, dir, sub, T, TM, xz, S + (int64_t)l * TM * kFD,
                    a.xch + X.S + ((int64_t)l * X.Rmax + rs) * kFD,
                    a.xch + X.H + (((int64_t)l * 2 + dir) * X.Rmax + rs) * kFH,
                    sm + L.gc + (int64_t)l * 2 * TM * kFG, sm + L.cs + (int64_t)l * 2 * TM * kFH,
@@ -667,27 +705,56 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
       if (warp == 0) fmark(step, 2 + l);
     } else {
       named_barrier(1, kThreads);
-      if (l == 0) {
-        // idle warps start the async copy of the attention/head weights (changed
-        // by the last Adam step) into 16-B rows of stride 68; waited for before
-        // the attention phase
-        const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
-        const float* src1 = a.prm + dm.Wq;
-        const float* src2 = a.prm + dm.W1;
-        const int tot = (rows1 + rows2) * 16 + 1;  // + the chunk holding b2
-        for (int e = tid - 128; e < tot; e += kThreads - 128) {
-          const int row = e >> 4, q = e & 15;
-          if (row < rows1)
-            cp_async16(W + row * kLdA + q * 4, src1 + e * 4);
-          else if (e + 1 < tot)
-            cp_async16(W1s + (row - rows1) * kLdA + q * 4, src2 + (e - rows1 * 16) * 4);
-          else  // b2 is the last parameter: a 4-byte copy stays inside the buffer
-            cp_async4(W1s + (int64_t)rows2 * kLdA, src2 + (int64_t)rows2 * 64);
+      // what this recurrence overlaps: layer l+1's block (if it reads W) or,
+      // during layer att_l, the attention/head block
+      const bool pf_lstm = l + 1 < dm.L - 1;
+      const bool pf_attn = l == att_l;
+      if (pf_lstm || pf_attn) {
+        const int g = pf_lstm ? l + 1 : dm.L;
+        if (step > 0) {  // that group's Adam update (previous minibatch) must be done
+          if (tid == 128) {
+            const unsigned target = (unsigned)(step * group_jobs(dm, g));
+            while (ld_acquire(a.ctr + ctr_adam(dm, g)) < target) {
+            }
+          }
+          named_barrier(5, kThreads - 128);  // ids 2, 3: recurrence warp pairs
+        }
+        if (pf_lstm) {
+          // two contiguous direction blocks: bulk copies on the TMA engine
+          if (warp == 4) {
+            sm100::fence_proxy_async_smem();  // W's generic reads before the async writes
+            if (lane == 0) sm100::mbar_expect_tx(&s_wbar, 2u * kBlk * 4u);
+            __syncwarp();
+            if (lane < 2) sm100::bulk_g2s(W + lane * kBlk, a.prm + dm.wx[l + 1][lane], kBlk * 4u, &s_wbar);
+          }
+        } else {
+          // attention/head weights into 16-B rows of stride 68 (per-thread async
+          // copies; they have this and the last layer's recurrence to land)
+          const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
+          const float* src1 = a.prm + dm.Wq;
+          const float* src2 = a.prm + dm.W1;
+          const int tot = (rows1 + rows2) * 16 + 1;  // + the chunk holding b2
+          for (int e = tid - 128; e < tot; e += kThreads - 128) {
+            const int row = e >> 4, q = e & 15;
+            if (row < rows1)
+              cp_async16(W + row * kLdA + q * 4, src1 + e * 4);
+            else if (e + 1 < tot)
+              cp_async16(W1s + (row - rows1) * kLdA + q * 4, src2 + (e - rows1 * 16) * 4);
+            else  // b2 is the last parameter: a 4-byte copy stays inside the buffer
+              cp_async4(W1s + (int64_t)rows2 * kLdA, src2 + (int64_t)rows2 * 64);
+          }
         }
       }
       if (l == dm.L - 1) cp_async_wait_all();
     }
     __syncthreads();
+    if (l + 1 < dm.L - 1) {
+      // the bulk copy issued during this layer's recurrence must have landed
+      const uint32_t wph = s_wph;
+      sm100::mbar_wait(&s_wbar, wph);
+      __syncthreads();
+      if (tid == 0) s_wph = wph ^ 1u;
+    }
   }
   // ---- attention (tuner.py:248-274)
   const int heads = dm.heads, dh = dm.dh, U = dm.U;
@@ -1245,7 +1312,11 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
   if (threadIdx.x == 0) {
     s_pref = -1;
     s_prof = g_prof_step;
+    s_wph = 0;
+    sm100::mbar_init(&s_wbar, 1);
+    sm100::fence_barrier_init();
   }
+  __syncthreads();
   if (blockIdx.x == 0 && threadIdx.x < 8)  // constant chunks [0 0 0 0 | 1 0 0 0] for job staging
     a.xch[a.xl.cst + threadIdx.x] = threadIdx.x == 4 ? 1.f : 0.f;
   const int tid = threadIdx.x;
@@ -1261,11 +1332,8 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     const unsigned cum = (unsigned)(b0 + bn);
     if (sampler && r < bn) {
       fmark(step, 0);
-      if (step > 0) {
-        // layer 0 and the attention block (staged during layer 0) must be updated
-        wait_counter(a.ctr + ctr_adam(dm, dm.L), (unsigned)(step * group_jobs(dm, dm.L)), false);
+      if (step > 0)  // layer 0's update (the other groups are awaited where prefetched)
         wait_counter(a.ctr + ctr_adam(dm, 0), (unsigned)(step * group_jobs(dm, 0)), false);
-      }
       fmark(step, 1);
       if (r == 0) fmark_any(step, 31);
       // step counts, labels and slot metadata: prefetched into smem during the
