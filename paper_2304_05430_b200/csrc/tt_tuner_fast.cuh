@@ -142,8 +142,11 @@ enum FastJobKind { FJ_LSTM = 0, FJ_WQ, FJ_WK, FJ_WV, FJ_WO, FJ_W1, FJ_W2 };
 // (same total job count, fewer CTAs per non-critical group).
 constexpr int kCwLstm0 = 4, kCwLstm = 16, kCwAttn = 16, kCwHead = 16;
 
-__host__ __device__ inline int lstm_cw(int l) { return l == 0 ? kCwLstm0 : kCwLstm; }
-__host__ __device__ inline int lstm_jobs(int l) { return 2 * (kFG / lstm_cw(l)); }
+__host__ __device__ inline int lstm_cw(int l, int L) {
+  (void)L;
+  return l == 0 ? kCwLstm0 : kCwLstm;
+}
+__host__ __device__ inline int lstm_jobs(int l, int L) { return 2 * (kFG / lstm_cw(l, L)); }
 __host__ __device__ inline int attn_jobs() { return 4 * (kFD / kCwAttn) + kHeadHidden / kCwHead + 1; }
 
 struct FastJob {
@@ -152,15 +155,15 @@ struct FastJob {
 
 __host__ __device__ inline int fast_n_jobs(const TDims& d) {
   int n = attn_jobs();
-  for (int l = 0; l < d.L; ++l) n += lstm_jobs(l);
+  for (int l = 0; l < d.L; ++l) n += lstm_jobs(l, d.L);
   return n;
 }
 
 __host__ __device__ inline FastJob fast_job(const TDims& d, int j) {
   for (int l = 0; l < d.L; ++l) {
-    const int nl = lstm_jobs(l);
+    const int nl = lstm_jobs(l, d.L);
     if (j < nl) {
-      const int cw = lstm_cw(l), per = kFG / cw;
+      const int cw = lstm_cw(l, d.L), per = kFG / cw;
       return FastJob{FJ_LSTM, l, j / per, (j % per) * cw, cw};
     }
     j -= nl;
@@ -287,13 +290,13 @@ __device__ __forceinline__ int ctr_bwd(int g) { return 1 + g; }
 __device__ __forceinline__ int ctr_adam(const TDims& d, int g) { return 2 + d.L + g; }
 __device__ __forceinline__ int job_group(const TDims& d, int j) {
   for (int l = 0; l < d.L; ++l) {
-    if (j < lstm_jobs(l)) return l;
-    j -= lstm_jobs(l);
+    if (j < lstm_jobs(l, d.L)) return l;
+    j -= lstm_jobs(l, d.L);
   }
   return d.L;
 }
 __device__ __forceinline__ int group_jobs(const TDims& d, int g) {
-  return g < d.L ? lstm_jobs(g) : attn_jobs();
+  return g < d.L ? lstm_jobs(g, d.L) : attn_jobs();
 }
 
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
@@ -638,9 +641,8 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
   // (two recurrences to land).
   const int att_l = dm.L >= 2 ? dm.L - 2 : 0;  // layer during which attention is prefetched
   for (int l = 0; l < dm.L; ++l) {
-    const bool direct = l == 0 || l == dm.L - 1;
-    if (l > 0 && direct && step > 0)  // last layer: its update must be done
-      wait_counter(a.ctr + ctr_adam(dm, l), (unsigned)(step * group_jobs(dm, l)), false);
+    const bool direct = l == 0 || l == dm.L - 1;  // (the last layer's update was
+                                                  //  awaited during layer att_l)
     {
       // ---- input projection xz[dir][t][c] = b[c] + x_t Wx[:, c], thread = column
       const int dir = tid >> 7, c = tid & 127;
@@ -742,6 +744,16 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
               cp_async16(W1s + (row - rows1) * kLdA + q * 4, src2 + (e - rows1 * 16) * 4);
             else  // b2 is the last parameter: a 4-byte copy stays inside the buffer
               cp_async4(W1s + (int64_t)rows2 * kLdA, src2 + (int64_t)rows2 * 64);
+          }
+          // the last layer reads L2 directly at its start: await its update
+          // here, off the critical path
+          if (step > 0 && l + 1 == dm.L - 1) {
+            if (tid == 128) {
+              const unsigned target = (unsigned)(step * group_jobs(dm, dm.L - 1));
+              while (ld_acquire(a.ctr + ctr_adam(dm, dm.L - 1)) < target) {
+              }
+            }
+            named_barrier(5, kThreads - 128);
           }
         }
       }
