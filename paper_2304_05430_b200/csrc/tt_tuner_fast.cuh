@@ -253,6 +253,7 @@ struct FastArgs {
   int n_jobs;
   int64_t rch;         // job staging rows per chunk
   int64_t pc_off;      // smem float offset of a job CTA's parameter cache [4][pc_n]
+  int l0_smem;         // layer 0's weight blocks fit in W (bulk-copied at each step start)
   int pc_n;            // floats per cache array (kap_max * 16)
 };
 
@@ -640,6 +641,13 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
   // L2 directly, so the attention block can be prefetched during layer L-2
   // (two recurrences to land).
   const int att_l = dm.L >= 2 ? dm.L - 2 : 0;  // layer during which attention is prefetched
+  const int blk0 = (dm.d0 + kFH + 1) * kFG;     // layer-0 direction block (a.l0_smem)
+  if (a.l0_smem) {
+    const uint32_t wph = s_wph;
+    sm100::mbar_wait(&s_wbar, wph);
+    __syncthreads();
+    if (tid == 0) s_wph = wph ^ 1u;
+  }
   for (int l = 0; l < dm.L; ++l) {
     const bool direct = l == 0 || l == dm.L - 1;  // (the last layer's update was
                                                   //  awaited during layer att_l)
@@ -648,8 +656,8 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
       const int dir = tid >> 7, c = tid & 127;
       float* xzr = xz + (int64_t)dir * TM * kFG + c;
       if (l == 0) {
-        const float* Wx = a.prm + dm.wx[0][dir] + c;
-        const float bc = __ldcg(a.prm + dm.bb[0][dir] + c);
+        const float* Wx = a.l0_smem ? W + dir * blk0 + c : a.prm + dm.wx[0][dir] + c;
+        const float bc = a.l0_smem ? Wx[(dm.d0 + kFH) * kFG] : __ldcg(a.prm + dm.bb[0][dir] + c);
         (void)direct;
         // raw rows staged in smem at the step start (zero padded to w0)
         const int w0 = round4(dm.d0);
@@ -658,7 +666,8 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
           float wk[8];
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            wk[kk] = k0 + kk < dm.d0 ? __ldcg(Wx + (int64_t)(k0 + kk) * kFG) : 0.f;
+            wk[kk] = k0 + kk < dm.d0 ? (a.l0_smem ? Wx[(k0 + kk) * kFG] : __ldcg(Wx + (int64_t)(k0 + kk) * kFG))
+                                     : 0.f;
           for (int t = 0; t < T; ++t) {
             float acc = k0 == 0 ? bc : xzr[(int64_t)t * kFG];
 #pragma unroll
@@ -688,7 +697,13 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     if (warp < 4) {
       WReg wh;
       const int dir = warp >> 1, sub = warp & 1;
-      if (direct) {
+      if (l == 0 && a.l0_smem) {
+        const float* Wh = W + dir * blk0 + dm.d0 * kFG + lane;
+#pragma unroll
+        for (int k = 0; k < kFH; ++k)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) wh[q * kFH + k] = Wh[k * kFG + (2 * sub + q) * kFH];
+      } else if (direct) {
         load_wh_cols(wh, a.prm + dm.wh[l][dir], sub);
       } else {
         const float* Wh = W + dir * kBlk + kFD * kFG + lane;
@@ -1346,6 +1361,17 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       fmark(step, 0);
       if (step > 0)  // layer 0's update (the other groups are awaited where prefetched)
         wait_counter(a.ctr + ctr_adam(dm, 0), (unsigned)(step * group_jobs(dm, 0)), false);
+      if (a.l0_smem && (tid >> 5) == 4) {
+        // layer 0's two direction blocks [Wx | Wh | b] into W (bulk copies; the
+        // previous step's attention weights there are dead), overlapping the
+        // metadata / step-row staging below
+        const uint32_t blk0 = (uint32_t)(dm.d0 + kFH + 1) * kFG;
+        sm100::fence_proxy_async_smem();
+        if ((tid & 31) == 0) sm100::mbar_expect_tx(&s_wbar, 2u * blk0 * 4u);
+        __syncwarp();
+        if ((tid & 31) < 2)
+          sm100::bulk_g2s(sm + a.sl.W + (tid & 31) * blk0, a.prm + dm.wx[0][tid & 31], blk0 * 4u, &s_wbar);
+      }
       fmark(step, 1);
       if (r == 0) fmark_any(step, 31);
       // step counts, labels and slot metadata: prefetched into smem during the
@@ -1467,7 +1493,7 @@ struct FastPlan {
   FastXch xl;
   size_t smem;
   int64_t rch, pc_off;
-  int pc_n;
+  int pc_n, l0_smem;
   int n_jobs;
 };
 
@@ -1509,6 +1535,7 @@ inline bool fast_plan(const TDims& dm, int B, int grid, FastPlan& p) {
   need = std::max(need, (size_t)(job_fixed + p.rch * (kap_max + nbp)) * sizeof(float));
   p.smem = need;
   p.pc_n = kap_max * nbp;
+  p.l0_smem = (int64_t)2 * (dm.d0 + kFH + 1) * kFG <= p.sl.total - p.sl.W ? 1 : 0;
   p.pc_off = (int64_t)(need / sizeof(float)) - 4 * (int64_t)p.pc_n;
   return true;
 }
@@ -1520,6 +1547,7 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   a.n_jobs = p.n_jobs;
   a.rch = p.rch;
   a.pc_off = p.pc_off;
+  a.l0_smem = p.l0_smem;
   a.pc_n = p.pc_n;
   a.xch = reinterpret_cast<float*>(w);
   w += align_up((size_t)p.xl.total * sizeof(float), 256);
