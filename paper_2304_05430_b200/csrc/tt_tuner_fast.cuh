@@ -1028,10 +1028,31 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
   float* dZ = sm + L.dZ;
   float* part = sm + L.xz;  // [4][TM][64] dX partials (xz is dead)
   const int xk = tid & 63, xq = tid >> 6, xdir = xq >> 1, xhalf = xq & 1;
+  // Wh rows of layer l-1 are prefetched into W (rows padded to 132 floats,
+  // double-buffered by layer parity) by warps 4..7 during BPTT of layer l, so
+  // only the first backward layer reads its Wh rows from L2.
+  constexpr int kLdWh = 132;
+  float* const Wm = sm + L.W;
+  auto whs = [&](int ll) { return Wm + (ll & 1) * (2 * kFH * kLdWh); };
   for (int l = dm.L - 1; l >= 0; --l) {
     WReg whr;
     float wx[64];
-    if (warp < 4) load_wh_row(whr, a.prm + dm.wh[l][warp >> 1], warp & 1);
+    if (warp < 4) {
+      if (l == dm.L - 1) {
+        load_wh_row(whr, a.prm + dm.wh[l][warp >> 1], warp & 1);
+      } else {
+        const float4* w4 =
+            reinterpret_cast<const float4*>(whs(l) + ((warp >> 1) * kFH + lane) * kLdWh + (warp & 1) * 64);
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const float4 v = w4[m];
+          whr[4 * m + 0] = v.x;
+          whr[4 * m + 1] = v.y;
+          whr[4 * m + 2] = v.z;
+          whr[4 * m + 3] = v.w;
+        }
+      }
+    }
     if (l > 0) {
       const float4* w4 =
           reinterpret_cast<const float4*>(a.prm + dm.wx[l][xdir] + (int64_t)xk * kFG + xhalf * 64);
@@ -1050,8 +1071,17 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
                    a.xch + X.dZ + (((int64_t)l * 2 + (warp >> 1)) * X.Rmax + rs) * kFG,
                    sm + L.gex);
       if (warp == 0) fmark(step, 11 + (dm.L - 1 - l) * 2);
-    } else if (warp == 7 && l == dm.L - 1) {
-      prefetch_next_sample(a, step, sm + L.lbn);
+    } else {
+      if (warp == 7 && l == dm.L - 1) prefetch_next_sample(a, step, sm + L.lbn);
+      if (l > 0) {
+        // next backward layer's Wh rows -> the other W buffer
+        float* dst = whs(l - 1);
+        for (int e = tid - 128; e < 2 * kFH * (kFG / 4); e += kThreads - 128) {
+          const int row = e >> 5, q = e & 31;  // row = dir*32 + j
+          cp_async16(dst + row * kLdWh + q * 4, a.prm + dm.wh[l - 1][row >> 5] + (row & 31) * kFG + q * 4);
+        }
+        cp_async_wait_all();
+      }
     }
     __syncthreads();
     signal_counter(a.ctr + ctr_bwd(l), 1);  // this layer's dZ published
