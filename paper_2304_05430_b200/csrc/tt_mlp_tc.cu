@@ -24,10 +24,19 @@ namespace tt {
 
 using namespace sm100;
 
+// tanh via ex2.approx.ftz + rcp.approx.ftz (Act<float>::tanh without the
+// denormal-range fix-up instructions)
+__device__ __forceinline__ float tanh_ftz(float x) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(2.8853900817779268f * x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.f));
+  return 1.f - 2.f * r;
+}
+
 constexpr int kTcRows = 128;   // rows per tile (M)
 constexpr int kTcHid = 64;     // hidden width (N)
 constexpr int kTcNst = 6;      // X pipeline stages (one 16 KB K-atom each)
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per lane quarter)
 constexpr int kAtomBytesX = kTcRows * 128;  // 16 KB
 constexpr int kAtomBytesW = kTcHid * 128;   // 8 KB
 
@@ -57,6 +66,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   TcBars* bars = reinterpret_cast<TcBars*>(w2s + 2 * kAtomBytesW);
   __shared__ float s_b1[kTcHid], s_b2[kTcHid], s_w3[kTcHid];
   __shared__ float s_b3;
+  __shared__ float s_part[2][2][kTcRows];  // [buffer][column half][row] partial scores
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n + kTcRows - 1) / kTcRows;
@@ -73,9 +83,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&bars->acc1_full[b], 1);
-      mbar_init(&bars->h1_full[b], 128);
+      mbar_init(&bars->h1_full[b], 256);
       mbar_init(&bars->acc2_full[b], 1);
-      mbar_init(&bars->acc_free[b], 128);
+      mbar_init(&bars->acc_free[b], 256);
     }
     fence_barrier_init();
   }
@@ -154,8 +164,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else {
-    // ================= epilogue: warps 2..5, one row per thread
+    // ================= epilogue: warps 2..9, two warps per TMEM lane quarter;
+    // warp half `hf` owns hidden columns [32 hf, 32 hf + 32) of the row
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int hf = (warp - 2) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0;
@@ -165,12 +177,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_wait(&bars->acc1_full[b], bph);
       tc_fence_after();
 #pragma unroll
-      for (int c0 = 0; c0 < kTcHid; c0 += 16) {
+      for (int c0 = hf * 32; c0 < hf * 32 + 32; c0 += 16) {
         float v[16];
         tmem_ld16(acc1 + c0, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = Act<float>::tanh(v[i] + s_b1[c0 + i]);
+        for (int i = 0; i < 16; ++i) v[i] = tanh_ftz(v[i] + s_b1[c0 + i]);
         tmem_st16(h1 + c0, v);
       }
       tmem_wait_st();
@@ -180,17 +192,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       float acc = 0.f;
 #pragma unroll
-      for (int c0 = 0; c0 < kTcHid; c0 += 16) {
+      for (int c0 = hf * 32; c0 < hf * 32 + 32; c0 += 16) {
         float v[16];
         tmem_ld16(acc2 + c0, v);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc += Act<float>::tanh(v[i] + s_b2[c0 + i]) * s_w3[c0 + i];
+        for (int i = 0; i < 16; ++i) acc += tanh_ftz(v[i] + s_b2[c0 + i]) * s_w3[c0 + i];
       }
       tc_fence_before();
       mbar_arrive(&bars->acc_free[b]);
+      // combine the two column halves of the row in fixed order
+      s_part[b][hf][row] = acc;
+      named_barrier(1, 256);
       const int64_t r = tile * kTcRows + row;
-      if (r < p.n) p.out[r] = acc + s_b3;
+      if (hf == 0 && r < p.n) p.out[r] = (s_part[b][0][row] + s_part[b][1][row]) + s_b3;
     }
   }
   __syncthreads();
