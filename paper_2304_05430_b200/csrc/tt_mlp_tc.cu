@@ -24,13 +24,12 @@ namespace tt {
 
 using namespace sm100;
 
-// tanh via ex2.approx.ftz + rcp.approx.ftz (Act<float>::tanh without the
-// denormal-range fix-up instructions)
+// tanh on the MUFU's native tanh.approx (one SFU op instead of ex2 + rcp):
+// max abs error ~5e-4, inside the tf32 mode's stated 1e-2 / 1e-3 tolerance
 __device__ __forceinline__ float tanh_ftz(float x) {
-  float e, r;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(2.8853900817779268f * x));
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.f));
-  return 1.f - 2.f * r;
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 constexpr int kTcRows = 128;   // rows per tile (M)
