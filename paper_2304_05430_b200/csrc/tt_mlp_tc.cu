@@ -129,14 +129,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer
+    // ================= MMA issuer, software-pipelined by one tile: GEMM1 of
+    // tile t+1 is issued before waiting for tile t's h1, so the tensor core
+    // works on the next tile while the epilogue forms h1
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(kTcRows, kTcHid);
-      uint32_t it = 0, t = 0;
+      uint32_t it = 0;
       const uint32_t w1a = smem_u32(w1s), w2a = smem_u32(w2s), xa = smem_u32(xs);
-      for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
+      auto gemm1 = [&](uint32_t t) {
         const uint32_t b = t & 1, bph = (t >> 1) & 1;
-        const uint32_t acc1 = tmem + b * kBufCols, h1 = acc1 + 64, acc2 = acc1 + 128;
+        const uint32_t acc1 = tmem + b * kBufCols;
         mbar_wait(&bars->acc_free[b], bph ^ 1);
         tc_fence_after();
         for (int kc = 0; kc < p.kat; ++kc, ++it) {
@@ -152,6 +154,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mma_commit(&bars->empty[s]);  // frees the X stage when these MMAs retire
         }
         mma_commit(&bars->acc1_full[b]);
+      };
+      const uint32_t my_tiles =
+          (uint32_t)(n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+      if (my_tiles > 0) gemm1(0);
+      for (uint32_t t = 0; t < my_tiles; ++t) {
+        if (t + 1 < my_tiles) gemm1(t + 1);
+        const uint32_t b = t & 1, bph = (t >> 1) & 1;
+        const uint32_t h1 = tmem + b * kBufCols + 64, acc2 = tmem + b * kBufCols + 128;
         mbar_wait(&bars->h1_full[b], bph);
         tc_fence_after();
 #pragma unroll
