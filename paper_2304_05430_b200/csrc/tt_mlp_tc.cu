@@ -34,7 +34,7 @@ __device__ __forceinline__ float tanh_ftz(float x) {
 
 constexpr int kTcRows = 128;   // rows per tile (M)
 constexpr int kTcHid = 64;     // hidden width (N)
-constexpr int kTcNst = 6;      // X pipeline stages (one 16 KB K-atom each)
+constexpr int kTcNst = 9;      // X pipeline stages (one 16 KB K-atom each; 1.5 tiles of F = 164 in flight)
 constexpr int kTcThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per lane quarter)
 constexpr int kAtomBytesX = kTcRows * 128;  // 16 KB
 constexpr int kAtomBytesW = kTcHid * 128;   // 8 KB
