@@ -824,15 +824,33 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
   const float sq = sqrtf((float)dh);
   float* const xpin = a.xch + X.pin + (int64_t)slot * U * kFD;
   float* const xmix = a.xch + X.mix + (int64_t)slot * U * kFD;
+  // Passes (tuner.py:259-274), warp-specialised: warp h owns head h end to
+  // end -- its 32-column slice of q = pooled Wq + bq, the logits and softmax
+  // over the program's steps, and its slice of mix -- with no block barrier;
+  // one barrier before pooled = mix Wo + bo (threads 0..63) and one after.
   for (int u = 0; u < U; ++u) {
     float* q = sm + L.q + u * kFD;
+    float* mix = sm + L.mix + u * kFD;
+    float* al = sm + L.alpha + (int64_t)u * heads * TM;
     if (tid < kFD) {
       sm[L.pin + u * kFD + tid] = pool[tid];
       xpin[u * kFD + tid] = pool[tid];
     }
-    fcol_mv(pool, Wq, kFD, bq, q, red);
-    float* al = sm + L.alpha + (int64_t)u * heads * TM;
     for (int h = warp; h < heads; h += kThreads / 32) {
+      for (int i = lane; i < dh; i += 32) {  // q_h
+        const int c = h * dh + i;
+        const float* wc = Wq + c;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+        for (int k = 0; k < kFD; k += 4) {
+          a0 = fmaf(pool[k], wc[k * kLdA], a0);
+          a1 = fmaf(pool[k + 1], wc[(k + 1) * kLdA], a1);
+          a2 = fmaf(pool[k + 2], wc[(k + 2) * kLdA], a2);
+          a3 = fmaf(pool[k + 3], wc[(k + 3) * kLdA], a3);
+        }
+        q[c] = bq[c] + ((a0 + a1) + (a2 + a3));
+      }
+      __syncwarp();
       const float* qh = q + h * dh;
       float* ar = al + (int64_t)h * TM;
       float mx = -INFINITY;
@@ -850,11 +868,34 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
       }
       sum = warp_sum(sum);
       for (int t = lane; t < T; t += 32) ar[t] = ar[t] / sum;
+      __syncwarp();
+      for (int i = lane; i < dh; i += 32) {  // mix_h
+        const int c = h * dh + i;
+        float a0 = 0.f, a1 = 0.f;
+        int t = 0;
+        for (; t + 1 < T; t += 2) {
+          a0 = fmaf(ar[t], V[(int64_t)t * kLdK + c], a0);
+          a1 = fmaf(ar[t + 1], V[(int64_t)(t + 1) * kLdK + c], a1);
+        }
+        if (t < T) a0 = fmaf(ar[t], V[(int64_t)t * kLdK + c], a0);
+        mix[c] = a0 + a1;
+        xmix[u * kFD + c] = a0 + a1;
+      }
     }
     __syncthreads();
-    float* mix = sm + L.mix + u * kFD;
-    fmix(al, TM, dh, V, T, 1.f, mix, xmix + u * kFD, red);
-    fcol_mv(mix, Wo, kFD, bo, pool, red);
+    if (tid < kFD) {  // pooled = mix Wo + bo
+      const float* wc = Wo + tid;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll 4
+      for (int k = 0; k < kFD; k += 4) {
+        a0 = fmaf(mix[k], wc[k * kLdA], a0);
+        a1 = fmaf(mix[k + 1], wc[(k + 1) * kLdA], a1);
+        a2 = fmaf(mix[k + 2], wc[(k + 2) * kLdA], a2);
+        a3 = fmaf(mix[k + 3], wc[(k + 3) * kLdA], a3);
+      }
+      pool[tid] = bo[tid] + ((a0 + a1) + (a2 + a3));
+    }
+    __syncthreads();
     fmark(step, u == 0 ? 9 : 17);
   }
   float* zb = sm + L.zb;
