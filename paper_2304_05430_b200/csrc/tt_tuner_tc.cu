@@ -28,6 +28,7 @@
 // Precision: tf32 GEMM operands, fp32 everything else -- the "tf32" scoring
 // mode with its own stated tolerance (tests/test_gpu_tuner_tc.py); the
 // CUDA-core kernel (tt_tuner.cu) is the strict fp32 path.
+#define TT_TC_TANH_APPROX 1
 #include "tt_sm100.cuh"
 #include "tt_tuner.cuh"
 
@@ -57,10 +58,20 @@ __device__ __forceinline__ float rcpf(float x) {
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+#ifdef TT_TC_TANH_APPROX
+// one SFU op per activation (MUFU.TANH): sigmoid(x) = 0.5 tanh(x/2) + 0.5
+__device__ __forceinline__ float tanh_f(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float sig_f(float x) { return fmaf(0.5f, tanh_f(0.5f * x), 0.5f); }
+#else
 __device__ __forceinline__ float sig_f(float x) { return rcpf(1.f + ex2f(-1.4426950408889634f * x)); }
 __device__ __forceinline__ float tanh_f(float x) {
   return 1.f - 2.f * rcpf(ex2f(2.8853900817779268f * x) + 1.f);
 }
+#endif
 
 namespace sc {
 constexpr int kRows = 128;

@@ -1,7 +1,8 @@
 """Tensor-core (tcgen05, kind::tf32) tuner scoring vs the float64 oracle.
 
 The "tf32" precision mode multiplies tf32-rounded operands (10-bit mantissa)
-and accumulates in fp32; activations, softmax and the cell state stay fp32.
+and accumulates in fp32; the LSTM gates use the hardware tanh (MUFU.TANH,
+sigmoid = 0.5 tanh(x/2) + 0.5); softmax and the cell state stay fp32.
 Stated tolerance (reduced-precision GEMM operands with fp32
 score output): max |d| <= 2e-3 and mean |d| <= 2e-4 against the float64
 reference; pairwise order of clearly separated scores is preserved.
