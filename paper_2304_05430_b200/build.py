@@ -58,7 +58,29 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def build_host(force: bool = False) -> str:
+    """The CPython host module (csrc/host/tt_pack.c -> _ttpack*.so, gcc -O3)."""
+    import sysconfig
+
+    src = os.path.join(CSRC, "host", "tt_pack.c")
+    out = os.path.join(PKG, "_ttpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
+        return out
+    cc = os.environ.get("CC") or shutil.which("gcc") or "cc"
+    import numpy
+
+    cmd = [cc, "-O3", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+           "-I", numpy.get_include(), src,
+           "-o", out + ".tmp"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"host module build failed:\n{r.stdout}\n{r.stderr}")
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
+    build_host(force)
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     if force:

@@ -37,9 +37,44 @@ class HostPrograms:
         return int(np.max(np.diff(self.offsets))) if self.n else 0
 
 
+def _native():
+    try:
+        from . import _ttpack
+    except ImportError:  # not built: the vectorised numpy path below
+        return None
+    return _ttpack
+
+
+def _pack_native(seqs, step_width, ctx_len, alloc):
+    """csrc/host/tt_pack.c: one pass over the list (buffer protocol), dtype
+    conversion while copying into the buffers ``alloc(rows, n, d0, C)``
+    returns.  Returns the int64 offsets, or None (module missing / malformed
+    item: the caller's numpy path reports the exact error)."""
+    mod = _native()
+    if mod is None or len(seqs) == 0:
+        return None
+    lens = mod.pack(seqs, -1 if step_width is None else int(step_width),
+                    -1 if ctx_len is None else int(ctx_len), alloc)
+    if lens is None:
+        return None
+    lens = np.frombuffer(lens, dtype=np.int64)
+    off = np.zeros(lens.shape[0] + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    return off
+
+
 def pack_sequences(seqs, step_width: int | None = None, ctx_len: int | None = None) -> HostPrograms:
     if len(seqs) == 0:
         raise DataValidationError("empty sequence batch")
+    out = {}
+
+    def alloc(rows, n, d0, C):
+        out["s"], out["c"] = np.empty((rows, d0)), np.empty((n, C))
+        return out["s"], out["c"]
+
+    off = _pack_native(seqs, step_width, ctx_len, alloc)
+    if off is not None:
+        return HostPrograms(out["s"], off, out["c"])
     fast = _pack_fast(seqs, step_width, ctx_len)
     if fast is not None:
         return fast
@@ -98,18 +133,42 @@ class DevicePrograms:
 
     def __init__(self, host: HostPrograms, precision: str = "fp32"):
         dt = _device.real_dtype(precision)
-        t = _device.torch()
+        self._set(precision, host.offsets, _device.to_dev(host.steps.reshape(-1), dt),
+                  _device.to_dev(host.ctx.reshape(-1), dt), host.steps.shape[1], host.ctx.shape[1])
+
+    def _set(self, precision, offsets, steps, ctx, d0, C):
         self.precision = precision
-        self.n = host.n
-        self.d0 = host.steps.shape[1]
-        self.C = host.ctx.shape[1]
-        self.max_steps = host.max_steps
-        self.steps = _device.to_dev(host.steps.reshape(-1), dt)
-        self.offsets = _device.to_dev(host.offsets.astype(np.int64))
-        self.ctx = _device.to_dev(host.ctx.reshape(-1), dt)
-        self.host_offsets = host.offsets
-        self._t = t
+        self.n = offsets.shape[0] - 1
+        self.d0, self.C = int(d0), int(C)
+        self.max_steps = int(np.max(np.diff(offsets))) if self.n else 0
+        self.steps, self.ctx = steps, ctx
+        self.offsets = _device.to_dev(offsets.astype(np.int64))
+        self.host_offsets = offsets
 
     @classmethod
     def from_sequences(cls, seqs, precision="fp32", step_width=None, ctx_len=None):
-        return cls(pack_sequences(seqs, step_width, ctx_len), precision)
+        """Host sequences -> device CSR.  With the native packer the rows are
+        converted straight into pinned compute-dtype staging buffers and
+        copied with one async H2D each (no float64 intermediate)."""
+        if len(seqs) == 0:
+            raise DataValidationError("empty sequence batch")
+        t = _device.require_cuda()
+        dt = _device.real_dtype(precision)
+        out = {}
+
+        def alloc(rows, n, d0, C):
+            out["s"] = t.empty((rows, d0), dtype=dt, pin_memory=True)
+            out["c"] = t.empty((n, C), dtype=dt, pin_memory=True)
+            out["d0"], out["C"] = d0, C
+            return out["s"].numpy(), out["c"].numpy()
+
+        off = _pack_native(seqs, step_width, ctx_len, alloc)
+        if off is None:
+            return cls(pack_sequences(seqs, step_width, ctx_len), precision)
+        dev = _device.device()
+        self = cls.__new__(cls)
+        self._set(precision, off, out["s"].reshape(-1).to(dev, non_blocking=True),
+                  out["c"].reshape(-1).to(dev, non_blocking=True), out["d0"], out["C"])
+        # (torch's pinned-host allocator holds the staging blocks until the
+        # copies recorded on the current stream have completed)
+        return self
