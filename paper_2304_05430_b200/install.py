@@ -13,6 +13,8 @@ the search scorer (models.py:364-378) and the CLI -- through the kernels:
   tensortune.models.per_task_metrics             -> one batched K1 + K10 launch
   tensortune.transfer._grouped_pca               -> metrics.grouped_pca
   tensortune.sampling.filter_invalid             -> sampling.filter_invalid (K2)
+  tensortune.features / .models / .transfer
+      encode_sequence_batch, encode_flat_batch   -> featurize (batched labels)
 
 ``uninstall()`` restores the originals.
 """
@@ -24,6 +26,7 @@ import sys
 import numpy as np
 
 from . import estimators as _est
+from . import featurize as _feat
 from . import metrics as _met
 from . import sampling as _samp
 
@@ -99,6 +102,12 @@ def install() -> None:
                make_per_task_metrics(mods["tensortune.models"]))
     _patch(mods["tensortune.transfer"], "_grouped_pca", _met.grouped_pca)
     _patch(mods["tensortune.sampling"], "filter_invalid", _samp.filter_invalid)
+    import tensortune.features as features
+
+    enc_seq, enc_flat = _feat.make_encoders(features)
+    for key in ("tensortune.features", "tensortune.models", "tensortune.transfer"):
+        _patch(sys.modules.get(key), "encode_sequence_batch", enc_seq)
+        _patch(sys.modules.get(key), "encode_flat_batch", enc_flat)
 
 
 def uninstall() -> None:
