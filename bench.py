@@ -244,7 +244,7 @@ def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
     return out
 
 
-def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam):
+def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam, batch=BATCH):
     """Per-phase marks of one minibatch inside the train kernel (CTA 0 clock64
     at 1965 MHz; the first gradient-job CTA in %globaltimer ns)."""
     import ctypes
@@ -265,7 +265,7 @@ def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam):
         ctypes.memmove(buf0, (ctypes.c_int64 * 32)(), 32 * 8)
         perm = _device.to_dev(rng.permutation(n).astype(np.int32))
         corr = _device.to_dev(_bias_corrections(t_adam, n_steps))
-        est._launch_train(dims, flat, m, v, prog, yd, perm, BATCH, _lib.TT_MODE_TRAIN, 1e-3, corr, None)
+        est._launch_train(dims, flat, m, v, prog, yd, perm, batch, _lib.TT_MODE_TRAIN, 1e-3, corr, None)
         t_adam += n_steps
         torch.cuda.synchronize()
         buf = (ctypes.c_int64 * 32)()
@@ -347,7 +347,7 @@ def run_b200(args, world, rank):
         t_adam += n_steps
     torch.cuda.synchronize()
     if args.phases and dp is None:
-        print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam)
+        print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam, args.phase_batch)
         t_adam += 3 * n_steps
     # pre-stage the timed epochs' inputs so the timed region holds only kernels
     perms = [_device.to_dev(rng.permutation(n).astype(np.int32)) for _ in range(args.steps)]
@@ -475,6 +475,35 @@ def run_b200(args, world, rank):
         extra["pca_pairs_per_s"] = pairs / pt
         extra["pca_mean"] = float(np.mean(c / (PER_TASK * (PER_TASK - 1) / 2)))
         extra.update(mlp_scoring(l2, stream, peaks))
+        # large-batch variants of C2: one epoch at B = 256 / 1024
+        for bb in (256, 1024):
+            nsb = (n + bb - 1) // bb
+            fl, mm, vv = flat.clone(), torch.zeros_like(flat), torch.zeros_like(flat)
+            ts = []
+            for k in range(2):
+                pb = _device.to_dev(rng.permutation(n).astype(np.int32))
+                cb = _device.to_dev(_bias_corrections(k * nsb, nsb))
+                flush_l2(l2)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                est._launch_train(dims, fl, mm, vv, prog, yd, pb, bb, _lib.TT_MODE_TRAIN, 1e-3, cb, None)
+                e1.record(stream)
+                ts.append((e0, e1))
+            torch.cuda.synchronize()
+            extra[f"train_b{bb}_samples_per_s"] = n / (ts[-1][0].elapsed_time(ts[-1][1]) / 1e3)
+        # search-time scoring latency through the public API (host sequences
+        # in, float64 scores out): one SA step scores 1, one evolution
+        # generation <= 32 candidates (search.py:319, :392-410)
+        few = as_seqs(steps, off, ctx)[:32]
+        for k_ in (1, 32):
+            est.predict(few[:k_])
+            w = []
+            for _ in range(20):
+                t0_ = time.perf_counter()
+                est.predict(few[:k_])
+                w.append(time.perf_counter() - t0_)
+            extra[f"predict_latency_{k_}_us"] = float(np.median(w)) * 1e6
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(steps, off, ctx, y)
@@ -509,6 +538,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--phase-batch", type=int, default=BATCH, help="minibatch of the --phases probe")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--profile", action="store_true", help="small dataset for ncu captures")
     ap.add_argument("--phases", action="store_true", help="print per-phase train-step timings")

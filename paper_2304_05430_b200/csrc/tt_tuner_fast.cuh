@@ -34,7 +34,8 @@ namespace tt {
 
 constexpr int kFH = 32, kFD = 64, kFG = 128;  // hidden, 2H, 4H
 constexpr int kLdA = 68;  // staged attention weights row stride (16-B rows, see frow_mv)
-constexpr int kMaxFastB = 160;  // minibatch limit of the latency path
+constexpr int kMaxFastB = 160;   // minibatch limit of the latency path (one slot per CTA)
+constexpr int kMaxRoundB = 2048; // minibatch limit of the multi-round mode
 constexpr int kLdK = 65;        // K/V row stride in smem (odd: lanes over steps hit distinct banks)
 
 __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
@@ -42,7 +43,7 @@ __host__ __device__ inline int round4(int x) { return (x + 3) & ~3; }
 // ------------------------------------------------------------ layouts --
 struct FastSmem {  // float offsets in dynamic shared memory (sample role)
   int64_t x0, lbn, ctxs, S, gc, cs, xz, hb, gex, K, V, alpha, pin, q, mix, pool, zb, a1, red, lb, dS, dS2, dZ, dK,
-      dV, dlg, dmix, dq, dpool, da1, W, total;
+      dV, dlg, dmix, dq, dpool, da1, ts, rsb, W, total;
 };
 
 struct FastXch {  // float offsets in the (stacked) exchange region
@@ -50,6 +51,12 @@ struct FastXch {  // float offsets in the (stacked) exchange region
   int w0, zw;
   int64_t x0, H, cst, S, dZ, dK, dV, pin, mix, dpool, dq, z, a1, da1, dl, total;
 };
+
+// attention + head weight image at the start of W (row stride kLdA):
+// [Wq|Wk|Wv|Wo|bq|bo] then [W1|b1|W2|b2]
+__host__ __device__ inline int64_t fast_attn_floats(const TDims& d) {
+  return (int64_t)(4 * kFD + 2) * kLdA + (int64_t)(kFD + d.C + 3) * kLdA;
+}
 
 inline FastSmem make_fast_smem(const TDims& d, int B) {
   FastSmem s{};
@@ -61,7 +68,6 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   };
   const int TM = d.Tmax;
   s.x0 = seg((int64_t)TM * round4(d.d0));
-  s.lbn = seg(B);
   s.ctxs = seg(d.C);
   s.S = seg((int64_t)d.L * TM * kFD);
   s.gc = seg((int64_t)d.L * 2 * TM * kFG);
@@ -78,8 +84,9 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   s.pool = seg(kFD);
   s.zb = seg(kFD + d.C);
   s.a1 = seg(kHeadHidden);
-  s.red = seg(std::max(kThreads, 2 * B));
+  s.red = seg(std::max(2 * kThreads, 2 * B));
   s.lb = seg((int64_t)3 * B);
+  s.lbn = seg(B);
   s.dS = seg((int64_t)TM * kFD);
   s.dS2 = seg((int64_t)TM * kFD);
   s.dZ = seg((int64_t)2 * TM * kFG);
@@ -90,11 +97,12 @@ inline FastSmem make_fast_smem(const TDims& d, int B) {
   s.dq = seg(kFD);
   s.dpool = seg(kFD);
   s.da1 = seg(kHeadHidden);
+  s.ts = seg(B);   // int: step count of every minibatch slot
+  s.rsb = seg(B);  // int: first stacked exchange row of every slot
   // attention + head weights, row stride 68: [Wq|Wk|Wv|Wo|bq|bo] then [W1|b1|W2]
   // attention/head weights (row stride 68, + b2 row) or one LSTM layer's two
   // direction blocks [Wx | Wh | b] (128 columns)
-  s.W = seg(std::max<int64_t>((int64_t)(4 * kFD + 2) * kLdA + (int64_t)(kFD + d.C + 3) * kLdA,
-                              (int64_t)2 * (kFD + kFH + 1) * kFG));
+  s.W = seg(std::max<int64_t>(fast_attn_floats(d), (int64_t)2 * (kFD + kFH + 1) * kFG));
   s.total = o;
   return s;
 }
@@ -249,7 +257,10 @@ struct FastArgs {
   float* xch;          // stacked exchange (FastXch)
   int64_t* meta;       // [B]: steps of each minibatch slot
   float* yhat_buf;     // [B]
-  unsigned int* ctr;   // [0] fwd, [1] bwd, [2] adam (monotone)
+  float* lossp;        // [B][2]: per-slot pair-loss partials (multi-round mode)
+  float* scache;       // [B][sl.red - sl.x0]: per-slot forward caches (multi-round mode)
+  float* wcache;       // [grid][attn_floats]: attention/head weight image per CTA (multi-round)
+  unsigned int* ctr;   // [0] fwd, [1 + g] bwd, [2 + L + g] adam, [kCtrLoss] loss (monotone)
   int n_jobs;
   int64_t rch;         // job staging rows per chunk
   int64_t pc_off;      // smem float offset of a job CTA's parameter cache [4][pc_n]
@@ -263,6 +274,7 @@ struct FastArgs {
 __shared__ int s_prof;
 // Weight-prefetch barrier of a sample CTA (bulk copies into W) and its phase.
 __shared__ __align__(8) uint64_t s_wbar;
+__shared__ __align__(8) uint64_t s_cbar;  // multi-round cache restores
 __shared__ uint32_t s_wph;
 
 // CTA 0, clock64 (cycles)
@@ -288,6 +300,7 @@ __device__ __forceinline__ void fmark_any(int step, int i) {
 // forward waits per layer, so the Adam updates of the upper layers overlap
 // the next forward's first layers.
 __device__ __forceinline__ int ctr_bwd(int g) { return 1 + g; }
+constexpr int kCtrLoss = 63;  // last of the 64 counters (L <= 30)
 __device__ __forceinline__ int ctr_adam(const TDims& d, int g) { return 2 + d.L + g; }
 __device__ __forceinline__ int job_group(const TDims& d, int j) {
   for (int l = 0; l < d.L; ++l) {
@@ -928,7 +941,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
 // Next-minibatch metadata of this CTA (kernel-wide shared state).
 __shared__ int64_t s_nmeta[3];
 __shared__ int s_pref;
-__shared__ int s_T[kMaxFastB], s_Tn[kMaxFastB];
+__shared__ int s_Tn[kMaxFastB];
 
 // Warp 7 during the first BPTT layer: fetch the next minibatch's step counts,
 // labels and this CTA's slot metadata into shared memory (none depends on
@@ -1113,7 +1126,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
                    sm + L.gex);
       if (warp == 0) fmark(step, 11 + (dm.L - 1 - l) * 2);
     } else {
-      if (warp == 7 && l == dm.L - 1) prefetch_next_sample(a, step, sm + L.lbn);
+      if (warp == 7 && l == dm.L - 1 && a.B <= (int)gridDim.x) prefetch_next_sample(a, step, sm + L.lbn);
       if (l > 0) {
         // next backward layer's Wh rows -> the other W buffer
         float* dst = whs(l - 1);
@@ -1400,6 +1413,59 @@ __device__ float fast_rank_loss(const float* y, const float* s, int n, float* ds
   return loss;
 }
 
+// Multi-round mode: the pair terms of this CTA's own slots only (rows
+// k = r, r + G, ..; warp per row, lanes sweep j), unnormalised dscore into
+// smem and the row's (loss part, pair count) into the global partials.
+__device__ void fast_rank_rows(const float* y, const float* s, int n, int r, int G, float* dscore,
+                               float* lossp) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = r + warp * G; k < n; k += (kThreads / 32) * G) {
+    const float yk = y[k], sk = s[k];
+    float d = 0.f, part = 0.f, pairs = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float yj = y[j], sj = s[j];
+      if (yj > yk) d += 1.f / (1.f + Act<float>::exp(sj - sk));
+      if (yk > yj) {
+        const float mg = sk - sj;
+        d -= 1.f / (1.f + Act<float>::exp(mg));
+        part += Act<float>::softplus(-mg);
+        pairs += 1.f;
+      }
+    }
+    d = warp_sum(d);
+    part = warp_sum(part);
+    pairs = warp_sum(pairs);
+    if (lane == 0) {
+      dscore[k] = d;
+      lossp[2 * k] = part;
+      lossp[2 * k + 1] = pairs;
+    }
+  }
+}
+
+// Fixed-order sum of the published partials (identical in every CTA).
+__device__ void fast_sum_partials(const float* lossp, int n, float* red, float* out2) {
+  const int tid = threadIdx.x;
+  float a = 0.f, b = 0.f;
+  for (int k = tid; k < n; k += kThreads) {
+    a += __ldcg(lossp + 2 * k);
+    b += __ldcg(lossp + 2 * k + 1);
+  }
+  red[tid] = a;
+  red[kThreads + tid] = b;
+  __syncthreads();
+  if (tid == 0) {
+    float ta = 0.f, tb = 0.f;
+    for (int i = 0; i < kThreads; ++i) {
+      ta += red[i];
+      tb += red[kThreads + i];
+    }
+    out2[0] = ta;
+    out2[1] = tb;
+  }
+  __syncthreads();
+}
+
 // ------------------------------------------------------------ kernel --
 __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1412,6 +1478,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     s_prof = g_prof_step;
     s_wph = 0;
     sm100::mbar_init(&s_wbar, 1);
+    sm100::mbar_init(&s_cbar, 1);
     sm100::fence_barrier_init();
   }
   __syncthreads();
@@ -1420,29 +1487,83 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
   const int tid = threadIdx.x;
   const int G = gridDim.x, r = blockIdx.x;
   const bool sampler = r < a.B;
-  const int first_job = (r - a.B + G) % G;
+  const int first_job = ((r - a.B) % G + G) % G;
   int my_jobs = 0, last_job = -1;
   for (int j = first_job; j < a.n_jobs; j += G) ++my_jobs, last_job = j;
   float* lb = sm + a.sl.lb;
+  int* const sT = reinterpret_cast<int*>(sm + a.sl.ts);
+  int* const sRs = reinterpret_cast<int*>(sm + a.sl.rsb);
+  // layer 0's two direction blocks [Wx | Wh | b] into W (bulk copies by warp
+  // 4; the attention weights there are dead), awaited inside the forward
+  auto issue_l0 = [&]() {
+    if (a.l0_smem && (tid >> 5) == 4) {
+      const uint32_t blk0 = (uint32_t)(dm.d0 + kFH + 1) * kFG;
+      sm100::fence_proxy_async_smem();
+      if ((tid & 31) == 0) sm100::mbar_expect_tx(&s_wbar, 2u * blk0 * 4u);
+      __syncwarp();
+      if ((tid & 31) < 2)
+        sm100::bulk_g2s(sm + a.sl.W + (tid & 31) * blk0, a.prm + dm.wx[0][tid & 31], blk0 * 4u, &s_wbar);
+    }
+  };
+  // raw step rows of slot k -> smem (layer-0 projection) and the stacked
+  // exchange (layer-0 weight gradient), zero padded to 16 B rows; context row
+  auto stage_rows = [&](int64_t rs, int64_t r0, int T, int64_t idx) {
+    const int w0 = a.xl.w0;
+    const float* x0 = a.steps + r0 * dm.d0;
+    float* xg = a.xch + a.xl.x0 + rs * w0;
+    for (int i = tid; i < T * w0; i += kThreads) {
+      const int t = i / w0, k = i - t * w0;
+      const float v = k < dm.d0 ? __ldg(x0 + (int64_t)t * dm.d0 + k) : 0.f;
+      sm[a.sl.x0 + i] = v;
+      xg[i] = v;
+    }
+    for (int i = tid; i < dm.C; i += kThreads) sm[a.sl.ctxs + i] = __ldg(a.ctx + idx * dm.C + i);
+    __syncthreads();
+  };
+  // multi-round mode: a slot's forward caches ([x0, red) of the sample
+  // layout) and the attention/head weight image in W go to L2 by bulk
+  // stores after its forward and come back by bulk loads before its
+  // backward (instead of recomputing the forward)
+  const int64_t cfl = a.sl.red - a.sl.x0;
+  const int64_t wfl = fast_attn_floats(dm);
+  uint32_t cph = 0;
+  auto save_slot = [&](int k, bool with_w) {
+    __syncthreads();
+    if (tid == 0) {
+      sm100::fence_proxy_async_smem();
+      sm100::bulk_s2g(a.scache + (int64_t)k * cfl, sm + a.sl.x0, (uint32_t)(cfl * 4));
+      if (with_w) sm100::bulk_s2g(a.wcache + (int64_t)r * wfl, sm + a.sl.W, (uint32_t)(wfl * 4));
+      sm100::bulk_commit();
+      sm100::bulk_wait_read0();
+    }
+    __syncthreads();
+  };
+  auto restore_slot = [&](int k) {
+    __syncthreads();
+    if (tid == 0) {
+      sm100::bulk_wait0();
+      sm100::fence_proxy_async_smem();
+      sm100::mbar_expect_tx(&s_cbar, (uint32_t)((cfl + wfl) * 4));
+      sm100::bulk_g2s(sm + a.sl.x0, a.scache + (int64_t)k * cfl, (uint32_t)(cfl * 4), &s_cbar);
+      sm100::bulk_g2s(sm + a.sl.W, a.wcache + (int64_t)r * wfl, (uint32_t)(wfl * 4), &s_cbar);
+    }
+    sm100::mbar_wait(&s_cbar, cph);
+    cph ^= 1u;
+  };
   for (int step = 0; step < a.n_steps; ++step) {
     const int64_t b0 = (int64_t)step * a.B;
     const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
     const unsigned cum = (unsigned)(b0 + bn);
     if (sampler && r < bn) {
+      // slots k = r, r + G, ..: one per CTA on the latency path (B <= grid);
+      // large minibatches run several rounds per CTA (forward of every slot,
+      // loss, then per slot a recomputed forward -- the last slot's caches
+      // are still resident -- and its backward)
+      const int nmine = (bn - r + G - 1) / G;
       fmark(step, 0);
       if (step > 0)  // layer 0's update (the other groups are awaited where prefetched)
         wait_counter(a.ctr + ctr_adam(dm, 0), (unsigned)(step * group_jobs(dm, 0)), false);
-      if (a.l0_smem && (tid >> 5) == 4) {
-        // layer 0's two direction blocks [Wx | Wh | b] into W (bulk copies; the
-        // previous step's attention weights there are dead), overlapping the
-        // metadata / step-row staging below
-        const uint32_t blk0 = (uint32_t)(dm.d0 + kFH + 1) * kFG;
-        sm100::fence_proxy_async_smem();
-        if ((tid & 31) == 0) sm100::mbar_expect_tx(&s_wbar, 2u * blk0 * 4u);
-        __syncwarp();
-        if ((tid & 31) < 2)
-          sm100::bulk_g2s(sm + a.sl.W + (tid & 31) * blk0, a.prm + dm.wx[0][tid & 31], blk0 * 4u, &s_wbar);
-      }
+      issue_l0();
       fmark(step, 1);
       if (r == 0) fmark_any(step, 31);
       // step counts, labels and slot metadata: prefetched into smem during the
@@ -1452,7 +1573,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
           const int64_t idx = a.order[b0 + i];
           const int64_t r0 = a.rowoff[idx], r1 = a.rowoff[idx + 1];
           lb[i] = a.y[idx];
-          s_T[i] = (int)(r1 - r0);
+          sT[i] = (int)(r1 - r0);
           if (i == r) {
             s_nmeta[0] = idx;
             s_nmeta[1] = r0;
@@ -1462,41 +1583,81 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       } else {
         for (int i = tid; i < bn; i += kThreads) {
           lb[i] = sm[a.sl.lbn + i];
-          s_T[i] = s_Tn[i];
+          sT[i] = s_Tn[i];
         }
       }
       __syncthreads();
-      const int64_t idx = s_nmeta[0], r0 = s_nmeta[1];
-      const int T = (int)s_nmeta[2];
-      int64_t rs = 0;  // first stacked row of this sample
-      for (int i = 0; i < r; ++i) rs += s_T[i];
-      if (tid == 0) a.meta[r] = T;
-      {
-        // raw step rows -> smem (layer-0 projection) and the stacked exchange
-        // (layer-0 weight gradient), zero padded to 16 B rows
-        const int w0 = a.xl.w0;
-        const float* x0 = a.steps + r0 * dm.d0;
-        float* xg = a.xch + a.xl.x0 + rs * w0;
-        for (int i = tid; i < T * w0; i += kThreads) {
-          const int t = i / w0, k = i - t * w0;
-          const float v = k < dm.d0 ? __ldg(x0 + (int64_t)t * dm.d0 + k) : 0.f;
-          sm[a.sl.x0 + i] = v;
-          xg[i] = v;
+      if (a.B > G && tid < 32) {  // exclusive prefix of the step counts (stacked rows)
+        int carry = 0;
+        for (int base = 0; base < bn; base += 32) {
+          const int i = base + tid;
+          const int v = i < bn ? sT[i] : 0;
+          int inc = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, o);
+            if (tid >= o) inc += u;
+          }
+          if (i < bn) sRs[i] = carry + inc - v;
+          carry += __shfl_sync(0xffffffffu, inc, 31);
         }
-        for (int i = tid; i < dm.C; i += kThreads) sm[a.sl.ctxs + i] = __ldg(a.ctx + idx * dm.C + i);
       }
-      __syncthreads();
-      const float yh = fast_sample_fwd(a, sm, rs, r, r0, T, idx, step);
+      if (a.B > G) __syncthreads();
+      for (int m = 0; m < nmine; ++m) {
+        const int k = r + m * G;
+        int64_t idx, r0;
+        int T;
+        if (m == 0) {
+          idx = s_nmeta[0];
+          r0 = s_nmeta[1];
+          T = (int)s_nmeta[2];
+        } else {
+          idx = a.order[b0 + k];
+          r0 = a.rowoff[idx];
+          T = sT[k];
+          issue_l0();
+        }
+        if (tid == 0) a.meta[k] = T;
+        int64_t rs;
+        if (a.B <= G) {  // one slot: only its own first stacked row
+          rs = 0;
+          for (int i = 0; i < r; ++i) rs += sT[i];
+          if (tid == 0) sRs[k] = (int)rs;  // for the backward (after stage_rows' barrier)
+        } else {
+          rs = sRs[k];
+        }
+        stage_rows(rs, r0, T, idx);
+        const float yh = fast_sample_fwd(a, sm, rs, k, r0, T, idx, step);
+        if (tid == 0) a.yhat_buf[k] = yh;
+        signal_counter(a.ctr + 0, 1);
+        if (m + 1 < nmine) save_slot(k, m == 0);
+      }
       fmark(step, 5);
-      if (tid == 0) a.yhat_buf[r] = yh;
-      signal_counter(a.ctr + 0, 1);
       wait_counter(a.ctr + 0, cum, false);
       fmark(step, 6);
       for (int i = tid; i < bn; i += kThreads) lb[bn + i] = __ldcg(a.yhat_buf + i);
       __syncthreads();
-      const float loss = a.loss_kind == TT_LOSS_RANK
-                             ? fast_rank_loss(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red)
-                             : mse_block<float>(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red);
+      float loss;
+      if (a.loss_kind == TT_LOSS_RANK && a.B > G) {
+        // O(B^2) pairs: each CTA evaluates its own rows, the loss total is
+        // exchanged through L2 (one more counter)
+        fast_rank_rows(lb, lb + bn, bn, r, G, lb + 2 * bn, a.lossp);
+        signal_counter(a.ctr + kCtrLoss, (unsigned)nmine);
+        wait_counter(a.ctr + kCtrLoss, cum, false);
+        __shared__ float s_lt[2];
+        fast_sum_partials(a.lossp, bn, sm + a.sl.red, s_lt);
+        const float np = s_lt[1];
+        for (int m = tid; m < nmine; m += kThreads) {
+          const int k = r + m * G;
+          lb[2 * bn + k] = np == 0.f ? 0.f : lb[2 * bn + k] / np;
+        }
+        loss = np == 0.f ? 0.f : s_lt[0] / np;
+        __syncthreads();
+      } else {
+        loss = a.loss_kind == TT_LOSS_RANK
+                   ? fast_rank_loss(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red)
+                   : mse_block<float>(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red);
+      }
       if (tid == 0) {
         s_stop = !isfinite(loss);
         if (r == 0) {
@@ -1507,9 +1668,14 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       __syncthreads();
       fmark(step, 7);
       if (!s_stop) {
-        fast_sample_bwd(a, sm, rs, r, T, lb[2 * bn + r], yh, step);
+        for (int m = nmine - 1; m >= 0; --m) {
+          const int k = r + m * G;
+          const int T = sT[k];
+          if (m != nmine - 1) restore_slot(k);  // the last slot's caches are resident
+          fast_sample_bwd(a, sm, sRs[k], k, T, lb[2 * bn + k], lb[bn + k], step);
+        }
       } else {
-        for (int g = 0; g <= dm.L; ++g) signal_counter(a.ctr + ctr_bwd(g), 1);  // wake the jobs
+        for (int g = 0; g <= dm.L; ++g) signal_counter(a.ctr + ctr_bwd(g), (unsigned)nmine);  // wake the jobs
       }
       fmark(step, 16);
       if (r == 0) fmark_any(step, 30);
@@ -1570,16 +1736,24 @@ struct FastPlan {
 
 inline size_t fast_ws_bytes(const TDims& dm, int B) {
   const FastXch xl = make_fast_xch(dm, B);
-  return align_up((size_t)xl.total * sizeof(float), 256) + align_up((size_t)B * 8, 256) +
-         align_up((size_t)B * sizeof(float), 256) + 256;
+  size_t b = align_up((size_t)xl.total * sizeof(float), 256) + align_up((size_t)B * 8, 256) +
+             align_up((size_t)B * sizeof(float), 256) + align_up((size_t)B * 2 * sizeof(float), 256) + 256;
+  if (B > sm_count()) {  // multi-round: per-slot forward caches + per-CTA weight images
+    const FastSmem sl = make_fast_smem(dm, B);
+    b += align_up((size_t)B * (sl.red - sl.x0) * sizeof(float), 256) +
+         align_up((size_t)sm_count() * fast_attn_floats(dm) * sizeof(float), 256);
+  }
+  return b;
 }
 
 // Eligible: fp32, hidden 32, one sample per CTA, every per-sample cache in
 // shared memory.  Returns false (generic kernel) otherwise.
 inline bool fast_plan(const TDims& dm, int B, int grid, FastPlan& p) {
-  if (dm.H != kFH || B > grid || B > kMaxFastB || B < 1 || dm.Tmax > 32 || dm.heads < 1 ||
-      kFD % (4 * dm.heads) != 0)
+  // B <= grid: one slot per CTA (latency path, <= kMaxFastB for the metadata
+  // prefetch); larger minibatches run ceil(B / grid) rounds per CTA
+  if (dm.H != kFH || B < 1 || dm.Tmax > 32 || dm.heads < 1 || kFD % (4 * dm.heads) != 0)
     return false;
+  if (B <= grid ? B > kMaxFastB : B > kMaxRoundB) return false;
   int dev = 0, optin = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
@@ -1626,6 +1800,15 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   w += align_up((size_t)a.B * 8, 256);
   a.yhat_buf = reinterpret_cast<float*>(w);
   w += align_up((size_t)a.B * sizeof(float), 256);
+  a.lossp = reinterpret_cast<float*>(w);
+  w += align_up((size_t)a.B * 2 * sizeof(float), 256);
+  a.scache = a.wcache = nullptr;
+  if (a.B > sm_count()) {
+    a.scache = reinterpret_cast<float*>(w);
+    w += align_up((size_t)a.B * (p.sl.red - p.sl.x0) * sizeof(float), 256);
+    a.wcache = reinterpret_cast<float*>(w);
+    w += align_up((size_t)sm_count() * fast_attn_floats(a.dm) * sizeof(float), 256);
+  }
   a.ctr = reinterpret_cast<unsigned int*>(w);
   TT_CUDA(cudaMemsetAsync(a.ctr, 0, 256, st));
   auto kern = tuner_train_fast_kernel;

@@ -150,3 +150,37 @@ def test_fast_and_generic_epochs_agree(cuda_ok):
     for k in res[1].params_:
         a, b = res[1].params_[k], res[2].params_[k]
         assert np.linalg.norm(a - b) <= 1e-3 * max(np.linalg.norm(a), 1e-12), k
+
+
+@pytest.mark.parametrize("n,loss", [(149, "ranking"), (300, "rmse"), (1024, "ranking")])
+def test_multi_round_gradients_match_oracle(cuda_ok, n, loss):
+    """Minibatches larger than the grid: several slots per CTA (forward of
+    every slot, loss, recomputed forward + backward per slot)."""
+    rng = np.random.default_rng(n)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=n))
+    y = rng.uniform(0.1, 0.9, size=n)
+    m = make(epochs=0, seed=2, loss=loss).fit(seqs, y)
+    p = otuner.init_params(2)
+    want_l, want = otuner.loss_and_gradients(p, seqs, y, loss)
+    res = {}
+    for path in (1, 2):
+        with train_path(path):
+            l, g = _grads(m, seqs, y)
+        assert l == pytest.approx(want_l, rel=1e-5), path
+        assert relative_gradient_error(g, want) <= 1e-4, path
+        res[path] = g
+    assert relative_gradient_error(res[2], res[1]) <= 1e-4
+
+
+def test_multi_round_trajectory(cuda_ok):
+    rng = np.random.default_rng(31)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=700))  # 2 x 300 + 100
+    y = rng.uniform(0.1, 0.9, size=700)
+    with train_path(2):
+        m = make(epochs=2, batch_size=300, loss="ranking", seed=4).fit(seqs, y)
+    p = otuner.init_params(4)
+    curve = otuner.train(p, seqs, y, epochs=2, lr=1e-3, batch_size=300, seed=4, loss="ranking")
+    np.testing.assert_allclose([c[0] for c in m.train_curve_], [c[0] for c in curve], rtol=1e-3)
+    for k in p:
+        err = np.linalg.norm(m.params_[k] - p[k]) / max(np.linalg.norm(p[k]), 1e-12)
+        assert err <= 2e-3, (k, err)
