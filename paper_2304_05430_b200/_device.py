@@ -27,11 +27,18 @@ def torch():
     return _torch
 
 
+_cuda_ok = False
+
+
 def require_cuda():
+    global _cuda_ok
     t = torch()
+    if _cuda_ok:  # checked once per process (is_available costs ~4 us per call)
+        return t
     if not t.cuda.is_available():
         raise _lib.LibraryError("paper_2304_05430_b200 needs a CUDA device (B200, sm_100a); none is visible")
     _lib.load()
+    _cuda_ok = True
     return t
 
 

@@ -148,27 +148,40 @@ class DevicePrograms:
     @classmethod
     def from_sequences(cls, seqs, precision="fp32", step_width=None, ctx_len=None):
         """Host sequences -> device CSR.  With the native packer the rows are
-        converted straight into pinned compute-dtype staging buffers and
-        copied with one async H2D each (no float64 intermediate)."""
+        converted straight into ONE pinned staging buffer [steps | ctx |
+        offsets] in the compute dtype and uploaded with one async copy."""
         if len(seqs) == 0:
             raise DataValidationError("empty sequence batch")
         t = _device.require_cuda()
         dt = _device.real_dtype(precision)
+        esz = 8 if dt == t.float64 else 4
+        npdt = np.float64 if esz == 8 else np.float32
         out = {}
 
         def alloc(rows, n, d0, C):
-            out["s"] = t.empty((rows, d0), dtype=dt, pin_memory=True)
-            out["c"] = t.empty((n, C), dtype=dt, pin_memory=True)
-            out["d0"], out["C"] = d0, C
-            return out["s"].numpy(), out["c"].numpy()
+            ns, nc = rows * d0, n * C
+            o_c = -(-ns * esz // 16) * 16
+            o_o = -(-(o_c + nc * esz) // 16) * 16
+            buf = t.empty(o_o + (n + 1) * 8, dtype=t.uint8, pin_memory=True)
+            hb = buf.numpy()
+            out.update(buf=buf, hb=hb, d0=d0, C=C, ns=ns, nc=nc, o_c=o_c, o_o=o_o)
+            return hb[:ns * esz].view(npdt), hb[o_c:o_c + nc * esz].view(npdt)
 
         off = _pack_native(seqs, step_width, ctx_len, alloc)
         if off is None:
             return cls(pack_sequences(seqs, step_width, ctx_len), precision)
-        dev = _device.device()
+        o = out
+        o["hb"][o["o_o"]:].view(np.int64)[:] = off
+        dev = o["buf"].to(_device.device(), non_blocking=True)
+        # (torch's pinned-host allocator keeps the staging block until the
+        # copy recorded on the current stream has completed)
         self = cls.__new__(cls)
-        self._set(precision, off, out["s"].reshape(-1).to(dev, non_blocking=True),
-                  out["c"].reshape(-1).to(dev, non_blocking=True), out["d0"], out["C"])
-        # (torch's pinned-host allocator holds the staging blocks until the
-        # copies recorded on the current stream have completed)
+        self.precision = precision
+        self.n = off.shape[0] - 1
+        self.d0, self.C = int(o["d0"]), int(o["C"])
+        self.max_steps = int(np.max(np.diff(off)))
+        self.steps = dev[:o["ns"] * esz].view(dt)
+        self.ctx = dev[o["o_c"]:o["o_c"] + o["nc"] * esz].view(dt)
+        self.offsets = dev[o["o_o"]:].view(t.int64)
+        self.host_offsets = off
         return self
