@@ -1107,7 +1107,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
         }
       }
     }
-    if (l > 0) {
+    auto load_wx = [&]() {
       const float4* w4 =
           reinterpret_cast<const float4*>(a.prm + dm.wx[l][xdir] + (int64_t)xk * kFG + xhalf * 64);
 #pragma unroll
@@ -1117,6 +1117,20 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
         wx[4 * m + 1] = v.y;
         wx[4 * m + 2] = v.z;
         wx[4 * m + 3] = v.w;
+      }
+    };
+    // dX operands: warps 4..7 (direction 1) hold their Wx slice in registers
+    // from L2; the recurrence warps must not have L2 loads outstanding during
+    // the BPTT (they slow its per-step exchange), so warps 4..7 also stage
+    // direction 0's Wx rows into the Wh buffer this layer no longer needs
+    // (rows padded to 132 floats) and warps 0..3 read them after the BPTT
+    if (l > 0 && l < dm.L - 1) __syncthreads();  // whr is out of whs(l)
+    if (l > 0 && warp >= 4) {
+      load_wx();
+      float* dst = whs(l);
+      for (int e = tid - 128; e < kFD * (kFG / 4); e += kThreads - 128) {
+        const int row = e >> 5, q = e & 31;
+        cp_async16(dst + row * kLdWh + q * 4, a.prm + dm.wx[l][0] + (int64_t)row * kFG + q * 4);
       }
     }
     if (warp < 4) {
@@ -1140,6 +1154,17 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
     __syncthreads();
     signal_counter(a.ctr + ctr_bwd(l), 1);  // this layer's dZ published
     if (l == 0) break;
+    if (warp < 4) {
+      const float4* w4 = reinterpret_cast<const float4*>(whs(l) + xk * kLdWh + xhalf * 64);
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const float4 v = w4[m];
+        wx[4 * m + 0] = v.x;
+        wx[4 * m + 1] = v.y;
+        wx[4 * m + 2] = v.z;
+        wx[4 * m + 3] = v.w;
+      }
+    }
     for (int t = 0; t < T; ++t)
       part[((int64_t)xq * TM + t) * kFD + xk] =
           dot64<0>(dZ + ((int64_t)xdir * TM + t) * kFG + xhalf * 64, wx);
