@@ -9,8 +9,9 @@
 //   warps 2..5  epilogue, one tile row per thread (TMEM lane): tanh(acc1+b1)
 //               is written back to TMEM as GEMM2's A operand; tanh(acc2+b2)
 //               . W3 + b3 is the score, stored coalesced.
-// TMEM holds two tile buffers (acc1 | h1 | acc2, 192 columns each) so the
-// epilogue of tile i overlaps the MMAs of tile i+1 and the loads of i+2.
+// TMEM holds four tile buffers (acc1 -> h1 in place | acc2, 128 columns
+// each) so GEMM1 runs up to three tiles ahead of the epilogue and the X ring
+// drains as soon as stages land.
 // Weights (W1^T zero-padded to K=ceil(F/32)*32, W2^T) are staged once per
 // CTA in the K-major SW128 layout.
 //
@@ -36,6 +37,7 @@ constexpr int kTcRows = 128;   // rows per tile (M)
 constexpr int kTcHid = 64;     // hidden width (N)
 constexpr int kTcNst = 9;      // X pipeline stages (one 16 KB K-atom each; 1.5 tiles of F = 164 in flight)
 constexpr int kTcThreads = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per lane quarter)
+constexpr int kTcBufs = 4;       // TMEM tile buffers (128 columns each)
 constexpr int kAtomBytesX = kTcRows * 128;  // 16 KB
 constexpr int kAtomBytesW = kTcHid * 128;   // 8 KB
 
@@ -49,7 +51,7 @@ struct MlpTcParams {
 
 struct __align__(8) TcBars {
   uint64_t full[kTcNst], empty[kTcNst];
-  uint64_t acc1_full[2], h1_full[2], acc2_full[2], acc_free[2];
+  uint64_t acc1_full[kTcBufs], h1_full[kTcBufs], acc2_full[kTcBufs], acc_free[kTcBufs];
   uint32_t tmem_base;
 };
 
@@ -65,7 +67,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   TcBars* bars = reinterpret_cast<TcBars*>(w2s + 2 * kAtomBytesW);
   __shared__ float s_b1[kTcHid], s_b2[kTcHid], s_w3[kTcHid];
   __shared__ float s_b3;
-  __shared__ float s_part[2][2][kTcRows];  // [buffer][column half][row] partial scores
+  __shared__ float s_part[kTcBufs][2][kTcRows];  // [buffer][column half][row] partial scores
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n + kTcRows - 1) / kTcRows;
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&bars->full[s], 1);
       mbar_init(&bars->empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kTcBufs; ++b) {
       mbar_init(&bars->acc1_full[b], 1);
       mbar_init(&bars->h1_full[b], 256);
       mbar_init(&bars->acc2_full[b], 1);
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  constexpr uint32_t kBufCols = 192;
+  constexpr uint32_t kBufCols = 128;
 
   if (warp == 0) {
     // ================= TMA producer
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       uint32_t it = 0;
       const uint32_t w1a = smem_u32(w1s), w2a = smem_u32(w2s), xa = smem_u32(xs);
       auto gemm1 = [&](uint32_t t) {
-        const uint32_t b = t & 1, bph = (t >> 1) & 1;
+        const uint32_t b = t % kTcBufs, bph = (t / kTcBufs) & 1;
         const uint32_t acc1 = tmem + b * kBufCols;
         mbar_wait(&bars->acc_free[b], bph ^ 1);
         tc_fence_after();
@@ -160,8 +162,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (my_tiles > 0) gemm1(0);
       for (uint32_t t = 0; t < my_tiles; ++t) {
         if (t + 1 < my_tiles) gemm1(t + 1);
-        const uint32_t b = t & 1, bph = (t >> 1) & 1;
-        const uint32_t h1 = tmem + b * kBufCols + 64, acc2 = tmem + b * kBufCols + 128;
+        const uint32_t b = t % kTcBufs, bph = (t / kTcBufs) & 1;
+        const uint32_t h1 = tmem + b * kBufCols, acc2 = tmem + b * kBufCols + 64;
         mbar_wait(&bars->h1_full[b], bph);
         tc_fence_after();
 #pragma unroll
@@ -181,8 +183,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t t = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
-      const uint32_t b = t & 1, bph = (t >> 1) & 1;
-      const uint32_t acc1 = tmem + lane_off + b * kBufCols, h1 = acc1 + 64, acc2 = acc1 + 128;
+      const uint32_t b = t % kTcBufs, bph = (t / kTcBufs) & 1;
+      const uint32_t acc1 = tmem + lane_off + b * kBufCols, h1 = acc1, acc2 = acc1 + 64;
       mbar_wait(&bars->acc1_full[b], bph);
       tc_fence_after();
 #pragma unroll
