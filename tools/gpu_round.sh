@@ -17,6 +17,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
     --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $OUT/${TAG}_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tuner_train -s 3 -c 1 \
     -o $OUT/${TAG}_prof_train_full python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-extra > $OUT/${TAG}_prof_train_full.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:'tuner_predict_tc|mlp_predict_tc|pca_tile' -c 3 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:'tuner_predict_tc|mlp_predict_tc|pca_tile' -c 12 \
     -o $OUT/${TAG}_prof_scoring python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > $OUT/${TAG}_prof_scoring.log 2>&1
 ls -la $OUT
