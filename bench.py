@@ -207,6 +207,90 @@ def flush_l2(buf):
     buf.fill_(1)
 
 
+def survey_configs(est, dims, flat, l2, stream, n_steps16, prog, yd, prng):
+    """The other SURVEY §8d configurations at their stated sizes (device-timed
+    with CUDA events unless noted): C3 bulk scoring of 4 M programs, C4 PCA
+    over 2,308 tasks x 4096 (half the tasks' labels rounded to 3 decimals
+    for ties) and its log-uniform-size variant, C5 pruning statistics over
+    64 x 4096 records and a heads-only fine-tuning epoch."""
+    import torch
+
+    from paper_2304_05430_b200 import _device, _lib
+    from paper_2304_05430_b200 import metrics as gm
+    from paper_2304_05430_b200.estimators import _bias_corrections
+    from paper_2304_05430_b200.layout import DevicePrograms, HostPrograms
+    from paper_2304_05430_b200.sampling import filter_stats
+
+    out = {}
+
+    def ev_time(fn, reps=2):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush_l2(l2)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        return float(np.mean([a.elapsed_time(b) for a, b in ts])) / 1e3
+
+    # C3: 4 M programs, T from the generator histogram
+    st, of, cx, _, ln = synth(n_tasks=1024, per_task=4096, seed=11)
+    big = DevicePrograms(HostPrograms(st, of, cx), "fp32")
+    del st, cx
+    nb = big.n
+    for prec, key in (("tf32", "c3_scoring_4M_tc_tf32_programs_per_s"),
+                      ("fp32", "c3_scoring_4M_fp32_programs_per_s")):
+        est.precision = prec
+        out[key] = nb / ev_time(lambda: est._predict_programs(big, dims, flat))
+    est.precision = "fp32"
+    del big
+    # C4: PCA over 2,308 tasks x 4096 (19.36 G pairs) and n_t log-uniform in [64, 4096]
+    rng = np.random.default_rng(4)
+    for name, sizes in (("c4_pca", np.full(2308, 4096)),
+                        ("c4_pca_loguniform", np.exp(rng.uniform(np.log(64), np.log(4096), 2308)).astype(np.int64))):
+        toff = np.zeros(len(sizes) + 1, dtype=np.int64)
+        np.cumsum(sizes, out=toff[1:])
+        yv = rng.uniform(0.05, 1.0, size=int(toff[-1]))
+        for t in range(0, len(sizes), 2):
+            yv[toff[t]:toff[t + 1]] = np.round(yv[toff[t]:toff[t + 1]], 3)
+        yt = torch.tensor(yv, device="cuda")
+        st_ = torch.randn(int(toff[-1]), dtype=torch.float64, device="cuda")
+        gm.pca_counts(yt, st_, toff)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gm.pca_counts(yt, st_, toff)
+        dt = time.perf_counter() - t0
+        pairs = float(np.sum(sizes * (sizes - 1) / 2))
+        out[f"{name}_pairs_per_s"] = pairs / dt
+        out[f"{name}_tasks_per_s"] = len(sizes) / dt
+    # C5: pruning statistics (K2) over 64 x 4096 records (wall, host arrays in,
+    # masks out) and one heads-only fine-tuning epoch at B = 16
+    n5 = N_TASKS * PER_TASK
+    fl = rng.integers(1 << 20, 1 << 40, size=n5)
+    co = rng.lognormal(-9, 0.5, size=n5)
+    va = rng.uniform(size=n5) > 0.02
+    poff = np.arange(0, n5 + 1, PER_TASK, dtype=np.int64)
+    filter_stats(fl, co, va, poff, 0.1, 8)
+    t0 = time.perf_counter()
+    filter_stats(fl, co, va, poff, 0.1, 8)
+    out["c5_prune_stats_records_per_s"] = n5 / (time.perf_counter() - t0)
+    host = est.__dict__["_host"]
+    heads = set(est.param_groups()["attention"]) | set(est.param_groups()["head"])
+    mask = _device.to_dev(np.concatenate([np.full(host[k].size, k in heads, dtype=np.uint8)
+                                          for k in dims["names"]]))
+    fl_, mm, vv = flat.clone(), torch.zeros_like(flat), torch.zeros_like(flat)
+    perm = _device.to_dev(prng.permutation(prog.n).astype(np.int32))
+    corr = _device.to_dev(_bias_corrections(0, n_steps16))
+    tt = ev_time(lambda: est._launch_train(dims, fl_, mm, vv, prog, yd, perm, BATCH, _lib.TT_MODE_TRAIN,
+                                           1e-3, corr, mask), reps=1)
+    out["c5_heads_only_finetune_samples_per_s"] = prog.n / tt
+    return out
+
+
 def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
     """CostMLP bulk scoring at TenSet width (configs[0]/[2] shape): the
     tcgen05 tf32 kernel and the fp32 CUDA-core kernel, HBM roofline
@@ -504,6 +588,7 @@ def run_b200(args, world, rank):
                 est.predict(few[:k_])
                 w.append(time.perf_counter() - t0_)
             extra[f"predict_latency_{k_}_us"] = float(np.median(w)) * 1e6
+        extra.update(survey_configs(est, dims, flat, l2, stream, n_steps, prog, yd, rng))
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(steps, off, ctx, y)
