@@ -155,6 +155,32 @@ int tt_tuner_train_f64(double *d_params, double *d_m, double *d_v, const double 
                        double *d_step_loss, double *d_grad_out, int32_t *d_status, void *d_ws,
                        size_t ws_bytes, tt_stream_t stream);
 
+/* Heads-only fine-tuning (transfer.py fine_tune with trainable = the
+ * attention + head groups, tuner.py:397-425): the recurrent stack is frozen,
+ * so its last-layer outputs S are computed once per call and training steps
+ * run only attention, head, loss and their gradients.
+ *   tt_tuner_lstm_outputs_f32: tt_tuner_predict_f32 that also writes S in the
+ *     CSR row layout, d_s_out [sum T][2 * hidden] (same workspace).
+ *   tt_tuner_train_heads_f32: tt_tuner_train_f32 (mode TRAIN) reading S from
+ *     d_s_cache; the recurrent parameters and their moments are left
+ *     untouched whatever d_trainable says.  Latency-path kernel only
+ *     (hidden 32, batch <= 2048): TT_EINVAL otherwise. */
+int tt_tuner_lstm_outputs_f32(const float *d_params, const float *d_steps,
+                              const int64_t *d_row_offsets, const float *d_ctx, int64_t n,
+                              int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                              int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                              float *d_s_out, float *d_yhat, void *d_ws, size_t ws_bytes,
+                              tt_stream_t stream);
+int tt_tuner_train_heads_f32(float *d_params, float *d_m, float *d_v, const float *d_steps,
+                             const int64_t *d_row_offsets, const float *d_ctx, const float *d_y,
+                             const int32_t *d_order, int64_t n_order, int32_t batch_size,
+                             int32_t loss_kind, double lr, double b1, double b2, double eps,
+                             const double *d_corr, const uint8_t *d_trainable, int32_t layers,
+                             int32_t hidden, int32_t heads, int32_t unroll, int32_t step_width,
+                             int32_t ctx_len, int32_t max_steps, const float *d_s_cache,
+                             float *d_step_loss, int32_t *d_status, void *d_ws, size_t ws_bytes,
+                             tt_stream_t stream);
+
 /* Kernel selection for tt_tuner_train_f32: 0 = automatic (the latency-path
  * kernel when hidden = 32, batch <= #SMs and the per-sample caches fit in
  * shared memory, else the generic kernel), 1 = generic only, 2 = latency path

@@ -40,6 +40,9 @@ SIGNATURES: dict[str, tuple] = {
                            + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
     "tt_tuner_train_f64": (ctypes.c_int, [_P] * 7 + [_P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P, _P]
                            + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
+    "tt_tuner_lstm_outputs_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64] + [_I32] * 7 + [_P, _P, _P, _SZ, _P]),
+    "tt_tuner_train_heads_f32": (ctypes.c_int, [_P] * 7 + [_P, _I64, _I32, _I32, _D, _D, _D, _D, _P, _P]
+                                 + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
     "tt_tuner_train_set_path": (ctypes.c_int, [_I32]),
     "tt_debug_profile_step": (ctypes.c_int, [_I32]),
     "tt_debug_phase_times": (ctypes.c_int, [_P, _I32]),

@@ -27,7 +27,7 @@ template <typename R, int H, int P>
 __global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
     TDims dm, const R* __restrict__ prm, const R* __restrict__ steps,
     const int64_t* __restrict__ rowoff, const R* __restrict__ ctx, int64_t n,
-    R* __restrict__ yhat, R* __restrict__ scratch, int64_t slot_elems) {
+    R* __restrict__ yhat, R* __restrict__ scratch, int64_t slot_elems, R* __restrict__ s_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ TileInfo<R, P> ti;
   constexpr int D = 2 * H, G = 4 * H;
@@ -82,6 +82,17 @@ __global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
                                      buf[2] + P * TD, nullptr, nullptr, nullptr);
       __syncthreads();
       cur ^= 1;
+    }
+    if (s_out) {  // last-layer outputs in the CSR row layout (heads-only training cache)
+      const R* so = buf[cur ^ 1];
+      for (int pp = 0; pp < P; ++pp) {
+        const int64_t prog = ti.prog[pp];
+        if (prog < 0) continue;
+        const int64_t r0 = rowoff[prog];
+        const int len = ti.len[pp];
+        for (int i = threadIdx.x; i < len * D; i += kThreads)
+          s_out[(r0 + i / D) * D + i % D] = so[((int64_t)pp * dm.Tmax + i / D) * D + i % D];
+      }
     }
     // final layer output is buf[cur ^ 1]; K -> buf[cur], V -> buf[2]
     attention_head_fwd<R, H, P, false>(dm, aw, ti, buf[cur ^ 1], buf[cur], buf[2], am, nullptr,
@@ -314,7 +325,7 @@ struct Launch {
   template <int H>
   static int predict_h(const TDims& dm, const R* prm, const R* steps, const int64_t* rowoff,
                        const R* ctx, int64_t n, R* yhat, void* ws, size_t ws_bytes,
-                       cudaStream_t st) {
+                       cudaStream_t st, R* s_out) {
     constexpr int P = ScoreP<R>::value;
     const int64_t slot = (int64_t)3 * P * dm.Tmax * dm.D + (int64_t)2 * P * dm.Tmax * dm.G;
     const size_t smem = score_smem_bytes<R, P>(dm);
@@ -330,18 +341,18 @@ struct Launch {
       TT_REQUIRE(grid >= 1, "tuner predict: workspace too small");
     }
     kern<<<grid, kThreads, smem, st>>>(dm, prm, steps, rowoff, ctx, n, yhat,
-                                       static_cast<R*>(ws), slot);
+                                       static_cast<R*>(ws), slot, s_out);
     return check_launch("tuner predict");
   }
 
   static int predict(const TDims& dm, const R* prm, const R* steps, const int64_t* rowoff,
                      const R* ctx, int64_t n, R* yhat, void* ws, size_t ws_bytes,
-                     cudaStream_t st) {
+                     cudaStream_t st, R* s_out = nullptr) {
     switch (dm.H) {
-      case 4: return predict_h<4>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
-      case 8: return predict_h<8>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
-      case 16: return predict_h<16>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
-      case 32: return predict_h<32>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st);
+      case 4: return predict_h<4>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st, s_out);
+      case 8: return predict_h<8>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st, s_out);
+      case 16: return predict_h<16>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st, s_out);
+      case 32: return predict_h<32>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st, s_out);
     }
     set_error("tuner: hidden size %d unsupported (4, 8, 16, 32)", dm.H);
     return TT_EINVAL;
@@ -407,7 +418,8 @@ struct Launch {
     return check_launch("tuner train");
   }
 
-  static int train(TrainArgs<R> a, void* ws, size_t ws_bytes, cudaStream_t st) {
+  static int train(TrainArgs<R> a, void* ws, size_t ws_bytes, cudaStream_t st,
+                   const R* scache = nullptr) {
     if constexpr (std::is_same<R, float>::value) {
       // v4 latency path (tt_tuner_fast.cuh) when eligible, else the generic kernel
       FastPlan fp;
@@ -435,9 +447,11 @@ struct Launch {
         f.step_loss = a.step_loss;
         f.grad_out = a.grad_out;
         f.status = a.status;
+        f.s_frozen = scache;
         return fast_launch(f, fp, ws, st);
       }
       TT_REQUIRE(g_train_path != 2, "tuner train: fast path requested but not eligible");
+      TT_REQUIRE(scache == nullptr, "tuner train (heads only): not eligible for the latency-path kernel");
     }
     switch (a.dm.H) {
       case 4: return train_h<4>(a, ws, ws_bytes, st);
@@ -464,12 +478,13 @@ template <typename R>
 static int predict_entry(const R* prm, const R* steps, const int64_t* rowoff, const R* ctx,
                          int64_t n, int32_t L, int32_t H, int32_t heads, int32_t U, int32_t d0,
                          int32_t C, int32_t Tmax, R* yhat, void* ws, size_t ws_bytes,
-                         tt_stream_t st) {
+                         tt_stream_t st, R* s_out = nullptr) {
   if (int rc = check_dims(L, H, heads, U, d0, C, Tmax)) return rc;
   TT_REQUIRE(n >= 0, "tuner predict: negative n");
   if (n == 0) return TT_OK;
   const TDims dm = make_dims(L, H, heads, U, d0, C, Tmax);
-  return Launch<R>::predict(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, as_stream(st));
+  return Launch<R>::predict(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, as_stream(st),
+                            s_out);
 }
 
 template <typename R>
@@ -479,7 +494,7 @@ static int train_entry(R* prm, R* m, R* v, const R* steps, const int64_t* rowoff
                        double eps, const double* corr, const uint8_t* trainable, int32_t L,
                        int32_t H, int32_t heads, int32_t U, int32_t d0, int32_t C, int32_t Tmax,
                        R* step_loss, R* grad_out, int32_t* status, void* ws, size_t ws_bytes,
-                       tt_stream_t st) {
+                       tt_stream_t st, const R* scache = nullptr) {
   if (int rc = check_dims(L, H, heads, U, d0, C, Tmax)) return rc;
   TT_REQUIRE(B >= 1 && B <= 4096, "tuner train: batch size must be in [1, 4096]");
   TT_REQUIRE(n_order >= 1, "tuner train: empty order");
@@ -510,7 +525,7 @@ static int train_entry(R* prm, R* m, R* v, const R* steps, const int64_t* rowoff
   a.step_loss = step_loss;
   a.grad_out = grad_out;
   a.status = status;
-  return Launch<R>::train(a, ws, ws_bytes, as_stream(st));
+  return Launch<R>::train(a, ws, ws_bytes, as_stream(st), scache);
 }
 
 }  // namespace tt
@@ -569,6 +584,29 @@ int tt_tuner_train_f32(float* prm, float* m, float* v, const float* steps, const
   return train_entry<float>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind, mode,
                             lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C, Tmax,
                             step_loss, grad_out, status, ws, ws_bytes, st);
+}
+
+int tt_tuner_lstm_outputs_f32(const float* prm, const float* steps, const int64_t* rowoff,
+                              const float* ctx, int64_t n, int32_t L, int32_t H, int32_t heads,
+                              int32_t U, int32_t d0, int32_t C, int32_t Tmax, float* s_out,
+                              float* yhat, void* ws, size_t ws_bytes, tt_stream_t st) {
+  TT_REQUIRE(s_out != nullptr && yhat != nullptr, "tuner lstm outputs: null output");
+  return predict_entry<float>(prm, steps, rowoff, ctx, n, L, H, heads, U, d0, C, Tmax, yhat, ws,
+                              ws_bytes, st, s_out);
+}
+
+int tt_tuner_train_heads_f32(float* prm, float* m, float* v, const float* steps,
+                             const int64_t* rowoff, const float* ctx, const float* y,
+                             const int32_t* order, int64_t n_order, int32_t B, int32_t loss_kind,
+                             double lr, double b1, double b2, double eps, const double* corr,
+                             const uint8_t* trainable, int32_t L, int32_t H, int32_t heads,
+                             int32_t U, int32_t d0, int32_t C, int32_t Tmax,
+                             const float* s_cache, float* step_loss, int32_t* status, void* ws,
+                             size_t ws_bytes, tt_stream_t st) {
+  TT_REQUIRE(s_cache != nullptr, "tuner train (heads only): s_cache required");
+  return train_entry<float>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind,
+                            TT_MODE_TRAIN, lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C,
+                            Tmax, step_loss, nullptr, status, ws, ws_bytes, st, s_cache);
 }
 
 int tt_tuner_train_set_path(int32_t path) {

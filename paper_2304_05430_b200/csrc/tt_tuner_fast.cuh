@@ -258,6 +258,7 @@ struct FastArgs {
   int64_t* meta;       // [B]: steps of each minibatch slot
   float* yhat_buf;     // [B]
   float* lossp;        // [B][2]: per-slot pair-loss partials (multi-round mode)
+  const float* s_frozen;  // heads-only mode: frozen last-layer LSTM outputs [sum T][64] (else null)
   float* scache;       // [B][sl.red - sl.x0]: per-slot forward caches (multi-round mode)
   float* wcache;       // [grid][attn_floats]: attention/head weight image per CTA (multi-round)
   unsigned int* ctr;   // [0] fwd, [1 + g] bwd, [2 + L + g] adam, [kCtrLoss] loss (monotone)
@@ -655,13 +656,49 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
   // (two recurrences to land).
   const int att_l = dm.L >= 2 ? dm.L - 2 : 0;  // layer during which attention is prefetched
   const int blk0 = (dm.d0 + kFH + 1) * kFG;     // layer-0 direction block (a.l0_smem)
-  if (a.l0_smem) {
+  if (a.l0_smem && !a.s_frozen) {
     const uint32_t wph = s_wph;
     sm100::mbar_wait(&s_wbar, wph);
     __syncthreads();
     if (tid == 0) s_wph = wph ^ 1u;
   }
-  for (int l = 0; l < dm.L; ++l) {
+  // attention/head weights into 16-B rows of stride 68 (threads t0, t0 + stride, ..)
+  auto copy_attn = [&](int t0, int stride) {
+    const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
+    const float* src1 = a.prm + dm.Wq;
+    const float* src2 = a.prm + dm.W1;
+    const int tot = (rows1 + rows2) * 16 + 1;  // + the chunk holding b2
+    for (int e = t0; e < tot; e += stride) {
+      const int row = e >> 4, q = e & 15;
+      if (row < rows1)
+        cp_async16(W + row * kLdA + q * 4, src1 + e * 4);
+      else if (e + 1 < tot)
+        cp_async16(W1s + (row - rows1) * kLdA + q * 4, src2 + (e - rows1 * 16) * 4);
+      else  // b2 is the last parameter: a 4-byte copy stays inside the buffer
+        cp_async4(W1s + (int64_t)rows2 * kLdA, src2 + (int64_t)rows2 * 64);
+    }
+  };
+  if (a.s_frozen) {
+    // heads-only mode: the recurrent stack is frozen; its last-layer rows come
+    // from the cache (to smem for the attention and to the exchange for the
+    // Wk / Wv jobs) once the attention group's previous update is done
+    if (step > 0) {
+      if (tid == 0) {
+        const unsigned target = (unsigned)(step * group_jobs(dm, dm.L));
+        while (ld_acquire(a.ctr + ctr_adam(dm, dm.L)) < target) {
+        }
+      }
+      __syncthreads();
+    }
+    copy_attn(tid, kThreads);
+    float* Sl = S + (int64_t)(dm.L - 1) * TM * kFD;
+    for (int i = tid; i < T * kFD / 4; i += kThreads) cp_async16(Sl + i * 4, a.s_frozen + r0 * kFD + i * 4);
+    cp_async_wait_all();
+    __syncthreads();
+    float* xs = a.xch + X.S + ((int64_t)(dm.L - 1) * X.Rmax + rs) * kFD;
+    for (int i = tid; i < T * kFD; i += kThreads) xs[i] = Sl[i];
+  }
+  for (int l = a.s_frozen ? dm.L : 0; l < dm.L; ++l) {
     const bool direct = l == 0 || l == dm.L - 1;  // (the last layer's update was
                                                   //  awaited during layer att_l)
     {
@@ -758,21 +795,9 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
             if (lane < 2) sm100::bulk_g2s(W + lane * kBlk, a.prm + dm.wx[l + 1][lane], kBlk * 4u, &s_wbar);
           }
         } else {
-          // attention/head weights into 16-B rows of stride 68 (per-thread async
-          // copies; they have this and the last layer's recurrence to land)
-          const int rows1 = 4 * kFD + 2, rows2 = kFD + dm.C + 2;
-          const float* src1 = a.prm + dm.Wq;
-          const float* src2 = a.prm + dm.W1;
-          const int tot = (rows1 + rows2) * 16 + 1;  // + the chunk holding b2
-          for (int e = tid - 128; e < tot; e += kThreads - 128) {
-            const int row = e >> 4, q = e & 15;
-            if (row < rows1)
-              cp_async16(W + row * kLdA + q * 4, src1 + e * 4);
-            else if (e + 1 < tot)
-              cp_async16(W1s + (row - rows1) * kLdA + q * 4, src2 + (e - rows1 * 16) * 4);
-            else  // b2 is the last parameter: a 4-byte copy stays inside the buffer
-              cp_async4(W1s + (int64_t)rows2 * kLdA, src2 + (int64_t)rows2 * 64);
-          }
+          // attention/head weights (per-thread async copies; they have this
+          // and the last layer's recurrence to land)
+          copy_attn(tid - 128, kThreads - 128);
           // the last layer reads L2 directly at its start: await its update
           // here, off the critical path
           if (step > 0 && l + 1 == dm.L - 1) {
@@ -1073,6 +1098,7 @@ __device__ void fast_sample_bwd(const FastArgs& a, float* sm, int64_t rs, int sl
   __syncthreads();
   fmark(step, 10);
   signal_counter(a.ctr + ctr_bwd(dm.L), 1);  // attention/head operands published
+  if (a.s_frozen) return;  // heads-only mode: the recurrent stack is frozen
   // ---- LSTM stack in reverse (tuner.py:340-359).  Warps 0..3 run the two
   //      BPTT recurrences (a warp pair per direction); every thread holds a
   //      64-column slice of one Wx row for dX, fetched before the BPTT so the
@@ -1521,7 +1547,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
   // layer 0's two direction blocks [Wx | Wh | b] into W (bulk copies by warp
   // 4; the attention weights there are dead), awaited inside the forward
   auto issue_l0 = [&]() {
-    if (a.l0_smem && (tid >> 5) == 4) {
+    if (a.l0_smem && !a.s_frozen && (tid >> 5) == 4) {
       const uint32_t blk0 = (uint32_t)(dm.d0 + kFH + 1) * kFG;
       sm100::fence_proxy_async_smem();
       if ((tid & 31) == 0) sm100::mbar_expect_tx(&s_wbar, 2u * blk0 * 4u);
@@ -1536,7 +1562,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     const int w0 = a.xl.w0;
     const float* x0 = a.steps + r0 * dm.d0;
     float* xg = a.xch + a.xl.x0 + rs * w0;
-    for (int i = tid; i < T * w0; i += kThreads) {
+    for (int i = tid; i < (a.s_frozen ? 0 : T * w0); i += kThreads) {
       const int t = i / w0, k = i - t * w0;
       const float v = k < dm.d0 ? __ldg(x0 + (int64_t)t * dm.d0 + k) : 0.f;
       sm[a.sl.x0 + i] = v;
@@ -1586,7 +1612,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       // are still resident -- and its backward)
       const int nmine = (bn - r + G - 1) / G;
       fmark(step, 0);
-      if (step > 0)  // layer 0's update (the other groups are awaited where prefetched)
+      if (step > 0 && !a.s_frozen)  // layer 0's update (the other groups are awaited where prefetched)
         wait_counter(a.ctr + ctr_adam(dm, 0), (unsigned)(step * group_jobs(dm, 0)), false);
       issue_l0();
       fmark(step, 1);
@@ -1722,7 +1748,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     // (the order in which the samples publish their backward operands)
     const bool keep = !sampler && my_jobs == 1;
     bool a_staged = false;
-    if (keep) {
+    if (keep && !(a.s_frozen && job_group(dm, last_job) < dm.L)) {
       // single job: stage its A operand (forward data) while the samples run
       // their backward, so only the B operand waits for the backward counter
       __syncthreads();
@@ -1736,6 +1762,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
     }
     for (int j = last_job; j >= 0; j -= G) {
       const int g = job_group(dm, j);
+      if (a.s_frozen && g < dm.L) continue;  // heads-only: recurrent slices are frozen
       wait_counter(a.ctr + ctr_bwd(g), cum, !sampler);
       if (r == a.B % G) fmark_any(step, 20);
       if (tid == 0) s_stop = __ldcg(a.status) >= 0;

@@ -285,7 +285,8 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         del t
         return out
 
-    def _launch_train(self, dims, flat, m, v, prog, y_dev, order, B, mode, lr, corr, mask):
+    def _launch_train(self, dims, flat, m, v, prog, y_dev, order, B, mode, lr, corr, mask,
+                      frozen=None):
         t = _device.torch()
         prec = self._prec()
         dt = _device.real_dtype(prec)
@@ -299,6 +300,16 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         grad = _device.empty(flat.numel(), dt) if mode == _lib.TT_MODE_GRAD else None
         fn = "tt_tuner_train_f64" if prec == "fp64" else "tt_tuner_train_f32"
         loss_kind = _lib.TT_LOSS_RANK if self.loss == "ranking" else _lib.TT_LOSS_MSE
+        if frozen is not None:
+            # heads-only: the latency-path kernel reading the frozen last-layer outputs
+            _lib.call("tt_tuner_train_heads_f32", flat.data_ptr(), _device.ptr(m), _device.ptr(v),
+                      prog.steps.data_ptr(), prog.offsets.data_ptr(), prog.ctx.data_ptr(),
+                      y_dev.data_ptr(), order.data_ptr(), order.numel(), B, loss_kind, lr, _BETA1,
+                      _BETA2, _EPS, _device.ptr(corr), _device.ptr(mask), dims["L"], dims["H"],
+                      dims["heads"], dims["U"], dims["d0"], dims["C"], prog.max_steps,
+                      frozen.data_ptr(), step_loss.data_ptr(), status.data_ptr(), ws.data_ptr(),
+                      nbytes, _device.stream_ptr())
+            return step_loss, status, grad
         _lib.call(fn, flat.data_ptr(), _device.ptr(m), _device.ptr(v), prog.steps.data_ptr(),
                   prog.offsets.data_ptr(), prog.ctx.data_ptr(), y_dev.data_ptr(), order.data_ptr(),
                   order.numel(), B, loss_kind, mode, lr, _BETA1, _BETA2, _EPS,
@@ -308,6 +319,23 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
                   _device.stream_ptr())
         del t
         return step_loss, status, grad
+
+    def _frozen_outputs(self, dims, flat, prog):
+        """Last-layer LSTM outputs of every program (CSR rows x 2H) for
+        heads-only training, or None when that path does not apply."""
+        if self._prec() != "fp32" or dims["H"] != 32:
+            return None
+        lib = _lib.load()
+        nbytes = lib.tt_tuner_predict_workspace_bytes(0, dims["L"], dims["H"], prog.max_steps)
+        ws = _device.workspace(nbytes, "tuner_predict")
+        rows = int(prog.host_offsets[-1])
+        out = _device.empty(rows * 2 * dims["H"], _device.real_dtype("fp32"))
+        yhat = _device.empty(prog.n, _device.real_dtype("fp32"))
+        _lib.call("tt_tuner_lstm_outputs_f32", flat.data_ptr(), prog.steps.data_ptr(),
+                  prog.offsets.data_ptr(), prog.ctx.data_ptr(), prog.n, dims["L"], dims["H"],
+                  dims["heads"], dims["U"], dims["d0"], dims["C"], prog.max_steps,
+                  out.data_ptr(), yhat.data_ptr(), ws.data_ptr(), nbytes, _device.stream_ptr())
+        return out
 
     # -- public API (tuner.py:364-483) ---------------------------------------
 
@@ -394,11 +422,24 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
             ev = (eprog, ey, gperm, goff)
         t_step = 0
         n_steps = (n + B - 1) // B
+        # heads-only fine-tuning (no recurrent parameter trainable): the frozen
+        # stack's outputs are computed once and the steps run attention + head only
+        frozen = None
+        if trainable is not None and not (set(trainable) & set(self.param_groups()["recurrent"])):
+            frozen = self._frozen_outputs(dims, flat, prog)
         for epoch in range(epochs):
             perm = rng.permutation(n).astype(np.int32)
             corr = _device.to_dev(_bias_corrections(t_step, n_steps))
-            _, status, _ = self._launch_train(dims, flat, m, v, prog, y_dev, _device.to_dev(perm), B,
-                                              _lib.TT_MODE_TRAIN, float(learning_rate), corr, mask)
+            try:
+                _, status, _ = self._launch_train(dims, flat, m, v, prog, y_dev, _device.to_dev(perm), B,
+                                                  _lib.TT_MODE_TRAIN, float(learning_rate), corr, mask,
+                                                  frozen)
+            except _lib.LibraryError:
+                if frozen is None:
+                    raise
+                frozen = None  # not eligible for the heads-only kernel: full steps
+                _, status, _ = self._launch_train(dims, flat, m, v, prog, y_dev, _device.to_dev(perm), B,
+                                                  _lib.TT_MODE_TRAIN, float(learning_rate), corr, mask)
             if int(status.item()) >= 0:
                 raise NumericFailure(f"loss became non-finite at epoch {epoch}")
             t_step += n_steps

@@ -184,3 +184,40 @@ def test_multi_round_trajectory(cuda_ok):
     for k in p:
         err = np.linalg.norm(m.params_[k] - p[k]) / max(np.linalg.norm(p[k]), 1e-12)
         assert err <= 2e-3, (k, err)
+
+
+@pytest.mark.parametrize("batch", [16, 200])
+def test_heads_only_finetune_matches_oracle(cuda_ok, batch):
+    """continue_fit with only the attention + head groups trainable runs the
+    heads-only kernel (frozen last-layer LSTM outputs computed once); the
+    trajectory follows the oracle's filtered-gradient Adam (tuner.py:397-425)
+    and the full-step kernels."""
+    rng = np.random.default_rng(batch)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=450))
+    y = rng.uniform(0.1, 0.9, size=450)
+    base = make(epochs=1, batch_size=batch, loss="ranking", seed=5).fit(seqs, y)
+    p0 = {k: v.copy() for k, v in base.params_.items()}
+    g = base.param_groups()
+    heads = set(g["attention"]) | set(g["head"])
+    base.continue_fit(seqs, y, epochs=2, learning_rate=1e-3, trainable=heads)
+    for k in g["recurrent"]:
+        assert np.array_equal(base.params_[k], p0[k]), k
+    p = {k: v.copy() for k, v in p0.items()}
+    curve = otuner.train(p, seqs, y, epochs=2, lr=1e-3, batch_size=batch, seed=5, seed_offset=9001,
+                         trainable=heads, loss="ranking")
+    np.testing.assert_allclose([c[0] for c in base.train_curve_], [c[0] for c in curve], rtol=1e-3)
+    # fine-tuning from trained weights: the small bias gradients carry fp32
+    # noise that Adam's normalisation amplifies, hence the looser norm bound
+    for k in heads:
+        err = np.linalg.norm(base.params_[k] - p[k]) / max(np.linalg.norm(p[k]), 1e-12)
+        assert err <= 1e-2, (k, err)
+    # the generic kernel (full steps with the trainable mask) agrees
+    full = make(epochs=0, batch_size=batch, loss="ranking", seed=5).fit(seqs[:2], y[:2])
+    full.set_weights(p0)
+    with train_path(1):
+        full.continue_fit(seqs, y, epochs=2, learning_rate=1e-3, trainable=heads)
+    np.testing.assert_allclose([c[0] for c in base.train_curve_], [c[0] for c in full.train_curve_],
+                               rtol=1e-4)
+    for k in heads:
+        err = np.linalg.norm(base.params_[k] - full.params_[k]) / max(np.linalg.norm(full.params_[k]), 1e-12)
+        assert err <= (1e-3 if batch <= 16 else 1e-2), (k, err)
