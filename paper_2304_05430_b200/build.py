@@ -69,7 +69,7 @@ def build_host(force: bool = False) -> str:
     cc = os.environ.get("CC") or shutil.which("gcc") or "cc"
     import numpy
 
-    cmd = [cc, "-O3", "-shared", "-fPIC", "-Wall", "-I", sysconfig.get_paths()["include"],
+    cmd = [cc, "-O3", "-shared", "-fPIC", "-Wall", "-pthread", "-I", sysconfig.get_paths()["include"],
            "-I", numpy.get_include(), src,
            "-o", out + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)

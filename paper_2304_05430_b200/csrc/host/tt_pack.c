@@ -23,37 +23,70 @@
 #include <Python.h>
 #define NPY_NO_DEPRECATED_API NPY_2_0_API_VERSION
 #include <numpy/arrayobject.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 static PyObject *s_steps, *s_context;
 
 static int float_type(int t) { return t == NPY_DOUBLE || t == NPY_FLOAT; }
 
-/* copy a (rows, cols) strided float array into dense out of type out_t */
-static void copy2d(PyArrayObject *a, npy_intp rows, npy_intp cols, char *out, int out_t) {
-  const int in_t = PyArray_TYPE(a);
-  const npy_intp isz = in_t == NPY_DOUBLE ? 8 : 4;
-  const npy_intp *st = PyArray_STRIDES(a);
-  const npy_intp rs = PyArray_NDIM(a) > 1 ? st[0] : 0;
-  const npy_intp cs = PyArray_NDIM(a) > 1 ? st[1] : st[0];
-  const char *src = (const char *)PyArray_DATA(a);
-  if (in_t == out_t && cs == isz && (rows == 1 || rs == cols * isz)) {
-    memcpy(out, src, (size_t)(rows * cols * isz));
+/* one strided float source block (rows x cols) */
+typedef struct {
+  const char *src;
+  npy_intp rs, cs;
+  int in_t;
+} Src;
+
+/* copy a (rows, cols) strided float block into dense out of type out_t */
+static void copy2d(const Src *a, npy_intp rows, npy_intp cols, char *out, int out_t) {
+  const npy_intp isz = a->in_t == NPY_DOUBLE ? 8 : 4;
+  const npy_intp n = rows * cols;
+  if (a->cs == isz && (rows == 1 || a->rs == cols * isz)) {  /* contiguous source */
+    if (a->in_t == out_t) {
+      memcpy(out, a->src, (size_t)(n * isz));
+    } else if (out_t == NPY_FLOAT) {
+      const double *in = (const double *)a->src;
+      float *o = (float *)out;
+      for (npy_intp i = 0; i < n; ++i) o[i] = (float)in[i];
+    } else {
+      const float *in = (const float *)a->src;
+      double *o = (double *)out;
+      for (npy_intp i = 0; i < n; ++i) o[i] = (double)in[i];
+    }
     return;
   }
   for (npy_intp r = 0; r < rows; ++r) {
-    const char *row = src + r * rs;
+    const char *row = a->src + r * a->rs;
     for (npy_intp c = 0; c < cols; ++c) {
-      const char *e = row + c * cs;
-      const double v = in_t == NPY_DOUBLE ? *(const double *)e : (double)*(const float *)e;
+      const char *e = row + c * a->cs;
+      const double v = a->in_t == NPY_DOUBLE ? *(const double *)e : (double)*(const float *)e;
       if (out_t == NPY_DOUBLE)
         ((double *)out)[r * cols + c] = v;
       else
         ((float *)out)[r * cols + c] = (float)v;
     }
   }
+}
+
+typedef struct {
+  const Src *st, *cx;
+  const int64_t *L, *roff; /* step counts, first output row of each item */
+  Py_ssize_t i0, i1;
+  npy_intp d0, C, ss, sc;
+  char *ps, *pc;
+  int ts, tc;
+} Job;
+
+static void *run_job(void *arg) {
+  const Job *j = (const Job *)arg;
+  for (Py_ssize_t i = j->i0; i < j->i1; ++i) {
+    copy2d(&j->st[i], (npy_intp)j->L[i], j->d0, j->ps + (npy_intp)j->roff[i] * j->d0 * j->ss, j->ts);
+    copy2d(&j->cx[i], 1, j->C, j->pc + (npy_intp)i * j->C * j->sc, j->tc);
+  }
+  return NULL;
 }
 
 static void release(PyObject **held, Py_ssize_t n) {
@@ -127,17 +160,61 @@ static PyObject *pack(PyObject *self, PyObject *args) {
         out_ok(PyTuple_GET_ITEM(bufs, 0), rows * d0) && out_ok(PyTuple_GET_ITEM(bufs, 1), n * C)) {
       PyArrayObject *os = (PyArrayObject *)PyTuple_GET_ITEM(bufs, 0);
       PyArrayObject *oc = (PyArrayObject *)PyTuple_GET_ITEM(bufs, 1);
-      const int ts = PyArray_TYPE(os), tc = PyArray_TYPE(oc);
-      const npy_intp ss = ts == NPY_DOUBLE ? 8 : 4, sc = tc == NPY_DOUBLE ? 8 : 4;
-      char *ps = (char *)PyArray_DATA(os), *pc = (char *)PyArray_DATA(oc);
-      for (Py_ssize_t j = 0; j < n; ++j) {
-        const npy_intp T = (npy_intp)L[j];
-        copy2d((PyArrayObject *)held[2 * j], T, d0, ps, ts);
-        ps += T * d0 * ss;
-        copy2d((PyArrayObject *)held[2 * j + 1], 1, C, pc, tc);
-        pc += C * sc;
+      Src *src = (Src *)malloc((size_t)(2 * n) * sizeof(Src));
+      int64_t *roff = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+      if (!src || !roff) {
+        free(src);
+        free(roff);
+        PyErr_NoMemory();
+      } else {
+        /* gather the source descriptors under the GIL, copy without it */
+        int64_t acc = 0;
+        for (Py_ssize_t j = 0; j < n; ++j) {
+          PyArrayObject *sa = (PyArrayObject *)held[2 * j], *ca = (PyArrayObject *)held[2 * j + 1];
+          src[j] = (Src){(const char *)PyArray_DATA(sa), PyArray_STRIDE(sa, 0), PyArray_STRIDE(sa, 1),
+                         PyArray_TYPE(sa)};
+          src[n + j] = (Src){(const char *)PyArray_DATA(ca), 0, PyArray_STRIDE(ca, 0), PyArray_TYPE(ca)};
+          roff[j] = acc;
+          acc += L[j];
+        }
+        Job base;
+        base.st = src;
+        base.cx = src + n;
+        base.L = L;
+        base.roff = roff;
+        base.d0 = d0;
+        base.C = C;
+        base.ts = PyArray_TYPE(os);
+        base.tc = PyArray_TYPE(oc);
+        base.ss = base.ts == NPY_DOUBLE ? 8 : 4;
+        base.sc = base.tc == NPY_DOUBLE ? 8 : 4;
+        base.ps = (char *)PyArray_DATA(os);
+        base.pc = (char *)PyArray_DATA(oc);
+        long ncpu = sysconf(_SC_NPROCESSORS_ONLN);
+        int nth = (int)(ncpu < 1 ? 1 : ncpu > 8 ? 8 : ncpu);
+        if (n < 4096) nth = 1;
+        Job jobs[8];
+        pthread_t tids[8];
+        int started[8] = {0};
+        Py_BEGIN_ALLOW_THREADS
+        for (int t = 0; t < nth; ++t) {
+          jobs[t] = base;
+          jobs[t].i0 = n * t / nth;
+          jobs[t].i1 = n * (t + 1) / nth;
+          if (t > 0) started[t] = pthread_create(&tids[t], NULL, run_job, &jobs[t]) == 0;
+        }
+        run_job(&jobs[0]);
+        for (int t = 1; t < nth; ++t) {
+          if (started[t])
+            pthread_join(tids[t], NULL);
+          else
+            run_job(&jobs[t]);
+        }
+        Py_END_ALLOW_THREADS
+        free(src);
+        free(roff);
+        ok = 1;
       }
-      ok = 1;
     } else {
       PyErr_SetString(PyExc_ValueError,
                       "alloc() must return two writable C-contiguous float32/float64 arrays of "
