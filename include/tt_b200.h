@@ -181,6 +181,41 @@ int tt_tuner_train_heads_f32(float *d_params, float *d_m, float *d_v, const floa
                              float *d_step_loss, int32_t *d_status, void *d_ws, size_t ws_bytes,
                              tt_stream_t stream);
 
+/* Data-parallel training fused into the training kernel (SURVEY §8e,
+ * option A: the reference's rank loss within each rank's microbatch, the
+ * step's gradient = the mean of the world's microbatch gradients, replicated
+ * Adam).  One launch per epoch per rank, each on its own data shard (equal
+ * shard sizes).  Every gradient job stores its reduced slice into the
+ * peers' exchange buffers (NVLink peer memory, opened with tt_ipc_open),
+ * raises a release flag there, waits for the peers' flags and sums the
+ * slots in rank order -- no separate all-reduce or Adam launch.
+ *   tt_tuner_dp_buffer_bytes: size of one rank's exchange buffer.
+ *   d_xb: device array [world] of the exchange buffer base pointers (own
+ *     included, index = rank); buffers zeroed once (tt_ipc_alloc does).
+ *   gbase: global index of this launch's first step, monotone across
+ *     launches (flags carry gbase + step + 1).
+ * A non-finite loss sets *d_status on the rank where it happened, but every
+ * rank runs the epoch to its end (the host combines the statuses).
+ * tt_ipc_alloc/open/close, tt_dev_free: the cudaIpc* plumbing (64-B handles).
+ * tt_tuner_train_set_grid: CTAs of the latency-path launch (0 = every SM);
+ * tests run several ranks concurrently on one GPU by splitting its SMs. */
+size_t tt_tuner_dp_buffer_bytes(int32_t layers, int32_t hidden, int32_t step_width, int32_t ctx_len,
+                                int32_t world);
+int tt_tuner_train_dp_f32(float *d_params, float *d_m, float *d_v, const float *d_steps,
+                          const int64_t *d_row_offsets, const float *d_ctx, const float *d_y,
+                          const int32_t *d_order, int64_t n_order, int32_t batch_size,
+                          int32_t loss_kind, double lr, double b1, double b2, double eps,
+                          const double *d_corr, const uint8_t *d_trainable, int32_t layers,
+                          int32_t hidden, int32_t heads, int32_t unroll, int32_t step_width,
+                          int32_t ctx_len, int32_t max_steps, int32_t world, int32_t rank,
+                          int64_t gbase, float *const *d_xb, float *d_step_loss, int32_t *d_status,
+                          void *d_ws, size_t ws_bytes, tt_stream_t stream);
+int tt_ipc_alloc(size_t bytes, void **d_ptr, uint8_t *h_handle);
+int tt_ipc_open(const uint8_t *h_handle, void **d_ptr);
+int tt_ipc_close(void *d_ptr);
+int tt_dev_free(void *d_ptr);
+int tt_tuner_train_set_grid(int32_t grid);
+
 /* Kernel selection for tt_tuner_train_f32: 0 = automatic (the latency-path
  * kernel when hidden = 32, batch <= #SMs and the per-sample caches fit in
  * shared memory, else the generic kernel), 1 = generic only, 2 = latency path

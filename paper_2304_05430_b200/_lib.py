@@ -43,6 +43,14 @@ SIGNATURES: dict[str, tuple] = {
     "tt_tuner_lstm_outputs_f32": (ctypes.c_int, [_P, _P, _P, _P, _I64] + [_I32] * 7 + [_P, _P, _P, _SZ, _P]),
     "tt_tuner_train_heads_f32": (ctypes.c_int, [_P] * 7 + [_P, _I64, _I32, _I32, _D, _D, _D, _D, _P, _P]
                                  + [_I32] * 7 + [_P, _P, _P, _P, _SZ, _P]),
+    "tt_tuner_dp_buffer_bytes": (_SZ, [_I32] * 5),
+    "tt_tuner_train_dp_f32": (ctypes.c_int, [_P] * 7 + [_P, _I64, _I32, _I32, _D, _D, _D, _D, _P, _P]
+                              + [_I32] * 7 + [_I32, _I32, _I64, _P] + [_P, _P, _P, _SZ, _P]),
+    "tt_ipc_alloc": (ctypes.c_int, [_SZ, _P, _P]),
+    "tt_ipc_open": (ctypes.c_int, [_P, _P]),
+    "tt_ipc_close": (ctypes.c_int, [_P]),
+    "tt_dev_free": (ctypes.c_int, [_P]),
+    "tt_tuner_train_set_grid": (ctypes.c_int, [_I32]),
     "tt_tuner_train_set_path": (ctypes.c_int, [_I32]),
     "tt_debug_profile_step": (ctypes.c_int, [_I32]),
     "tt_debug_phase_times": (ctypes.c_int, [_P, _I32]),

@@ -1,6 +1,7 @@
 // Attention tuner kernels: bulk scoring (K5) and the fused training step
 // (K5 cached forward + K7 loss + K6 backward + deterministic reduction + K8
 // Adam) -- see tt_tuner.cuh / tt_tuner_train.cuh for the per-block code.
+#include <cstring>
 #include <type_traits>
 
 #include "tt_tuner_fast.cuh"
@@ -320,6 +321,12 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
 }
 
 // ------------------------------------------------------------- dispatch --
+struct DpArgs {
+  int world, rank;
+  int64_t gbase;
+  float* const* xb;
+};
+
 template <typename R>
 struct Launch {
   template <int H>
@@ -419,11 +426,11 @@ struct Launch {
   }
 
   static int train(TrainArgs<R> a, void* ws, size_t ws_bytes, cudaStream_t st,
-                   const R* scache = nullptr) {
+                   const R* scache = nullptr, const DpArgs* dp = nullptr) {
     if constexpr (std::is_same<R, float>::value) {
       // v4 latency path (tt_tuner_fast.cuh) when eligible, else the generic kernel
       FastPlan fp;
-      const bool ok = g_train_path != 1 && fast_plan(a.dm, a.B, sm_count(), fp) &&
+      const bool ok = g_train_path != 1 && fast_plan(a.dm, a.B, fast_grid(), fp) &&
                       ws_bytes >= fast_ws_bytes(a.dm, a.B);
       if (ok) {
         FastArgs f{};
@@ -448,8 +455,16 @@ struct Launch {
         f.grad_out = a.grad_out;
         f.status = a.status;
         f.s_frozen = scache;
+        f.world = 1;
+        if (dp) {
+          f.world = dp->world;
+          f.rank = dp->rank;
+          f.gbase = dp->gbase;
+          f.xb = dp->xb;
+        }
         return fast_launch(f, fp, ws, st);
       }
+      TT_REQUIRE(dp == nullptr, "tuner train (data parallel): not eligible for the latency-path kernel");
       TT_REQUIRE(g_train_path != 2, "tuner train: fast path requested but not eligible");
       TT_REQUIRE(scache == nullptr, "tuner train (heads only): not eligible for the latency-path kernel");
     }
@@ -494,7 +509,7 @@ static int train_entry(R* prm, R* m, R* v, const R* steps, const int64_t* rowoff
                        double eps, const double* corr, const uint8_t* trainable, int32_t L,
                        int32_t H, int32_t heads, int32_t U, int32_t d0, int32_t C, int32_t Tmax,
                        R* step_loss, R* grad_out, int32_t* status, void* ws, size_t ws_bytes,
-                       tt_stream_t st, const R* scache = nullptr) {
+                       tt_stream_t st, const R* scache = nullptr, const DpArgs* dp = nullptr) {
   if (int rc = check_dims(L, H, heads, U, d0, C, Tmax)) return rc;
   TT_REQUIRE(B >= 1 && B <= 4096, "tuner train: batch size must be in [1, 4096]");
   TT_REQUIRE(n_order >= 1, "tuner train: empty order");
@@ -525,7 +540,7 @@ static int train_entry(R* prm, R* m, R* v, const R* steps, const int64_t* rowoff
   a.step_loss = step_loss;
   a.grad_out = grad_out;
   a.status = status;
-  return Launch<R>::train(a, ws, ws_bytes, as_stream(st), scache);
+  return Launch<R>::train(a, ws, ws_bytes, as_stream(st), scache, dp);
 }
 
 }  // namespace tt
@@ -607,6 +622,68 @@ int tt_tuner_train_heads_f32(float* prm, float* m, float* v, const float* steps,
   return train_entry<float>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind,
                             TT_MODE_TRAIN, lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C,
                             Tmax, step_loss, nullptr, status, ws, ws_bytes, st, s_cache);
+}
+
+size_t tt_tuner_dp_buffer_bytes(int32_t L, int32_t H, int32_t d0, int32_t C, int32_t world) {
+  if (L < 1 || L > kMaxLayers || H != kFH || world < 1) return 0;
+  const TDims dm = make_dims(L, H, 1, 1, d0, C, 1);
+  const int kap_max = std::max(round4(round4(std::max(d0, kFD)) + kFH + 1), round4(round4(kFD + C) + 1));
+  return (size_t)fast_dp_buffer_floats(fast_n_jobs(dm), world, (int64_t)kap_max * 16) * sizeof(float);
+}
+
+int tt_tuner_train_dp_f32(float* prm, float* m, float* v, const float* steps, const int64_t* rowoff,
+                          const float* ctx, const float* y, const int32_t* order, int64_t n_order,
+                          int32_t B, int32_t loss_kind, double lr, double b1, double b2, double eps,
+                          const double* corr, const uint8_t* trainable, int32_t L, int32_t H,
+                          int32_t heads, int32_t U, int32_t d0, int32_t C, int32_t Tmax,
+                          int32_t world, int32_t rank, int64_t gbase, float* const* d_xb,
+                          float* step_loss, int32_t* status, void* ws, size_t ws_bytes,
+                          tt_stream_t st) {
+  TT_REQUIRE(world >= 1 && rank >= 0 && rank < world, "tuner train (dp): bad world/rank");
+  TT_REQUIRE(world == 1 || d_xb != nullptr, "tuner train (dp): exchange buffers required");
+  TT_REQUIRE(gbase >= 0, "tuner train (dp): bad step base");
+  DpArgs dp{world, rank, gbase, d_xb};
+  return train_entry<float>(prm, m, v, steps, rowoff, ctx, y, order, n_order, B, loss_kind,
+                            TT_MODE_TRAIN, lr, b1, b2, eps, corr, trainable, L, H, heads, U, d0, C,
+                            Tmax, step_loss, nullptr, status, ws, ws_bytes, st, nullptr,
+                            world > 1 ? &dp : nullptr);
+}
+
+int tt_ipc_alloc(size_t bytes, void** d_ptr, uint8_t* h_handle) {
+  TT_REQUIRE(d_ptr != nullptr && h_handle != nullptr && bytes > 0, "ipc alloc: bad arguments");
+  void* p = nullptr;
+  TT_CUDA(cudaMalloc(&p, bytes));
+  TT_CUDA(cudaMemset(p, 0, bytes));
+  cudaIpcMemHandle_t h;
+  TT_CUDA(cudaIpcGetMemHandle(&h, p));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  memcpy(h_handle, &h, sizeof(h));
+  *d_ptr = p;
+  return TT_OK;
+}
+
+int tt_ipc_open(const uint8_t* h_handle, void** d_ptr) {
+  TT_REQUIRE(d_ptr != nullptr && h_handle != nullptr, "ipc open: bad arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, h_handle, sizeof(h));
+  TT_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return TT_OK;
+}
+
+int tt_ipc_close(void* d_ptr) {
+  TT_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return TT_OK;
+}
+
+int tt_dev_free(void* d_ptr) {
+  TT_CUDA(cudaFree(d_ptr));
+  return TT_OK;
+}
+
+int tt_tuner_train_set_grid(int32_t grid) {
+  TT_REQUIRE(grid >= 0, "grid must be >= 0");
+  g_fast_grid = grid;
+  return TT_OK;
 }
 
 int tt_tuner_train_set_path(int32_t path) {

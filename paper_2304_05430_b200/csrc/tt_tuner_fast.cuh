@@ -259,6 +259,13 @@ struct FastArgs {
   float* yhat_buf;     // [B]
   float* lossp;        // [B][2]: per-slot pair-loss partials (multi-round mode)
   const float* s_frozen;  // heads-only mode: frozen last-layer LSTM outputs [sum T][64] (else null)
+  // data parallel (world > 1): every rank runs this kernel on its own shard;
+  // each gradient job exchanges its slice with the peers through their
+  // exchange buffers (xb[p], NVLink peer memory) before the Adam update
+  int world, rank;
+  int64_t gbase;        // global step index of this launch's first minibatch (monotone flags)
+  int64_t dp_slice;     // floats per slice slot (>= kap * nbp of every job)
+  float* const* xb;     // [world] exchange buffers (fast_dp_layout)
   float* scache;       // [B][sl.red - sl.x0]: per-slot forward caches (multi-round mode)
   float* wcache;       // [grid][attn_floats]: attention/head weight image per CTA (multi-round)
   unsigned int* ctr;   // [0] fwd, [1 + g] bwd, [2 + L + g] adam, [kCtrLoss] loss (monotone)
@@ -318,6 +325,14 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // All threads; thread 0 spins until *ctr >= target.
@@ -1296,6 +1311,57 @@ __device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGe
   __syncthreads();
 }
 
+// Data-parallel exchange buffer of one rank (allocated by the host, shared
+// with the peers by IPC): n_jobs x world monotone u32 flags (padded to 64
+// words), then the receive slots [parity][job][source rank][slice].
+__host__ __device__ inline int64_t fast_dp_flag_words(int n_jobs, int world) {
+  return ((int64_t)n_jobs * world + 63) / 64 * 64;
+}
+__host__ __device__ inline int64_t fast_dp_buffer_floats(int n_jobs, int world, int64_t slice) {
+  return fast_dp_flag_words(n_jobs, world) + 2 * (int64_t)n_jobs * world * slice;
+}
+
+// The job's reduced slice gout[n] (this rank's microbatch) -> the mean over
+// the world's microbatches (SURVEY §8e option A: pairs stay inside each
+// rank's microbatch), identical on every rank: the slice is stored into every
+// peer's receive slot, one release flag per (job, source) is raised on the
+// peer, and after the peers' flags arrive the slots are summed in rank order.
+// Receive slots alternate by step parity: a rank can only reach the next use
+// of a parity after every peer has finished reading it (it needs their slices
+// of the step in between).
+__device__ void fast_dp_exchange(const FastArgs& a, int j, int step, float* gout, int n) {
+  const int tid = threadIdx.x, W = a.world, me = a.rank;
+  const int64_t gs = a.gbase + step;
+  const unsigned want = (unsigned)(gs + 1);
+  const int64_t fw = fast_dp_flag_words(a.n_jobs, W);
+  const int64_t base = fw + ((gs & 1) * (int64_t)a.n_jobs + j) * W * a.dp_slice;
+  for (int i = tid; i < n; i += kThreads) {
+    const float v = gout[i];
+    for (int p = 0; p < W; ++p)
+      if (p != me) a.xb[p][base + (int64_t)me * a.dp_slice + i] = v;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence_system();
+    for (int p = 0; p < W; ++p)
+      if (p != me) st_release_sys(reinterpret_cast<unsigned*>(a.xb[p]) + (int64_t)j * W + me, want);
+    const unsigned* mine = reinterpret_cast<const unsigned*>(a.xb[me]) + (int64_t)j * W;
+    for (int p = 0; p < W; ++p)
+      if (p != me)
+        while (ld_acquire_sys(mine + p) < want) {
+        }
+  }
+  __syncthreads();
+  const float* rx = a.xb[me] + base;
+  const float inv = 1.f / (float)W;
+  for (int i = tid; i < n; i += kThreads) {
+    float acc = 0.f;
+    for (int p = 0; p < W; ++p) acc += p == me ? gout[i] : __ldcg(rx + (int64_t)p * a.dp_slice + i);
+    gout[i] = acc * inv;
+  }
+  __syncthreads();
+}
+
 // R: stacked step rows of the minibatch; bn: samples.
 // keep: this CTA owns the slice for the whole launch (not a sampler), so the
 // parameters, Adam moments and trainable mask of the slice stay in shared
@@ -1308,8 +1374,8 @@ __device__ __forceinline__ int64_t job_rows(const TDims& dm, const FastJob& jb, 
 }
 
 // a_staged: the A operand of all rows was staged by the caller (single chunk).
-__device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64_t R, int step,
-                             float* sm, bool keep, bool a_staged) {
+__device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int jidx, int bn, int64_t R,
+                             int step, float* sm, bool keep, bool a_staged) {
   const TDims& dm = a.dm;
   const int tid = threadIdx.x;
   const JobGeo geo = job_geo(dm, jb);
@@ -1363,6 +1429,7 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int bn, int64
   }
   __syncthreads();
   if (blockIdx.x == (unsigned)(a.B % gridDim.x)) fmark_any(step, 23);
+  if (a.world > 1 && a.mode == TT_MODE_TRAIN) fast_dp_exchange(a, jidx, step, gout, kap * nbp);
   // parameter addresses of the slice and the fused Adam update
   const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
   const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
@@ -1710,10 +1777,12 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
                    : mse_block<float>(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red);
       }
       if (tid == 0) {
-        s_stop = !isfinite(loss);
+        // data parallel: a non-finite loss is recorded but the rank keeps
+        // stepping (its peers wait for its slices); the host raises afterwards
+        s_stop = !isfinite(loss) && a.world <= 1;
         if (r == 0) {
           a.step_loss[step] = loss;
-          if (s_stop) a.status[0] = step;
+          if (!isfinite(loss) && __ldcg(a.status) < 0) a.status[0] = step;
         }
       }
       __syncthreads();
@@ -1765,10 +1834,10 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
       if (a.s_frozen && g < dm.L) continue;  // heads-only: recurrent slices are frozen
       wait_counter(a.ctr + ctr_bwd(g), cum, !sampler);
       if (r == a.B % G) fmark_any(step, 20);
-      if (tid == 0) s_stop = __ldcg(a.status) >= 0;
+      if (tid == 0) s_stop = a.world <= 1 && __ldcg(a.status) >= 0;
       __syncthreads();
       if (s_stop) break;
-      fast_run_job(a, fast_job(dm, j), bn, s_R, step, sm, keep, a_staged);
+      fast_run_job(a, fast_job(dm, j), j, bn, s_R, step, sm, keep, a_staged);
       signal_counter(a.ctr + ctr_adam(dm, g), 1);
       if (r == a.B % G) fmark_any(step, 21);
     }
@@ -1777,6 +1846,11 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
 }
 
 // --------------------------------------------------------- host side --
+// CTAs of the latency-path launch: every SM, unless a test splits the GPU
+// between concurrently running "ranks" (tt_tuner_train_set_grid)
+static int g_fast_grid = 0;
+inline int fast_grid() { return g_fast_grid > 0 ? std::min(g_fast_grid, sm_count()) : sm_count(); }
+
 struct FastPlan {
   FastSmem sl;
   FastXch xl;
@@ -1784,16 +1858,17 @@ struct FastPlan {
   int64_t rch, pc_off;
   int pc_n, l0_smem;
   int n_jobs;
+  int64_t dp_slice;  // floats per data-parallel slice slot
 };
 
 inline size_t fast_ws_bytes(const TDims& dm, int B) {
   const FastXch xl = make_fast_xch(dm, B);
   size_t b = align_up((size_t)xl.total * sizeof(float), 256) + align_up((size_t)B * 8, 256) +
              align_up((size_t)B * sizeof(float), 256) + align_up((size_t)B * 2 * sizeof(float), 256) + 256;
-  if (B > sm_count()) {  // multi-round: per-slot forward caches + per-CTA weight images
+  if (B > fast_grid()) {  // multi-round: per-slot forward caches + per-CTA weight images
     const FastSmem sl = make_fast_smem(dm, B);
     b += align_up((size_t)B * (sl.red - sl.x0) * sizeof(float), 256) +
-         align_up((size_t)sm_count() * fast_attn_floats(dm) * sizeof(float), 256);
+         align_up((size_t)fast_grid() * fast_attn_floats(dm) * sizeof(float), 256);
   }
   return b;
 }
@@ -1834,6 +1909,7 @@ inline bool fast_plan(const TDims& dm, int B, int grid, FastPlan& p) {
   p.pc_n = kap_max * nbp;
   p.l0_smem = (int64_t)2 * (dm.d0 + kFH + 1) * kFG <= p.sl.total - p.sl.W ? 1 : 0;
   p.pc_off = (int64_t)(need / sizeof(float)) - 4 * (int64_t)p.pc_n;
+  p.dp_slice = (int64_t)kap_max * nbp;
   return true;
 }
 
@@ -1842,6 +1918,7 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   a.sl = p.sl;
   a.xl = p.xl;
   a.n_jobs = p.n_jobs;
+  a.dp_slice = p.dp_slice;
   a.rch = p.rch;
   a.pc_off = p.pc_off;
   a.l0_smem = p.l0_smem;
@@ -1855,11 +1932,11 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   a.lossp = reinterpret_cast<float*>(w);
   w += align_up((size_t)a.B * 2 * sizeof(float), 256);
   a.scache = a.wcache = nullptr;
-  if (a.B > sm_count()) {
+  if (a.B > fast_grid()) {
     a.scache = reinterpret_cast<float*>(w);
     w += align_up((size_t)a.B * (p.sl.red - p.sl.x0) * sizeof(float), 256);
     a.wcache = reinterpret_cast<float*>(w);
-    w += align_up((size_t)sm_count() * fast_attn_floats(a.dm) * sizeof(float), 256);
+    w += align_up((size_t)fast_grid() * fast_attn_floats(a.dm) * sizeof(float), 256);
   }
   a.ctr = reinterpret_cast<unsigned int*>(w);
   TT_CUDA(cudaMemsetAsync(a.ctr, 0, 256, st));
@@ -1868,7 +1945,7 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   int per_sm = 0;
   TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, p.smem));
   TT_REQUIRE(per_sm >= 1, "tuner train (fast): kernel cannot be resident (smem %zu)", p.smem);
-  const int grid = sm_count();
+  const int grid = fast_grid();
   void* args[] = {&a};
   TT_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, kThreads, args, p.smem, st));
   return check_launch("tuner train (fast)");

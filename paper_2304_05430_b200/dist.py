@@ -9,7 +9,11 @@
   perm[k*W*B : (k+1)*W*B]; rank r takes its B-slice as the reference's
   minibatch (pairs of the rank loss stay inside it, SURVEY §8e option A) and
   the step gradient is the mean of the non-empty microbatch gradients,
-  formed by one all-reduce before the (replicated) fused Adam update.
+  formed by one all-reduce before the (replicated) fused Adam update
+  (DataParallelTunerEpoch, any kernel), or -- the B200 path --
+  FusedDataParallelTuner: one training launch per epoch per rank whose
+  gradient jobs exchange their slices with the peers through NVLink peer
+  memory (tt_tuner_train_dp_f32), no separate collective or Adam launch.
 """
 
 from __future__ import annotations
@@ -143,3 +147,133 @@ def gather_counts(local_counts: dict, n_tasks: int, group=None) -> np.ndarray:
         buf = buf.cuda()
     dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
     return buf.cpu().numpy()
+
+
+class FusedDataParallelTuner:
+    """One rank of the fused data-parallel epoch (tt_tuner_train_dp_f32).
+
+    Every rank holds an equal-size shard; global step k uses each rank's k-th
+    local microbatch (SURVEY §8e option A).  Inside the one training launch
+    per epoch, each gradient job of the latency-path kernel stores its
+    reduced parameter slice into the peers' exchange buffers (opened by CUDA
+    IPC: NVLink peer memory on the box), raises a release flag there, waits
+    for the peers' flags and sums the slots in rank order -- the update is
+    bit-identical on every rank.  ``create`` wires the buffers over
+    torch.distributed; ``local_group`` builds W ranks inside one process on
+    one GPU (tests: the ranks run concurrently on disjoint SMs).
+    """
+
+    def __init__(self, est, prog, y_dev, batch: int, world: int, rank: int, xb, owned):
+        import torch
+
+        from . import _device
+
+        self.est, self.prog, self.y, self.B = est, prog, y_dev, batch
+        self.world, self.rank = world, rank
+        self.dims = est._dims()
+        self.flat = est._dev_params(self.dims).clone()
+        self.m = torch.zeros_like(self.flat)
+        self.v = torch.zeros_like(self.flat)
+        self.xb = xb          # device int64 tensor [world] of buffer addresses
+        self._owned = owned   # (pointer, is_ipc_mapping) to release
+        self.gstep = 0
+        self._dev = _device
+
+    @staticmethod
+    def _buffer_bytes(dims, world: int) -> int:
+        from . import _lib
+
+        n = _lib.load().tt_tuner_dp_buffer_bytes(dims["L"], dims["H"], dims["d0"], dims["C"], world)
+        if n == 0:
+            raise _lib.LibraryError("fused data parallel training needs hidden 32")
+        return int(n)
+
+    @staticmethod
+    def _alloc(nbytes: int):
+        import ctypes
+
+        from . import _lib
+
+        ptr = ctypes.c_void_p()
+        handle = (ctypes.c_uint8 * 64)()
+        _lib.call("tt_ipc_alloc", nbytes, ctypes.byref(ptr), handle)
+        return int(ptr.value), bytes(handle)
+
+    @classmethod
+    def create(cls, est, prog, y_dev, batch: int, group=None):
+        """Collective over torch.distributed: allocate this rank's exchange
+        buffer, all-gather the IPC handles, open the peers' buffers."""
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import _device, _lib
+
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        own, handle = cls._alloc(cls._buffer_bytes(est._dims(), world))
+        handles = [None] * world
+        dist.all_gather_object(handles, handle, group=group)
+        ptrs, owned = [], [(own, False)]
+        for r, h in enumerate(handles):
+            if r == rank:
+                ptrs.append(own)
+                continue
+            p = ctypes.c_void_p()
+            _lib.call("tt_ipc_open", (ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p))
+            ptrs.append(int(p.value))
+            owned.append((int(p.value), True))
+        xb = torch.tensor(ptrs, dtype=torch.int64, device=_device.device())
+        dist.barrier(group=group)
+        return cls(est, prog, y_dev, batch, world, rank, xb, owned)
+
+    @classmethod
+    def local_group(cls, ests, progs, ys, batch: int):
+        """W ranks in this process on one GPU (plain device buffers)."""
+        import torch
+
+        from . import _device
+
+        world = len(ests)
+        nbytes = cls._buffer_bytes(ests[0]._dims(), world)
+        bufs = [cls._alloc(nbytes)[0] for _ in range(world)]
+        xb = torch.tensor(bufs, dtype=torch.int64, device=_device.device())
+        return [cls(e, p, y, batch, world, r, xb, [(bufs[r], False)])
+                for r, (e, p, y) in enumerate(zip(ests, progs, ys))]
+
+    def run(self, perm: np.ndarray, lr: float):
+        """Enqueue one epoch over this rank's shard in the order `perm` (equal
+        length on every rank) on the current stream; returns the device
+        status (>= 0: first non-finite step on this rank)."""
+        from . import _lib
+        from .estimators import _BETA1, _BETA2, _EPS, _bias_corrections
+
+        d, est, prog = self.dims, self.est, self.prog
+        n = len(perm)
+        n_steps = (n + self.B - 1) // self.B
+        lib = _lib.load()
+        nbytes = lib.tt_tuner_train_workspace_bytes(0, d["L"], d["H"], d["d0"], d["C"], prog.max_steps,
+                                                    self.B)
+        ws = self._dev.workspace(nbytes, "tuner_train_dp")
+        order = self._dev.to_dev(np.asarray(perm, dtype=np.int32))
+        corr = self._dev.to_dev(_bias_corrections(self.gstep, n_steps))
+        self.step_loss = self._dev.empty(n_steps, self.flat.dtype)
+        status = self._dev.to_dev(np.array([-1], dtype=np.int32))
+        loss_kind = _lib.TT_LOSS_RANK if est.loss == "ranking" else _lib.TT_LOSS_MSE
+        _lib.call("tt_tuner_train_dp_f32", self.flat.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                  prog.steps.data_ptr(), prog.offsets.data_ptr(), prog.ctx.data_ptr(), self.y.data_ptr(),
+                  order.data_ptr(), n, self.B, loss_kind, float(lr), _BETA1, _BETA2, _EPS,
+                  corr.data_ptr(), None, d["L"], d["H"], d["heads"], d["U"], d["d0"], d["C"],
+                  prog.max_steps, self.world, self.rank, self.gstep, self.xb.data_ptr(),
+                  self.step_loss.data_ptr(), status.data_ptr(), ws.data_ptr(), nbytes,
+                  self._dev.stream_ptr())
+        self.gstep += n_steps
+        self._keep = (order, corr)  # alive until the launch completes
+        return status
+
+    def close(self):
+        from . import _lib
+
+        for ptr, mapped in self._owned:
+            _lib.call("tt_ipc_close" if mapped else "tt_dev_free", ptr)
+        self._owned = []

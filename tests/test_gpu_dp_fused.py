@@ -1,0 +1,87 @@
+"""Fused data-parallel training (tt_tuner_train_dp_f32, dist.FusedDataParallelTuner):
+W ranks run the training kernel concurrently -- here inside one process on one
+GPU, each rank on its own share of the SMs and its own stream, the exchange
+buffers plain device memory standing in for the peers' NVLink-mapped ones.
+
+Reference semantics (SURVEY §8e option A): step k's gradient is the mean of
+the ranks' k-th microbatch gradients (rank loss pairs inside each
+microbatch), followed by the replicated Adam step.  Checked against the
+float64 oracle, plus bit-identical parameters on every rank.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import random_seqs
+from oracle import tuner as otuner
+from oracle.adam import AdamOracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _unflatten(est, flat):
+    host = est.__dict__["_host"]
+    out, o = {}, 0
+    for k in est._dims()["names"]:
+        out[k] = flat[o:o + host[k].size].reshape(host[k].shape)
+        o += host[k].size
+    return out
+
+
+@pytest.mark.parametrize("world,batch,loss", [(2, 8, "ranking"), (3, 5, "rmse")])
+def test_fused_dp_matches_oracle(cuda_ok, world, batch, loss):
+    import torch
+
+    from paper_2304_05430_b200 import RecurrentAttentionTuner, _device, _lib
+    from paper_2304_05430_b200.dist import FusedDataParallelTuner
+    from paper_2304_05430_b200.layout import DevicePrograms
+
+    n_local = 4 * batch + 3  # a partial last microbatch on every rank
+    rng = np.random.default_rng(world)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=world * n_local))
+    y = rng.uniform(0.1, 0.9, size=world * n_local)
+    shards = [slice(r * n_local, (r + 1) * n_local) for r in range(world)]
+    ests, progs, ys = [], [], []
+    for sh in shards:
+        e = RecurrentAttentionTuner(epochs=0, seed=3, loss=loss)
+        e.precision = "fp32"
+        e.fit(seqs[sh], y[sh])
+        ests.append(e)
+        progs.append(DevicePrograms.from_sequences(seqs[sh], "fp32", 6, 35))
+        ys.append(_device.to_dev(y[sh], torch.float32))
+    ranks = FusedDataParallelTuner.local_group(ests, progs, ys, batch)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    p = otuner.init_params(3)
+    opt = AdamOracle(p, 1e-3)
+    _lib.call("tt_tuner_train_set_grid", sms // world)
+    try:
+        streams = [torch.cuda.Stream() for _ in range(world)]
+        for epoch in range(2):
+            perms = [rng.permutation(n_local) for _ in range(world)]
+            torch.cuda.synchronize()
+            stats = []
+            for r in range(world):
+                with torch.cuda.stream(streams[r]):
+                    stats.append(ranks[r].run(perms[r], 1e-3))
+            torch.cuda.synchronize()
+            assert all(int(s.item()) < 0 for s in stats)
+            for k in range(0, n_local, batch):
+                grads = []
+                for r in range(world):
+                    idx = [shards[r].start + i for i in perms[r][k:k + batch]]
+                    _, g = otuner.loss_and_gradients(p, [seqs[i] for i in idx], y[idx], loss)
+                    grads.append(g)
+                opt.step({name: sum(g[name] for g in grads) / world for name in grads[0]})
+    finally:
+        _lib.call("tt_tuner_train_set_grid", 0)
+    flats = [rk.flat.cpu().numpy() for rk in ranks]
+    for f in flats[1:]:
+        assert np.array_equal(f, flats[0])  # replicated update, identical on every rank
+    got = _unflatten(ests[0], flats[0].astype(np.float64))
+    for name in p:
+        err = np.linalg.norm(got[name] - p[name]) / max(np.linalg.norm(p[name]), 1e-12)
+        assert err <= 2e-3, (name, err)
+    for rk in ranks:
+        rk.close()
