@@ -420,15 +420,16 @@ def run_b200(args, world, rank):
     dp = None
     if world > 1:
         # data parallel: every rank holds its own 64x4096 shard (weak scaling);
-        # global step = per-rank microbatch of 16 -> NCCL gradient all-reduce
-        # -> replicated fused Adam (paper_2304_05430_b200.dist)
-        from paper_2304_05430_b200.dist import DataParallelTunerEpoch
+        # global step = the ranks' microbatches of 16 (SURVEY §8e option A),
+        # exchanged inside the one training launch per epoch over NVLink peer
+        # memory (paper_2304_05430_b200.dist.FusedDataParallelTuner)
+        from paper_2304_05430_b200.dist import FusedDataParallelTuner
 
-        dp = DataParallelTunerEpoch(est, prog, yd, BATCH)
+        dp = FusedDataParallelTuner.create(est, prog, yd, BATCH)
 
     def epoch(t0):
         if dp is not None:
-            return dp.run(rng.permutation(n), 1e-3, local_shard=True)
+            return dp.run(rng.permutation(n), 1e-3)
         perm = _device.to_dev(rng.permutation(n).astype(np.int32))
         corr = _device.to_dev(_bias_corrections(t0, n_steps))
         return est._launch_train(dims, flat, m, v, prog, yd, perm, BATCH, _lib.TT_MODE_TRAIN, 1e-3,
@@ -458,8 +459,7 @@ def run_b200(args, world, rank):
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if dp is not None:
-                dp.run(rng.permutation(n), 1e-3, local_shard=True)
-                status = None
+                status = dp.run(rng.permutation(n), 1e-3)
             else:
                 _, status, _ = est._launch_train(dims, flat, m, v, prog, yd, perms[k], BATCH,
                                                  _lib.TT_MODE_TRAIN, 1e-3, corrs[k], None)
@@ -614,8 +614,8 @@ def run_b200(args, world, rank):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # fused path: one cooperative launch per epoch; DP: grad kernel + Adam per step
-            "gpu_launches": args.steps if dp is None else 2 * n_steps * args.steps,
+            # one cooperative training launch per epoch per rank (DP included)
+            "gpu_launches": args.steps,
             "clocks": clocks.summary(int(os.environ.get("LOCAL_RANK", 0))),
             "extra": extra,
         }
