@@ -149,6 +149,17 @@ def gather_counts(local_counts: dict, n_tasks: int, group=None) -> np.ndarray:
     return buf.cpu().numpy()
 
 
+def exchange_handles(handle: bytes, group=None) -> list:
+    """All-gather one 64-byte CUDA IPC handle per rank (rank order)."""
+    import torch.distributed as dist
+
+    if len(handle) != 64:
+        raise ValueError("CUDA IPC handles are 64 bytes")
+    handles = [None] * dist.get_world_size(group)
+    dist.all_gather_object(handles, bytes(handle), group=group)
+    return handles
+
+
 class FusedDataParallelTuner:
     """One rank of the fused data-parallel epoch (tt_tuner_train_dp_f32).
 
@@ -212,8 +223,7 @@ class FusedDataParallelTuner:
 
         world, rank = dist.get_world_size(group), dist.get_rank(group)
         own, handle = cls._alloc(cls._buffer_bytes(est._dims(), world))
-        handles = [None] * world
-        dist.all_gather_object(handles, handle, group=group)
+        handles = exchange_handles(handle, group)
         ptrs, owned = [], [(own, False)]
         for r, h in enumerate(handles):
             if r == rank:

@@ -144,3 +144,39 @@ def test_sharding_helpers_partition_everything(world):
     seen = np.concatenate([tdist.dp_microbatch(perm, k, 4, r, world)
                            for k in range(tdist.dp_steps(103, 4, world)) for r in range(world)])
     assert np.array_equal(seen, perm)
+
+
+def _handles_worker(rank, world, port, out):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2304_05430_b200 import dist as tdist
+
+    _init(rank, world, port)
+    out[rank] = tdist.exchange_handles(bytes([rank]) * 64)
+    dist.destroy_process_group()
+
+
+def test_ipc_handle_exchange_is_rank_ordered():
+    """FusedDataParallelTuner.create's wiring: every rank receives every
+    rank's exchange-buffer handle, in rank order (index = peer rank)."""
+    world = 3
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_handles_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    want = [bytes([r]) * 64 for r in range(world)]
+    assert all(list(out[r]) == want for r in range(world))
+
+
+def test_dp_buffer_size_covers_every_slot():
+    """tt_tuner_dp_buffer_bytes = flags (padded) + 2 parities x jobs x world
+    x slice, slice >= the widest job slice (host-only entry point)."""
+    from paper_2304_05430_b200 import _lib
+
+    lib = _lib.load()
+    one = lib.tt_tuner_dp_buffer_bytes(3, 32, 6, 35, 1)
+    two = lib.tt_tuner_dp_buffer_bytes(3, 32, 6, 35, 2)
+    assert one > 0 and two > one
+    assert lib.tt_tuner_dp_buffer_bytes(3, 16, 6, 35, 2) == 0  # fused path is hidden-32 only
+    wide = lib.tt_tuner_dp_buffer_bytes(3, 32, 164, 35, 2)
+    assert wide > two  # wider layer-0 slices
