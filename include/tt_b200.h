@@ -186,9 +186,10 @@ int tt_tuner_train_heads_f32(float *d_params, float *d_m, float *d_v, const floa
  * step's gradient = the mean of the world's microbatch gradients, replicated
  * Adam).  One launch per epoch per rank, each on its own data shard (equal
  * shard sizes).  Every gradient job stores its reduced slice into the
- * peers' exchange buffers (NVLink peer memory, opened with tt_ipc_open),
- * raises a release flag there, waits for the peers' flags and sums the
- * slots in rank order -- no separate all-reduce or Adam launch.
+ * peers' exchange buffers (NVLink peer memory, opened with tt_ipc_open) as
+ * 8-byte {value, step flag} words, spins on its own slots until the peers'
+ * words carry the step's flag and sums them in rank order -- no fences, no
+ * separate all-reduce or Adam launch.
  *   tt_tuner_dp_buffer_bytes: size of one rank's exchange buffer.
  *   d_xb: device array [world] of the exchange buffer base pointers (own
  *     included, index = rank); buffers zeroed once (tt_ipc_alloc does).
@@ -208,7 +209,7 @@ int tt_tuner_train_dp_f32(float *d_params, float *d_m, float *d_v, const float *
                           const double *d_corr, const uint8_t *d_trainable, int32_t layers,
                           int32_t hidden, int32_t heads, int32_t unroll, int32_t step_width,
                           int32_t ctx_len, int32_t max_steps, int32_t world, int32_t rank,
-                          int64_t gbase, float *const *d_xb, float *d_step_loss, int32_t *d_status,
+                          int64_t gbase, void *const *d_xb, float *d_step_loss, int32_t *d_status,
                           void *d_ws, size_t ws_bytes, tt_stream_t stream);
 int tt_ipc_alloc(size_t bytes, void **d_ptr, uint8_t *h_handle);
 int tt_ipc_open(const uint8_t *h_handle, void **d_ptr);

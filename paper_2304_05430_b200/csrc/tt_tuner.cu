@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
 struct DpArgs {
   int world, rank;
   int64_t gbase;
-  float* const* xb;
+  void* const* xb;
 };
 
 template <typename R>
@@ -628,7 +628,7 @@ size_t tt_tuner_dp_buffer_bytes(int32_t L, int32_t H, int32_t d0, int32_t C, int
   if (L < 1 || L > kMaxLayers || H != kFH || world < 1) return 0;
   const TDims dm = make_dims(L, H, 1, 1, d0, C, 1);
   const int kap_max = std::max(round4(round4(std::max(d0, kFD)) + kFH + 1), round4(round4(kFD + C) + 1));
-  return (size_t)fast_dp_buffer_floats(fast_n_jobs(dm), world, (int64_t)kap_max * 16) * sizeof(float);
+  return (size_t)fast_dp_buffer_bytes(fast_n_jobs(dm), world, (int64_t)kap_max * 16);
 }
 
 int tt_tuner_train_dp_f32(float* prm, float* m, float* v, const float* steps, const int64_t* rowoff,
@@ -636,7 +636,7 @@ int tt_tuner_train_dp_f32(float* prm, float* m, float* v, const float* steps, co
                           int32_t B, int32_t loss_kind, double lr, double b1, double b2, double eps,
                           const double* corr, const uint8_t* trainable, int32_t L, int32_t H,
                           int32_t heads, int32_t U, int32_t d0, int32_t C, int32_t Tmax,
-                          int32_t world, int32_t rank, int64_t gbase, float* const* d_xb,
+                          int32_t world, int32_t rank, int64_t gbase, void* const* d_xb,
                           float* step_loss, int32_t* status, void* ws, size_t ws_bytes,
                           tt_stream_t st) {
   TT_REQUIRE(world >= 1 && rank >= 0 && rank < world, "tuner train (dp): bad world/rank");

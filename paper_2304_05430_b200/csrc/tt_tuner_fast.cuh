@@ -265,7 +265,7 @@ struct FastArgs {
   int world, rank;
   int64_t gbase;        // global step index of this launch's first minibatch (monotone flags)
   int64_t dp_slice;     // floats per slice slot (>= kap * nbp of every job)
-  float* const* xb;     // [world] exchange buffers (fast_dp_layout)
+  void* const* xb;      // [world] exchange buffers (fast_dp_buffer_bytes each)
   float* scache;       // [B][sl.red - sl.x0]: per-slot forward caches (multi-round mode)
   float* wcache;       // [grid][attn_floats]: attention/head weight image per CTA (multi-round)
   unsigned int* ctr;   // [0] fwd, [1 + g] bwd, [2 + L + g] adam, [kCtrLoss] loss (monotone)
@@ -325,14 +325,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
-}
-__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // All threads; thread 0 spins until *ctr >= target.
@@ -1312,51 +1304,52 @@ __device__ void fast_job_stage(const FastArgs& a, const FastJob& jb, const JobGe
 }
 
 // Data-parallel exchange buffer of one rank (allocated by the host, shared
-// with the peers by IPC): n_jobs x world monotone u32 flags (padded to 64
-// words), then the receive slots [parity][job][source rank][slice].
-__host__ __device__ inline int64_t fast_dp_flag_words(int n_jobs, int world) {
-  return ((int64_t)n_jobs * world + 63) / 64 * 64;
-}
-__host__ __device__ inline int64_t fast_dp_buffer_floats(int n_jobs, int world, int64_t slice) {
-  return fast_dp_flag_words(n_jobs, world) + 2 * (int64_t)n_jobs * world * slice;
+// with the peers by IPC): receive slots [parity][job][source rank][slice] of
+// 8-byte words {value bits, flag} (the flag = global step + 1).
+__host__ __device__ inline int64_t fast_dp_buffer_bytes(int n_jobs, int world, int64_t slice) {
+  return 2 * (int64_t)n_jobs * world * slice * 8;
 }
 
 // The job's reduced slice gout[n] (this rank's microbatch) -> the mean over
 // the world's microbatches (SURVEY §8e option A: pairs stay inside each
-// rank's microbatch), identical on every rank: the slice is stored into every
-// peer's receive slot, one release flag per (job, source) is raised on the
-// peer, and after the peers' flags arrive the slots are summed in rank order.
-// Receive slots alternate by step parity: a rank can only reach the next use
-// of a parity after every peer has finished reading it (it needs their slices
-// of the step in between).
+// rank's microbatch), identical on every rank.  Low-latency protocol: every
+// value travels with its step flag in one 8-byte single-copy-atomic word,
+// stored straight into each peer's receive slot; the receiver spins on its
+// own words until the flags match and sums the ranks in fixed order -- no
+// fences, no separate flag round trip.  Slots alternate by step parity: a
+// rank can only reach the next use of a parity after every peer has read it
+// (it needs their slices of the step in between).
 __device__ void fast_dp_exchange(const FastArgs& a, int j, int step, float* gout, int n) {
   const int tid = threadIdx.x, W = a.world, me = a.rank;
   const int64_t gs = a.gbase + step;
-  const unsigned want = (unsigned)(gs + 1);
-  const int64_t fw = fast_dp_flag_words(a.n_jobs, W);
-  const int64_t base = fw + ((gs & 1) * (int64_t)a.n_jobs + j) * W * a.dp_slice;
+  const unsigned long long tag = (unsigned long long)(unsigned)(gs + 1) << 32;
+  const int64_t base = ((gs & 1) * (int64_t)a.n_jobs + j) * W * a.dp_slice;
   for (int i = tid; i < n; i += kThreads) {
-    const float v = gout[i];
+    const unsigned long long w = tag | __float_as_uint(gout[i]);
     for (int p = 0; p < W; ++p)
-      if (p != me) a.xb[p][base + (int64_t)me * a.dp_slice + i] = v;
+      if (p != me) {
+        unsigned long long* dst =
+            reinterpret_cast<unsigned long long*>(a.xb[p]) + base + (int64_t)me * a.dp_slice + i;
+        asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
+      }
   }
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence_system();
-    for (int p = 0; p < W; ++p)
-      if (p != me) st_release_sys(reinterpret_cast<unsigned*>(a.xb[p]) + (int64_t)j * W + me, want);
-    const unsigned* mine = reinterpret_cast<const unsigned*>(a.xb[me]) + (int64_t)j * W;
-    for (int p = 0; p < W; ++p)
-      if (p != me)
-        while (ld_acquire_sys(mine + p) < want) {
-        }
-  }
-  __syncthreads();
-  const float* rx = a.xb[me] + base;
+  const unsigned long long* rx = reinterpret_cast<const unsigned long long*>(a.xb[me]) + base;
   const float inv = 1.f / (float)W;
   for (int i = tid; i < n; i += kThreads) {
     float acc = 0.f;
-    for (int p = 0; p < W; ++p) acc += p == me ? gout[i] : __ldcg(rx + (int64_t)p * a.dp_slice + i);
+    for (int p = 0; p < W; ++p) {
+      float v;
+      if (p == me) {
+        v = gout[i];
+      } else {
+        unsigned long long w;
+        do {
+          asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(rx + (int64_t)p * a.dp_slice + i) : "memory");
+        } while ((w & 0xffffffff00000000ull) != tag);
+        v = __uint_as_float((unsigned)w);
+      }
+      acc += v;
+    }
     gout[i] = acc * inv;
   }
   __syncthreads();
