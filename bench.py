@@ -418,18 +418,31 @@ def run_b200(args, world, rank):
     stream = torch.cuda.current_stream()
 
     dp = None
+    dp_kind = "none"
     if world > 1:
         # data parallel: every rank holds its own 64x4096 shard (weak scaling);
         # global step = the ranks' microbatches of 16 (SURVEY §8e option A),
         # exchanged inside the one training launch per epoch over NVLink peer
         # memory (paper_2304_05430_b200.dist.FusedDataParallelTuner)
-        from paper_2304_05430_b200.dist import FusedDataParallelTuner
+        from paper_2304_05430_b200.dist import DataParallelTunerEpoch, FusedDataParallelTuner
 
-        dp = FusedDataParallelTuner.create(est, prog, yd, BATCH)
+        try:
+            dp = FusedDataParallelTuner.create(est, prog, yd, BATCH)
+            dp_kind = "fused peer-memory exchange in the training kernel"
+        except Exception as exc:  # noqa: BLE001  (no P2P/IPC between the GPUs)
+            print(f"fused DP unavailable ({exc}); NCCL all-reduce path", file=sys.stderr)
+            dp = DataParallelTunerEpoch(est, prog, yd, BATCH)
+            dp_kind = "NCCL all-reduce + Adam launch per step"
+
+    def dp_epoch():
+        if isinstance(dp, DataParallelTunerEpoch):
+            dp.run(rng.permutation(n), 1e-3, local_shard=True)
+            return None
+        return dp.run(rng.permutation(n), 1e-3)
 
     def epoch(t0):
         if dp is not None:
-            return dp.run(rng.permutation(n), 1e-3)
+            return dp_epoch()
         perm = _device.to_dev(rng.permutation(n).astype(np.int32))
         corr = _device.to_dev(_bias_corrections(t0, n_steps))
         return est._launch_train(dims, flat, m, v, prog, yd, perm, BATCH, _lib.TT_MODE_TRAIN, 1e-3,
@@ -459,7 +472,7 @@ def run_b200(args, world, rank):
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             if dp is not None:
-                status = dp.run(rng.permutation(n), 1e-3)
+                status = dp_epoch()
             else:
                 _, status, _ = est._launch_train(dims, flat, m, v, prog, yd, perms[k], BATCH,
                                                  _lib.TT_MODE_TRAIN, 1e-3, corrs[k], None)
@@ -610,12 +623,14 @@ def run_b200(args, world, rank):
                                    "training, 64 tasks x 4096 programs, batch 16, Adam; 1 step = 1 epoch",
                        "global_batch": BATCH * world, "seq_len": int(lens.max()),
                        "parallelism": f"dp{world}" if world > 1 else "single",
+                       "dp_exchange": dp_kind,
                        "l2": "flushed (256 MB write) between timed epochs"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            # one cooperative training launch per epoch per rank (DP included)
-            "gpu_launches": args.steps,
+            # one cooperative training launch per epoch per rank (fused DP
+            # included); the NCCL fallback launches gradient + Adam per step
+            "gpu_launches": args.steps if world == 1 or "fused" in dp_kind else 2 * n_steps * args.steps,
             "clocks": clocks.summary(int(os.environ.get("LOCAL_RANK", 0))),
             "extra": extra,
         }

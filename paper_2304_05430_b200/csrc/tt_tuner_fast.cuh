@@ -1319,21 +1319,23 @@ __host__ __device__ inline int64_t fast_dp_buffer_bytes(int n_jobs, int world, i
 // fences, no separate flag round trip.  Slots alternate by step parity: a
 // rank can only reach the next use of a parity after every peer has read it
 // (it needs their slices of the step in between).
-__device__ void fast_dp_exchange(const FastArgs& a, int j, int step, float* gout, int n) {
-  const int tid = threadIdx.x, W = a.world, me = a.rank;
-  const int64_t gs = a.gbase + step;
+// (out of line with scalar arguments: keeps the exchange out of the
+// register allocation of the single-GPU kernel body)
+__device__ __noinline__ void fast_dp_exchange(void* const* xb, int W, int me, int64_t gs,
+                                              int64_t slice, int n_jobs, int j, float* gout, int n) {
+  const int tid = threadIdx.x;
   const unsigned long long tag = (unsigned long long)(unsigned)(gs + 1) << 32;
-  const int64_t base = ((gs & 1) * (int64_t)a.n_jobs + j) * W * a.dp_slice;
+  const int64_t base = ((gs & 1) * (int64_t)n_jobs + j) * W * slice;
   for (int i = tid; i < n; i += kThreads) {
     const unsigned long long w = tag | __float_as_uint(gout[i]);
     for (int p = 0; p < W; ++p)
       if (p != me) {
         unsigned long long* dst =
-            reinterpret_cast<unsigned long long*>(a.xb[p]) + base + (int64_t)me * a.dp_slice + i;
+            reinterpret_cast<unsigned long long*>(xb[p]) + base + (int64_t)me * slice + i;
         asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(w) : "memory");
       }
   }
-  const unsigned long long* rx = reinterpret_cast<const unsigned long long*>(a.xb[me]) + base;
+  const unsigned long long* rx = reinterpret_cast<const unsigned long long*>(xb[me]) + base;
   const float inv = 1.f / (float)W;
   for (int i = tid; i < n; i += kThreads) {
     float acc = 0.f;
@@ -1344,7 +1346,7 @@ __device__ void fast_dp_exchange(const FastArgs& a, int j, int step, float* gout
       } else {
         unsigned long long w;
         do {
-          asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(rx + (int64_t)p * a.dp_slice + i) : "memory");
+          asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(rx + (int64_t)p * slice + i) : "memory");
         } while ((w & 0xffffffff00000000ull) != tag);
         v = __uint_as_float((unsigned)w);
       }
@@ -1422,7 +1424,8 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int jidx, int
   }
   __syncthreads();
   if (blockIdx.x == (unsigned)(a.B % gridDim.x)) fmark_any(step, 23);
-  if (a.world > 1 && a.mode == TT_MODE_TRAIN) fast_dp_exchange(a, jidx, step, gout, kap * nbp);
+  if (a.world > 1 && a.mode == TT_MODE_TRAIN)
+    fast_dp_exchange(a.xb, a.world, a.rank, a.gbase + step, a.dp_slice, a.n_jobs, jidx, gout, kap * nbp);
   // parameter addresses of the slice and the fused Adam update
   const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
   const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
