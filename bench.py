@@ -300,6 +300,39 @@ def survey_configs(est, dims, flat, l2, stream, n_steps16, prog, yd, prng):
     return out
 
 
+def mlp_training(n=65536, F=164):
+    """CostMLP.fit's epoch kernel (mlp.py:111-144) at the reference's
+    minibatch of 16, device time of one launch (one epoch)."""
+    import torch
+
+    from paper_2304_05430_b200 import CostMLP, _device, _lib
+    from paper_2304_05430_b200.estimators import _bias_corrections
+
+    rng = np.random.default_rng(3)
+    X = rng.normal(size=(n, F))
+    y = rng.uniform(0.1, 0.9, size=n)
+    m = CostMLP(epochs=0, batch_size=BATCH, loss="ranking", seed=0)
+    m.precision = "fp32"
+    m.fit(X[:64], y[:64])
+    flat = m._device_flat(list(m.NAMES)).clone()
+    mm, vv = torch.zeros_like(flat), torch.zeros_like(flat)
+    Xd = _device.to_dev(X.ravel(), torch.float32)
+    yd = _device.to_dev(y, torch.float32)
+    order = _device.to_dev(rng.permutation(n).astype(np.int32))
+    steps = (n + BATCH - 1) // BATCH
+    corr = _device.to_dev(_bias_corrections(0, steps))
+    ts = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        m._launch_train(flat, mm, vv, Xd, yd, F, order, BATCH, _lib.TT_MODE_TRAIN, 1e-3, corr)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t = float(np.median(ts))
+    return {"mlp_train_f164_samples_per_s": n / t, "mlp_train_us_per_step": t / steps * 1e6}
+
+
 def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
     """CostMLP bulk scoring at TenSet width (configs[0]/[2] shape): the
     tcgen05 tf32 kernel and the fp32 CUDA-core kernel, HBM roofline
@@ -611,6 +644,7 @@ def run_b200(args, world, rank):
                 w.append(time.perf_counter() - t0_)
             extra[f"predict_latency_{k_}_us"] = float(np.median(w)) * 1e6
         extra.update(survey_configs(est, dims, flat, l2, stream, n_steps, prog, yd, rng))
+        extra.update(mlp_training())
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(steps, off, ctx, y)

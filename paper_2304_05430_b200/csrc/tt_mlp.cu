@@ -8,6 +8,8 @@
 // the 64x64 second layer reuses the same tiling from shared memory and the
 // 64->1 output is a per-row dot product.  This CUDA-core tile is the
 // correctness baseline for the tcgen05 version.
+#include <type_traits>
+
 #include "tt_ops.cuh"
 
 namespace tt {
@@ -265,6 +267,284 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_kernel(MlpTrainArgs<R> a) {
   }
 }
 
+// ------------------------------------------- training, shared-memory resident --
+// fp32, minibatch <= 16 rows at the reference's widths: the parameters and
+// both Adam moments live in shared memory for the whole epoch (3 x 14,785
+// floats at F = 164), so a step touches global memory only for its X rows
+// (prefetched one step ahead by cp.async) and the loss value.  Per step:
+// forward h1, h2, out (thread = (4 rows, 1 column)); loss; D2 and D1 with
+// the pre-update W3 / W2; then every gradient entry is formed by a
+// fixed-order sum over the rows and immediately applied by the fused Adam
+// update (or written out in gradient mode).  Deterministic: no atomics.
+constexpr int kMB = 16;  // rows per minibatch of this kernel
+
+struct MlpSmemLayout {
+  int64_t prm, m, v, x, h1, h2, d1, d2, out, ys, dsc, red, total;  // float offsets
+};
+
+inline __host__ __device__ int mlp_fp(int F) { return (F + 3) / 4 * 4; }  // padded X row
+
+inline __host__ __device__ MlpSmemLayout mlp_smem_layout(int F) {
+  MlpSmemLayout l{};
+  const int64_t np = mlp_offsets(F).total;
+  const int64_t npp = (np + 3) / 4 * 4;
+  const int64_t xf = (int64_t)kMB * mlp_fp(F);
+  l.prm = 0;
+  l.m = npp;
+  l.v = 2 * npp;
+  l.x = 3 * npp;                // two X buffers, rows padded to a multiple of 4 (zeros)
+  l.h1 = l.x + 2 * xf;
+  l.h2 = l.h1 + kMB * kW;
+  l.d1 = l.h2 + kMB * kW;
+  l.d2 = l.d1 + kMB * kW;
+  l.out = l.d2 + kMB * kW;
+  l.ys = l.out + kMB;
+  l.dsc = l.ys + kMB;
+  l.red = l.dsc + kMB;
+  l.total = l.red + kMT + 3 * kMB + 2 * kMB;  // + order ring [3][16] (int), y ring [2][16]
+  return l;
+}
+
+__device__ __forceinline__ void cp_async4_mlp(float* s, const float* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(s)),
+               "l"(g)
+               : "memory");
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// 4x4 register tile of a weight gradient dW[a][b] = sum_r A[r][a] Bm[r][b]
+// (A rows stride lda, Bm rows stride ldb, both 16-B aligned), rows in order.
+__device__ __forceinline__ void grad_tile(const float* A, int lda, const float* Bm, int ldb, int a0,
+                                          int b0, int bn, float (&g)[4][4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) g[i][j] = 0.f;
+  for (int r = 0; r < bn; ++r) {
+    const float4 x = ld4(A + r * lda + a0), d = ld4(Bm + r * ldb + b0);
+    const float xa[4] = {x.x, x.y, x.z, x.w}, da[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) g[i][j] = fmaf(xa[i], da[j], g[i][j]);
+  }
+}
+
+__global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<float> a) {
+  extern __shared__ __align__(16) float smf[];
+  const int F = a.F, Fp = mlp_fp(F), tid = threadIdx.x, lane = tid & 31;
+  const MOff o = mlp_offsets(F);
+  const MlpSmemLayout L = mlp_smem_layout(F);
+  const int64_t xf = (int64_t)kMB * Fp;
+  float* P = smf + L.prm;
+  float* M = smf + L.m;
+  float* V = smf + L.v;
+  float* H1 = smf + L.h1;
+  float* H2 = smf + L.h2;
+  float* D1 = smf + L.d1;
+  float* D2 = smf + L.d2;
+  float* out = smf + L.out;
+  float* ys = smf + L.ys;
+  float* dsc = smf + L.dsc;
+  float* red = smf + L.red;
+  for (int64_t p = tid; p < o.total; p += kMT) {
+    P[p] = a.prm[p];
+    if (a.mode == TT_MODE_TRAIN) {
+      M[p] = a.m[p];
+      V[p] = a.v[p];
+    }
+  }
+  for (int64_t i = tid; i < 2 * xf; i += kMT) smf[L.x + i] = 0.f;  // pads stay zero
+  // staging pipeline (no global load on a step's critical path): during step
+  // s the order indices of step s + 2 and, through the indices already in
+  // shared memory, the X rows and labels of step s + 1 are copied by cp.async
+  int* ordr = reinterpret_cast<int*>(smf + L.red + kMT);  // [3][kMB]
+  float* yr = smf + L.red + kMT + 3 * kMB;                // [2][kMB]
+  auto rows_of = [&](int step) {
+    const int64_t b0 = (int64_t)step * a.B;
+    return (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
+  };
+  auto stage_order = [&](int step) {
+    if (step >= a.n_steps) return;
+    const int bn = rows_of(step);
+    for (int i = tid; i < bn; i += kMT)
+      cp_async4_mlp(reinterpret_cast<float*>(ordr + (step % 3) * kMB + i),
+                    reinterpret_cast<const float*>(a.order + (int64_t)step * a.B + i));
+  };
+  auto stage_rows = [&](int step) {
+    if (step >= a.n_steps) return;
+    const int bn = rows_of(step);
+    const int* od = ordr + (step % 3) * kMB;
+    float* xs = smf + L.x + (step & 1) * xf;
+    for (int i = tid; i < bn * F; i += kMT) {
+      const int r = i / F, k = i - r * F;
+      cp_async4_mlp(xs + r * Fp + k, a.X + (int64_t)od[r] * F + k);
+    }
+    for (int i = tid; i < bn; i += kMT) cp_async4_mlp(yr + (step & 1) * kMB + i, a.y + od[i]);
+  };
+  stage_order(0);
+  stage_order(1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  stage_rows(0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  const int c = tid & 63, rq = tid >> 6;  // forward: output column, group of 4 rows
+  for (int step = 0; step < a.n_steps; ++step) {
+    const int64_t b0 = (int64_t)step * a.B;
+    const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
+    const float* X = smf + L.x + (step & 1) * xf;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    for (int k = tid; k < bn; k += kMT) ys[k] = yr[(step & 1) * kMB + k];
+    stage_order(step + 2);  // overlaps this step
+    stage_rows(step + 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    // ---- forward (mlp.py:72-79): rows 4 rq .. 4 rq + 3, column c; the X / H1
+    //      rows are read as float4 broadcasts, the weight column per k
+    {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int k = 0; k < Fp; k += 4) {
+        float w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = k + j < F ? P[o.W1 + (k + j) * kW + c] : 0.f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 x = ld4(X + (4 * rq + i) * Fp + k);
+          acc[i] = fmaf(x.x, w[0], acc[i]);
+          acc[i] = fmaf(x.y, w[1], acc[i]);
+          acc[i] = fmaf(x.z, w[2], acc[i]);
+          acc[i] = fmaf(x.w, w[3], acc[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) H1[(4 * rq + i) * kW + c] = Act<float>::tanh(acc[i] + P[o.b1 + c]);
+    }
+    __syncthreads();
+    {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int k = 0; k < kW; k += 4) {
+        float w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = P[o.W2 + (k + j) * kW + c];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 x = ld4(H1 + (4 * rq + i) * kW + k);
+          acc[i] = fmaf(x.x, w[0], acc[i]);
+          acc[i] = fmaf(x.y, w[1], acc[i]);
+          acc[i] = fmaf(x.z, w[2], acc[i]);
+          acc[i] = fmaf(x.w, w[3], acc[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) H2[(4 * rq + i) * kW + c] = Act<float>::tanh(acc[i] + P[o.b2 + c]);
+    }
+    __syncthreads();
+    // out[r] = H2[r] . W3 + b3: warp w < bn / 2 handles rows 2w, 2w + 1 (lane halves)
+    if (tid < 8 * 32) {
+      const int r = (tid >> 5) * 2 + (lane >> 4), q = lane & 15;
+      float s = 0.f;
+      if (r < bn) {
+        const float4 h = ld4(H2 + r * kW + 4 * q), w = ld4(P + o.W3 + 4 * q);
+        s = fmaf(h.x, w.x, fmaf(h.y, w.y, fmaf(h.z, w.z, h.w * w.w)));
+      }
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+      if (q == 0 && r < bn) out[r] = s + P[o.b3];
+    }
+    __syncthreads();
+    const float loss = a.loss_kind == TT_LOSS_RANK ? rank_loss_block<float>(ys, out, bn, dsc, red)
+                                                   : mse_block<float>(ys, out, bn, dsc, red);
+    if (tid == 0) a.step_loss[step] = loss;
+    if (!isfinite(loss)) {
+      if (tid == 0) a.status[0] = step;
+      return;
+    }
+    // ---- backward (mlp.py:81-95) with the pre-update W3, W2
+    for (int i = tid; i < kMB * kW; i += kMT) {
+      const int r = i / kW, k = i % kW;
+      const float h = H2[i];
+      D2[i] = r < bn ? dsc[r] * P[o.W3 + k] * (1.f - h * h) : 0.f;  // rows >= bn: zero
+    }
+    __syncthreads();
+    for (int i = tid; i < kMB * kW; i += kMT) {
+      const int r = i / kW, k = i % kW;
+      float s = 0.f;
+      // lane-rotated column order: W2 row k is read without bank conflicts
+      for (int t = 0; t < kW; ++t) {
+        const int cc = (t + lane) & (kW - 1);
+        s = fmaf(D2[r * kW + cc], P[o.W2 + k * kW + cc], s);
+      }
+      const float h = H1[i];
+      D1[i] = r < bn ? s * (1.f - h * h) : 0.f;
+    }
+    __syncthreads();
+    // ---- gradients (4x4 register tiles, rows in order) + fused Adam
+    const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
+    const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
+    auto apply = [&](int64_t p, float g) {
+      if (a.mode == TT_MODE_GRAD) {
+        a.grad_out[p] = g;
+      } else {
+        float pp = P[p], mm = M[p], vv = V[p];
+        adam_update<float>(pp, g, mm, vv, a.hyp, c1, c2);
+        P[p] = pp;
+        M[p] = mm;
+        V[p] = vv;
+      }
+    };
+    const int t1 = (Fp / 4) * (kW / 4), t2 = (kW / 4) * (kW / 4);
+    for (int t = tid; t < t1 + t2; t += kMT) {
+      float g[4][4];
+      if (t < t1) {  // W1[f][k] = sum_r X[r][f] D1[r][k]
+        const int f0 = (t / (kW / 4)) * 4, k0 = (t % (kW / 4)) * 4;
+        grad_tile(X, Fp, D1, kW, f0, k0, bn, g);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (f0 + i < F)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) apply(o.W1 + (int64_t)(f0 + i) * kW + k0 + j, g[i][j]);
+      } else {  // W2[k][cc] = sum_r H1[r][k] D2[r][cc]
+        const int u = t - t1, k0 = (u / (kW / 4)) * 4, c0 = (u % (kW / 4)) * 4;
+        grad_tile(H1, kW, D2, kW, k0, c0, bn, g);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) apply(o.W2 + (int64_t)(k0 + i) * kW + c0 + j, g[i][j]);
+      }
+    }
+    // biases and W3 (rows in order)
+    for (int i = tid; i < 3 * kW + 1; i += kMT) {
+      float g = 0.f;
+      int64_t p;
+      if (i < kW) {
+        for (int r = 0; r < bn; ++r) g += D1[r * kW + i];
+        p = o.b1 + i;
+      } else if (i < 2 * kW) {
+        for (int r = 0; r < bn; ++r) g += D2[r * kW + i - kW];
+        p = o.b2 + i - kW;
+      } else if (i < 3 * kW) {
+        for (int r = 0; r < bn; ++r) g += H2[r * kW + i - 2 * kW] * dsc[r];
+        p = o.W3 + i - 2 * kW;
+      } else {
+        for (int r = 0; r < bn; ++r) g += dsc[r];
+        p = o.b3;
+      }
+      apply(p, g);
+    }
+    __syncthreads();
+  }
+  if (a.mode == TT_MODE_TRAIN)
+    for (int64_t p = tid; p < o.total; p += kMT) {
+      a.prm[p] = P[p];
+      a.m[p] = M[p];
+      a.v[p] = V[p];
+    }
+}
+
+inline size_t mlp_smem_bytes(int F) { return (size_t)mlp_smem_layout(F).total * sizeof(float); }
+
 template <typename R>
 static int mlp_predict(const R* prm, const R* X, int64_t n, int F, R* out, tt_stream_t st) {
   TT_REQUIRE(n >= 0 && F >= 1, "mlp predict: bad shape");
@@ -322,6 +602,19 @@ static int mlp_train(R* prm, R* m, R* v, const R* X, const R* y, int F, const in
   a.dsc = a.ys + B;
   a.grad = reinterpret_cast<R*>(static_cast<char*>(ws) +
                                 align_up((size_t)(4 * kW + 3) * B * sizeof(R), 256));
+  if constexpr (std::is_same<R, float>::value) {
+    // shared-memory resident kernel when the minibatch and the parameters fit
+    const size_t sm2 = mlp_smem_bytes(F);
+    int dev = 0, optin = 0;
+    TT_CUDA(cudaGetDevice(&dev));
+    TT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (B <= kMB && sm2 + 1024 <= (size_t)optin) {
+      TT_CUDA(cudaFuncSetAttribute(mlp_train_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)sm2));
+      mlp_train_smem_kernel<<<1, kMT, sm2, as_stream(st)>>>(a);
+      return check_launch("mlp train (smem)");
+    }
+  }
   const size_t smem = sizeof(MlpSmem<R>);
   auto kern = mlp_train_kernel<R>;
   TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
