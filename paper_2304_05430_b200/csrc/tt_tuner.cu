@@ -329,11 +329,25 @@ struct DpArgs {
 
 template <typename R>
 struct Launch {
+  // Small batches (search-time scoring: one candidate per annealing step,
+  // <= 32 per evolution generation, search.py:319, :392-410) use one program
+  // per CTA: a tile walks its programs one after another inside each time
+  // step, so the latency grows with the programs per tile, while a small
+  // batch cannot fill the GPU anyway.
   template <int H>
   static int predict_h(const TDims& dm, const R* prm, const R* steps, const int64_t* rowoff,
                        const R* ctx, int64_t n, R* yhat, void* ws, size_t ws_bytes,
                        cudaStream_t st, R* s_out) {
-    constexpr int P = ScoreP<R>::value;
+    if (n <= (int64_t)sm_count())
+      return predict_hp<H, 1>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st, s_out);
+    return predict_hp<H, ScoreP<R>::value>(dm, prm, steps, rowoff, ctx, n, yhat, ws, ws_bytes, st,
+                                           s_out);
+  }
+
+  template <int H, int P>
+  static int predict_hp(const TDims& dm, const R* prm, const R* steps, const int64_t* rowoff,
+                        const R* ctx, int64_t n, R* yhat, void* ws, size_t ws_bytes,
+                        cudaStream_t st, R* s_out) {
     const int64_t slot = (int64_t)3 * P * dm.Tmax * dm.D + (int64_t)2 * P * dm.Tmax * dm.G;
     const size_t smem = score_smem_bytes<R, P>(dm);
     auto kern = tuner_predict_kernel<R, H, P>;
