@@ -276,7 +276,8 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_kernel(MlpTrainArgs<R> a) {
 // the pre-update W3 / W2; then every gradient entry is formed by a
 // fixed-order sum over the rows and immediately applied by the fused Adam
 // update (or written out in gradient mode).  Deterministic: no atomics.
-constexpr int kMB = 16;  // rows per minibatch of this kernel
+constexpr int kMB = 16;   // rows per minibatch of this kernel
+constexpr int kMT2 = 512; // its threads
 
 struct MlpSmemLayout {
   int64_t prm, m, v, x, h1, h2, d1, d2, out, ys, dsc, red, total;  // float offsets
@@ -301,7 +302,7 @@ inline __host__ __device__ MlpSmemLayout mlp_smem_layout(int F) {
   l.ys = l.out + kMB;
   l.dsc = l.ys + kMB;
   l.red = l.dsc + kMB;
-  l.total = l.red + kMT + 3 * kMB + 2 * kMB;  // + order ring [3][16] (int), y ring [2][16]
+  l.total = l.red + kMT2 + 3 * kMB + 2 * kMB;  // + order ring [3][16] (int), y ring [2][16]
   return l;
 }
 
@@ -331,7 +332,7 @@ __device__ __forceinline__ void grad_tile(const float* A, int lda, const float* 
   }
 }
 
-__global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<float> a) {
+__global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<float> a) {
   extern __shared__ __align__(16) float smf[];
   const int F = a.F, Fp = mlp_fp(F), tid = threadIdx.x, lane = tid & 31;
   const MOff o = mlp_offsets(F);
@@ -348,19 +349,19 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
   float* ys = smf + L.ys;
   float* dsc = smf + L.dsc;
   float* red = smf + L.red;
-  for (int64_t p = tid; p < o.total; p += kMT) {
+  for (int64_t p = tid; p < o.total; p += kMT2) {
     P[p] = a.prm[p];
     if (a.mode == TT_MODE_TRAIN) {
       M[p] = a.m[p];
       V[p] = a.v[p];
     }
   }
-  for (int64_t i = tid; i < 2 * xf; i += kMT) smf[L.x + i] = 0.f;  // pads stay zero
+  for (int64_t i = tid; i < 2 * xf; i += kMT2) smf[L.x + i] = 0.f;  // pads stay zero
   // staging pipeline (no global load on a step's critical path): during step
   // s the order indices of step s + 2 and, through the indices already in
   // shared memory, the X rows and labels of step s + 1 are copied by cp.async
-  int* ordr = reinterpret_cast<int*>(smf + L.red + kMT);  // [3][kMB]
-  float* yr = smf + L.red + kMT + 3 * kMB;                // [2][kMB]
+  int* ordr = reinterpret_cast<int*>(smf + L.red + kMT2);  // [3][kMB]
+  float* yr = smf + L.red + kMT2 + 3 * kMB;                // [2][kMB]
   auto rows_of = [&](int step) {
     const int64_t b0 = (int64_t)step * a.B;
     return (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
@@ -368,7 +369,7 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
   auto stage_order = [&](int step) {
     if (step >= a.n_steps) return;
     const int bn = rows_of(step);
-    for (int i = tid; i < bn; i += kMT)
+    for (int i = tid; i < bn; i += kMT2)
       cp_async4_mlp(reinterpret_cast<float*>(ordr + (step % 3) * kMB + i),
                     reinterpret_cast<const float*>(a.order + (int64_t)step * a.B + i));
   };
@@ -377,11 +378,11 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
     const int bn = rows_of(step);
     const int* od = ordr + (step % 3) * kMB;
     float* xs = smf + L.x + (step & 1) * xf;
-    for (int i = tid; i < bn * F; i += kMT) {
+    for (int i = tid; i < bn * F; i += kMT2) {
       const int r = i / F, k = i - r * F;
       cp_async4_mlp(xs + r * Fp + k, a.X + (int64_t)od[r] * F + k);
     }
-    for (int i = tid; i < bn; i += kMT) cp_async4_mlp(yr + (step & 1) * kMB + i, a.y + od[i]);
+    for (int i = tid; i < bn; i += kMT2) cp_async4_mlp(yr + (step & 1) * kMB + i, a.y + od[i]);
   };
   stage_order(0);
   stage_order(1);
@@ -390,28 +391,28 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
   __syncthreads();
   stage_rows(0);
   asm volatile("cp.async.commit_group;" ::: "memory");
-  const int c = tid & 63, rq = tid >> 6;  // forward: output column, group of 4 rows
+  const int c = tid & 63, rq = tid >> 6;  // forward: output column, rows 2 rq, 2 rq + 1
   for (int step = 0; step < a.n_steps; ++step) {
     const int64_t b0 = (int64_t)step * a.B;
     const int bn = (int)(a.n_order - b0 < (int64_t)a.B ? a.n_order - b0 : (int64_t)a.B);
     const float* X = smf + L.x + (step & 1) * xf;
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    for (int k = tid; k < bn; k += kMT) ys[k] = yr[(step & 1) * kMB + k];
+    for (int k = tid; k < bn; k += kMT2) ys[k] = yr[(step & 1) * kMB + k];
     stage_order(step + 2);  // overlaps this step
     stage_rows(step + 1);
     asm volatile("cp.async.commit_group;" ::: "memory");
     // ---- forward (mlp.py:72-79): rows 4 rq .. 4 rq + 3, column c; the X / H1
     //      rows are read as float4 broadcasts, the weight column per k
     {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float acc[2] = {0.f, 0.f};
       for (int k = 0; k < Fp; k += 4) {
         float w[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) w[j] = k + j < F ? P[o.W1 + (k + j) * kW + c] : 0.f;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 x = ld4(X + (4 * rq + i) * Fp + k);
+        for (int i = 0; i < 2; ++i) {
+          const float4 x = ld4(X + (2 * rq + i) * Fp + k);
           acc[i] = fmaf(x.x, w[0], acc[i]);
           acc[i] = fmaf(x.y, w[1], acc[i]);
           acc[i] = fmaf(x.z, w[2], acc[i]);
@@ -419,18 +420,18 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) H1[(4 * rq + i) * kW + c] = Act<float>::tanh(acc[i] + P[o.b1 + c]);
+      for (int i = 0; i < 2; ++i) H1[(2 * rq + i) * kW + c] = Act<float>::tanh(acc[i] + P[o.b1 + c]);
     }
     __syncthreads();
     {
-      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      float acc[2] = {0.f, 0.f};
       for (int k = 0; k < kW; k += 4) {
         float w[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) w[j] = P[o.W2 + (k + j) * kW + c];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 x = ld4(H1 + (4 * rq + i) * kW + k);
+        for (int i = 0; i < 2; ++i) {
+          const float4 x = ld4(H1 + (2 * rq + i) * kW + k);
           acc[i] = fmaf(x.x, w[0], acc[i]);
           acc[i] = fmaf(x.y, w[1], acc[i]);
           acc[i] = fmaf(x.z, w[2], acc[i]);
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
         }
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) H2[(4 * rq + i) * kW + c] = Act<float>::tanh(acc[i] + P[o.b2 + c]);
+      for (int i = 0; i < 2; ++i) H2[(2 * rq + i) * kW + c] = Act<float>::tanh(acc[i] + P[o.b2 + c]);
     }
     __syncthreads();
     // out[r] = H2[r] . W3 + b3: warp w < bn / 2 handles rows 2w, 2w + 1 (lane halves)
@@ -462,13 +463,13 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
       return;
     }
     // ---- backward (mlp.py:81-95) with the pre-update W3, W2
-    for (int i = tid; i < kMB * kW; i += kMT) {
+    for (int i = tid; i < kMB * kW; i += kMT2) {
       const int r = i / kW, k = i % kW;
       const float h = H2[i];
       D2[i] = r < bn ? dsc[r] * P[o.W3 + k] * (1.f - h * h) : 0.f;  // rows >= bn: zero
     }
     __syncthreads();
-    for (int i = tid; i < kMB * kW; i += kMT) {
+    for (int i = tid; i < kMB * kW; i += kMT2) {
       const int r = i / kW, k = i % kW;
       float s = 0.f;
       // lane-rotated column order: W2 row k is read without bank conflicts
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
       }
     };
     const int t1 = (Fp / 4) * (kW / 4), t2 = (kW / 4) * (kW / 4);
-    for (int t = tid; t < t1 + t2; t += kMT) {
+    for (int t = tid; t < t1 + t2; t += kMT2) {
       float g[4][4];
       if (t < t1) {  // W1[f][k] = sum_r X[r][f] D1[r][k]
         const int f0 = (t / (kW / 4)) * 4, k0 = (t % (kW / 4)) * 4;
@@ -515,7 +516,7 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
       }
     }
     // biases and W3 (rows in order)
-    for (int i = tid; i < 3 * kW + 1; i += kMT) {
+    for (int i = tid; i < 3 * kW + 1; i += kMT2) {
       float g = 0.f;
       int64_t p;
       if (i < kW) {
@@ -536,7 +537,7 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_smem_kernel(MlpTrainArgs<flo
     __syncthreads();
   }
   if (a.mode == TT_MODE_TRAIN)
-    for (int64_t p = tid; p < o.total; p += kMT) {
+    for (int64_t p = tid; p < o.total; p += kMT2) {
       a.prm[p] = P[p];
       a.m[p] = M[p];
       a.v[p] = V[p];
@@ -611,7 +612,7 @@ static int mlp_train(R* prm, R* m, R* v, const R* X, const R* y, int F, const in
     if (B <= kMB && sm2 + 1024 <= (size_t)optin) {
       TT_CUDA(cudaFuncSetAttribute(mlp_train_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)sm2));
-      mlp_train_smem_kernel<<<1, kMT, sm2, as_stream(st)>>>(a);
+      mlp_train_smem_kernel<<<1, kMT2, sm2, as_stream(st)>>>(a);
       return check_launch("mlp train (smem)");
     }
   }
