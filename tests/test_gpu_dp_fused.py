@@ -30,7 +30,7 @@ def _unflatten(est, flat):
     return out
 
 
-@pytest.mark.parametrize("world,batch,loss", [(2, 8, "ranking"), (3, 5, "rmse")])
+@pytest.mark.parametrize("world,batch,loss", [(2, 8, "ranking"), (3, 5, "rmse"), (2, 100, "ranking")])
 def test_fused_dp_matches_oracle(cuda_ok, world, batch, loss):
     import torch
 
@@ -38,7 +38,8 @@ def test_fused_dp_matches_oracle(cuda_ok, world, batch, loss):
     from paper_2304_05430_b200.dist import FusedDataParallelTuner
     from paper_2304_05430_b200.layout import DevicePrograms
 
-    n_local = 4 * batch + 3  # a partial last microbatch on every rank
+    n_local = (4 if batch < 50 else 2) * batch + 3  # a partial last microbatch on every rank
+    # (batch 100 > the 74 CTAs of a rank here: the multi-round mode)
     rng = np.random.default_rng(world)
     seqs = random_seqs(rng, rng.integers(1, 11, size=world * n_local))
     y = rng.uniform(0.1, 0.9, size=world * n_local)
