@@ -20,7 +20,8 @@ template <typename R, int P>
 static size_t score_smem_bytes(const TDims& d) {
   const size_t n = (size_t)2 * P * d.H + (size_t)2 * P * d.G +
                    (size_t)3 * P * d.D + (size_t)P * d.heads * d.Tmax + (size_t)P * (d.D + d.C) +
-                   (size_t)P * kHeadHidden + kThreads + P + 8;
+                   (size_t)P * kHeadHidden + kThreads + P + 8 +
+                   (size_t)P * d.Tmax * d.D + 4;  // + the staged layer-input rows
   return n * sizeof(R) + 64;
 }
 
@@ -53,6 +54,9 @@ __global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
   am.red = sp;
   sp += kThreads;
   R* sh_y = sp;
+  sp += P + 8;
+  // layer-input rows of the tile, staged from the L2 scratch per layer (16-B aligned)
+  R* xin_s = reinterpret_cast<R*>((reinterpret_cast<uintptr_t>(sp) + 15) & ~uintptr_t(15));
   const AttnW<R> aw = attn_global_view<R>(dm, prm);
   const int64_t TD = (int64_t)dm.Tmax * D;
   R* buf[3];
@@ -80,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
     int cur = 0;
     for (int l = 0; l < dm.L; ++l) {
       lstm_layer_fwd<R, H, P, false>(dm, prm, l, ti, buf[cur ^ 1], buf[cur], sh_h, sh_g,
-                                     buf[2] + P * TD, nullptr, nullptr, nullptr);
+                                     buf[2] + P * TD, nullptr, nullptr, nullptr, xin_s);
       __syncthreads();
       cur ^= 1;
     }

@@ -334,7 +334,8 @@ __device__ void bmv_col_batch(const R* v, int ldv, const R* W, int ld, int K, in
 template <typename R, int H, int P, bool TRAIN>
 __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l,
                                const TileInfo<R, P>& ti, const R* inbuf, R* __restrict__ out,
-                               R* sh_h, R* sh_g, R* xzbuf, R* cache_g, R* cache_c, R* cache_tc) {
+                               R* sh_h, R* sh_g, R* xzbuf, R* cache_g, R* cache_c, R* cache_tc,
+                               R* xin_s = nullptr) {
   constexpr int G = 4 * H, D = 2 * H, NR = 128 / G, NQ = 128 / H;
   const int dir = threadIdx.x >> 7, lt = threadIdx.x & 127;
   const int c = lt % G, r = lt / G;
@@ -349,6 +350,27 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
   // the entries it wrote, so no barrier is needed.  The Wx column is live
   // only here, leaving the recurrence with the Wh column alone.
   R* xz = xzbuf + (int64_t)dir * P * Tmax * G;
+  if (l > 0 && xin_s != nullptr) {
+    // (all threads of the CTA) the layer-input rows from the L2 scratch into
+    // shared memory in one pass, so the projection below does not wait one
+    // L2 round trip per row
+    constexpr int V = 16 / sizeof(R);
+    const int tot = P * Tmax * D / V;  // whole tile block (rows past a program's end unused)
+    const int4* src = reinterpret_cast<const int4*>(inbuf);
+    int4* dst = reinterpret_cast<int4*>(xin_s);
+    const int nt = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < tot; i0 += 4 * nt) {
+      int4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * nt < tot) v[u] = src[i0 + u * nt];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (i0 + u * nt < tot) dst[i0 + u * nt] = v[u];
+    }
+    __syncthreads();
+    inbuf = xin_s;
+  }
   if (l > 0) {
     R wx[D];
 #pragma unroll
