@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
   R* sh_y = sp;
   sp += P + 8;
   // layer-input rows of the tile, staged from the L2 scratch per layer (16-B aligned)
-  R* xin_s = reinterpret_cast<R*>((reinterpret_cast<uintptr_t>(sp) + 15) & ~uintptr_t(15));
+  R* xin_s = sp + ((16 - (reinterpret_cast<uintptr_t>(sp) & 15)) & 15) / sizeof(R);
   const AttnW<R> aw = attn_global_view<R>(dm, prm);
   const int64_t TD = (int64_t)dm.Tmax * D;
   R* buf[3];

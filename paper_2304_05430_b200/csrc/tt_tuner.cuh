@@ -369,18 +369,28 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
         if (i0 + u * nt < tot) dst[i0 + u * nt] = v[u];
     }
     __syncthreads();
-    inbuf = xin_s;
   }
   if (l > 0) {
     R wx[D];
 #pragma unroll
     for (int k = 0; k < D; ++k) wx[k] = ldw<TRAIN>(Wx + k * G + c);
+    // (two copies of the loop so the staged one compiles to shared-memory loads)
+    if (xin_s != nullptr) {
 #pragma unroll 1
-    for (int p = r; p < P; p += NR) {
-      const int n = ti.len[p];
-      for (int t = 0; t < n; ++t)
-        xz[((int64_t)p * Tmax + t) * G + c] =
-            dot_reg<D>(inbuf + ((int64_t)p * Tmax + t) * D, wx) + bc;
+      for (int p = r; p < P; p += NR) {
+        const int n = ti.len[p];
+        for (int t = 0; t < n; ++t)
+          xz[((int64_t)p * Tmax + t) * G + c] =
+              dot_reg<D>(xin_s + ((int64_t)p * Tmax + t) * D, wx) + bc;
+      }
+    } else {
+#pragma unroll 1
+      for (int p = r; p < P; p += NR) {
+        const int n = ti.len[p];
+        for (int t = 0; t < n; ++t)
+          xz[((int64_t)p * Tmax + t) * G + c] =
+              dot_reg<D>(inbuf + ((int64_t)p * Tmax + t) * D, wx) + bc;
+      }
     }
   }
   R wh[H];
