@@ -99,9 +99,10 @@ __global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
           s_out[(r0 + i / D) * D + i % D] = so[((int64_t)pp * dm.Tmax + i / D) * D + i % D];
       }
     }
-    // final layer output is buf[cur ^ 1]; K -> buf[cur], V -> buf[2]
-    attention_head_fwd<R, H, P, false>(dm, aw, ti, buf[cur ^ 1], buf[cur], buf[2], am, nullptr,
-                                       sh_y);
+    // final layer output buf[cur ^ 1] -> shared memory (pooling and the K / V
+    // projection read it); K -> buf[cur], V -> buf[2]
+    stage_rows_cta(buf[cur ^ 1], xin_s, (int)(P * TD * sizeof(R) / 16));
+    attention_head_fwd<R, H, P, false>(dm, aw, ti, xin_s, buf[cur], buf[2], am, nullptr, sh_y);
     if (threadIdx.x < P && ti.prog[threadIdx.x] >= 0) yhat[ti.prog[threadIdx.x]] = sh_y[threadIdx.x];
     __syncthreads();
   }

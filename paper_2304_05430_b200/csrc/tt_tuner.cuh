@@ -331,6 +331,24 @@ __device__ void bmv_col_batch(const R* v, int ldv, const R* W, int ld, int K, in
 // otherwise (previous layer output).  Output rows:
 // out[(p*Tmax + t)*D + dir*H + j].
 // TRAIN (P == 1): also records gates / cell state / tanh(cell) per step.
+// Copy n16 16-byte chunks global -> shared with all threads of the CTA, four
+// loads in flight per thread (a tile's layer rows; ends synced).
+__device__ __forceinline__ void stage_rows_cta(const void* src_, void* dst_, int n16) {
+  const int4* src = reinterpret_cast<const int4*>(src_);
+  int4* dst = reinterpret_cast<int4*>(dst_);
+  const int nt = blockDim.x;
+  for (int i0 = threadIdx.x; i0 < n16; i0 += 4 * nt) {
+    int4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * nt < n16) v[u] = src[i0 + u * nt];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (i0 + u * nt < n16) dst[i0 + u * nt] = v[u];
+  }
+  __syncthreads();
+}
+
 template <typename R, int H, int P, bool TRAIN>
 __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l,
                                const TileInfo<R, P>& ti, const R* inbuf, R* __restrict__ out,
@@ -354,21 +372,8 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
     // (all threads of the CTA) the layer-input rows from the L2 scratch into
     // shared memory in one pass, so the projection below does not wait one
     // L2 round trip per row
-    constexpr int V = 16 / sizeof(R);
-    const int tot = P * Tmax * D / V;  // whole tile block (rows past a program's end unused)
-    const int4* src = reinterpret_cast<const int4*>(inbuf);
-    int4* dst = reinterpret_cast<int4*>(xin_s);
-    const int nt = blockDim.x;
-    for (int i0 = threadIdx.x; i0 < tot; i0 += 4 * nt) {
-      int4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i0 + u * nt < tot) v[u] = src[i0 + u * nt];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (i0 + u * nt < tot) dst[i0 + u * nt] = v[u];
-    }
-    __syncthreads();
+    // whole tile block (rows past a program's end are copied but unused)
+    stage_rows_cta(inbuf, xin_s, (int)(P * Tmax * D * sizeof(R) / 16));
   }
   if (l > 0) {
     R wx[D];
