@@ -314,6 +314,18 @@ __device__ __forceinline__ void cp_async4_mlp(float* s, const float* g) {
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
+// optim.py:33-46 in fp32 with one division per parameter: the bias
+// corrections are applied as precomputed reciprocals and the denominator's
+// square root by the hardware's correctly rounded sqrt (differs from the
+// exactly rounded two-division form by an ulp; inside the fp32 tolerance)
+__device__ __forceinline__ void adam_fast(float& p, float g, float& m, float& v, float b1, float b2,
+                                          float ob1, float ob2, float lr, float eps, float ic1,
+                                          float ic2) {
+  m = fmaf(m, b1, ob1 * g);
+  v = fmaf(v, b2, ob2 * g * g);
+  p -= lr * (m * ic1) / (sqrtf(v * ic2) + eps);
+}
+
 // 4x4 register tile of a weight gradient dW[a][b] = sum_r A[r][a] Bm[r][b]
 // (A rows stride lda, Bm rows stride ldb, both 16-B aligned), rows in order.
 __device__ __forceinline__ void grad_tile(const float* A, int lda, const float* Bm, int ldb, int a0,
@@ -484,12 +496,15 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
     // ---- gradients (4x4 register tiles, rows in order) + fused Adam
     const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
     const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
+    const float hb1 = (float)a.hyp.b1, hb2 = (float)a.hyp.b2, ob1 = (float)(1.0 - a.hyp.b1),
+                ob2 = (float)(1.0 - a.hyp.b2), hlr = (float)a.hyp.lr, heps = (float)a.hyp.eps;
+    const float ic1 = (float)(1.0 / c1), ic2 = (float)(1.0 / c2);
     auto apply = [&](int64_t p, float g) {
       if (a.mode == TT_MODE_GRAD) {
         a.grad_out[p] = g;
       } else {
         float pp = P[p], mm = M[p], vv = V[p];
-        adam_update<float>(pp, g, mm, vv, a.hyp, c1, c2);
+        adam_fast(pp, g, mm, vv, hb1, hb2, ob1, ob2, hlr, heps, ic1, ic2);
         P[p] = pp;
         M[p] = mm;
         V[p] = vv;
