@@ -303,6 +303,57 @@ def survey_configs(est, dims, flat, l2, stream, n_steps16, prog, yd, prng):
     return out
 
 
+def dp_exchange_cost(n_tasks=4):
+    """Fused data-parallel exchange measured on this one GPU:
+    two ranks run concurrently on disjoint halves of the SMs, exchanging
+    their gradient slices inside the training kernel, against two
+    independent single-rank runs on the same halves (tools/dp_sim_bench.py
+    has the longer version).  The transport is this GPU's memory, not
+    NVLink."""
+    import torch
+
+    from paper_2304_05430_b200 import RecurrentAttentionTuner, _device, _lib
+    from paper_2304_05430_b200.dist import FusedDataParallelTuner
+    from paper_2304_05430_b200.layout import DevicePrograms, HostPrograms
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    parts = []
+    for r in range(2):
+        st, of, cx, yy, _ = synth(n_tasks=n_tasks, per_task=PER_TASK, seed=10 + r)
+        e = RecurrentAttentionTuner(batch_size=BATCH, loss="ranking", seed=0)
+        e.precision = "fp32"
+        e._init_params()
+        parts.append((e, DevicePrograms(HostPrograms(st, of, cx), "fp32"), _device.to_dev(yy, torch.float32)))
+    n = parts[0][1].n
+    steps = (n + BATCH - 1) // BATCH
+    out = {}
+    _lib.call("tt_tuner_train_set_grid", sms // 2)
+    try:
+        for name, groups in (("independent", [[p] for p in parts]), ("fused_dp2", [parts])):
+            ranks = [rk for g in groups
+                     for rk in FusedDataParallelTuner.local_group([a for a, _, _ in g], [b for _, b, _ in g],
+                                                                  [c for _, _, c in g], BATCH)]
+            streams = [torch.cuda.Stream() for _ in ranks]
+            rng = np.random.default_rng(0)
+            best = None
+            for _ in range(3):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for rk, s in zip(ranks, streams):
+                    with torch.cuda.stream(s):
+                        rk.run(rng.permutation(n), 1e-3)
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+                best = dt if best is None else min(best, dt)
+            out[name] = best / steps * 1e6
+            for rk in ranks:
+                rk.close()
+    finally:
+        _lib.call("tt_tuner_train_set_grid", 0)
+    return {"dp2_sim_us_per_step": out["fused_dp2"], "dp2_sim_independent_us_per_step": out["independent"],
+            "dp2_sim_exchange_us_per_step": out["fused_dp2"] - out["independent"]}
+
+
 def mlp_training(n=65536, F=164):
     """CostMLP.fit's epoch kernel (mlp.py:111-144) at the reference's
     minibatch of 16, device time of one launch (one epoch)."""
@@ -651,6 +702,7 @@ def run_b200(args, world, rank):
             extra[f"predict_latency_{k_}_us"] = float(np.median(w)) * 1e6
         extra.update(survey_configs(est, dims, flat, l2, stream, n_steps, prog, yd, rng))
         extra.update(mlp_training())
+        extra.update(dp_exchange_cost())
 
     if rank == 0:
         cpu = None if args.no_cpu else cpu_baseline(steps, off, ctx, y)
