@@ -416,7 +416,7 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
     // gate phase: z = b + x_t Wx + h Wh ; activation by gate block.  One
     // program at a time (not unrolled) keeps the register file for the
     // stationary weight columns.
-#pragma unroll 1
+#pragma unroll 2
     for (int p = r; p < P; p += NR) {
       const int n = ti.len[p];
       if (s < n) {
