@@ -1,30 +1,35 @@
-// Attention tuner training, latency path (v4): hidden 32, fp32, minibatch
-// B <= #SMs with every per-sample cache in shared memory.
+// Attention tuner training, latency path: hidden 32, fp32, every per-sample
+// cache in shared memory (longest program <= ~14 steps at the default widths).
 //
 // Reference: estimators/tuner.py _train/_forward/_backward (:227-466),
 // _LstmDirection (:55-151), ranking_grad (mlp.py:25-35), Adam (optim.py).
 //
 // One persistent cooperative launch runs a whole epoch.  Two CTA roles:
 //
-//  * sample CTAs (blockIdx < B): CTA k owns minibatch slot k.  It runs the
-//    sample's forward (3 x biLSTM, attention passes, head), exchanges the
-//    scores through L2, evaluates the minibatch loss (identical arithmetic in
-//    every sample CTA), then runs the ACTIVATION backward only: the
-//    per-direction recurrences (BPTT) run on one warp each, lane j owning
-//    hidden unit j and its 4 gate columns / its Wh row in registers.  Every
-//    operand a weight gradient needs (layer outputs, dZ, dK, dV, attention
-//    pass vectors, head vectors) is published to an L2 exchange slot.
+//  * sample CTAs: CTA k owns minibatch slot k (B <= #SMs; larger minibatches
+//    run several rounds per CTA, the forward caches of all but the last slot
+//    parked in L2 by bulk copies).  A slot's forward (3 x biLSTM with a warp
+//    PAIR per direction, attention passes, head), the score exchange through
+//    L2, the minibatch loss (identical arithmetic in every sample CTA), then
+//    the ACTIVATION backward only.  Every operand a weight gradient needs
+//    (layer inputs, h_prev, dZ, dK, dV, attention pass vectors, head vectors)
+//    is published to the L2 exchange, stacked by minibatch row.
 //  * gradient jobs (all CTAs, non-sample CTAs first): the parameter vector is
 //    cut into column slices of every weight matrix; a job reduces
 //    dW[:, slice] = sum_rows A^T B over the minibatch rows in a fixed order
 //    (deterministic, no atomics on data) and applies the fused Adam update
-//    (or writes the gradient in TT_MODE_GRAD).
+//    (or writes the gradient in TT_MODE_GRAD).  Data parallel (world > 1):
+//    the reduced slice is first exchanged with the peer ranks through their
+//    exchange buffers (fast_dp_exchange) and averaged in rank order.
 //
-// Phases are ordered by three monotone L2 counters instead of grid barriers:
-// forward-done (score exchange), backward-done (jobs may start) and
-// adam-done (next minibatch may read the parameters).  The weight gradient
-// never materialises per sample: the traffic per step is the exchange slots
-// (~45 KB/sample at T = 10) instead of B partial 330 KB gradient vectors.
+// Phases are ordered by monotone L2 counters instead of grid barriers:
+// forward-done (score exchange), backward-done per parameter group (jobs may
+// start) and Adam-done per group (the next minibatch may read those
+// parameters, layer by layer).  Heads-only mode (s_frozen): the recurrent
+// stack is frozen, its last-layer outputs come from a cache, the steps run
+// attention + head only.  The weight gradient never materialises per sample:
+// the traffic per step is the exchange rows (~45 KB/sample at T = 10)
+// instead of B partial 330 KB gradient vectors.
 #pragma once
 
 #include "tt_sm100.cuh"
