@@ -213,7 +213,10 @@ class FusedDataParallelTuner:
     @classmethod
     def create(cls, est, prog, y_dev, batch: int, group=None):
         """Collective over torch.distributed: allocate this rank's exchange
-        buffer, all-gather the IPC handles, open the peers' buffers."""
+        buffer, all-gather the IPC handles, open the peers' buffers.  Every
+        rank takes part in every collective even when a step fails, and the
+        ranks agree on the outcome (LibraryError on all of them if any
+        failed: e.g. no peer access between the GPUs)."""
         import ctypes
 
         import torch
@@ -222,19 +225,36 @@ class FusedDataParallelTuner:
         from . import _device, _lib
 
         world, rank = dist.get_world_size(group), dist.get_rank(group)
-        own, handle = cls._alloc(cls._buffer_bytes(est._dims(), world))
+        ok, own, handle, owned = True, None, bytes(64), []
+        try:
+            own, handle = cls._alloc(cls._buffer_bytes(est._dims(), world))
+            owned.append((own, False))
+        except Exception:  # noqa: BLE001
+            ok = False
         handles = exchange_handles(handle, group)
-        ptrs, owned = [], [(own, False)]
-        for r, h in enumerate(handles):
-            if r == rank:
-                ptrs.append(own)
-                continue
-            p = ctypes.c_void_p()
-            _lib.call("tt_ipc_open", (ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p))
-            ptrs.append(int(p.value))
-            owned.append((int(p.value), True))
+        ptrs = []
+        if ok:
+            try:
+                for r, h in enumerate(handles):
+                    if r == rank:
+                        ptrs.append(own)
+                        continue
+                    p = ctypes.c_void_p()
+                    _lib.call("tt_ipc_open", (ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p))
+                    ptrs.append(int(p.value))
+                    owned.append((int(p.value), True))
+            except Exception:  # noqa: BLE001
+                ok = False
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=_device.device())
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) == 0:
+            for ptr, mapped in owned:
+                try:
+                    _lib.call("tt_ipc_close" if mapped else "tt_dev_free", ptr)
+                except Exception:  # noqa: BLE001
+                    pass
+            raise _lib.LibraryError("fused data parallel: peer exchange buffers unavailable on some rank")
         xb = torch.tensor(ptrs, dtype=torch.int64, device=_device.device())
-        dist.barrier(group=group)
         return cls(est, prog, y_dev, batch, world, rank, xb, owned)
 
     @classmethod
