@@ -86,3 +86,50 @@ def test_fused_dp_matches_oracle(cuda_ok, world, batch, loss):
         assert err <= 2e-3, (name, err)
     for rk in ranks:
         rk.close()
+
+
+def test_create_over_nccl_world_one(cuda_ok):
+    """FusedDataParallelTuner.create over a real NCCL process group (world
+    size 1 on this box): the IPC allocation, handle exchange and agreement
+    collectives run, and the epoch equals the single-GPU training kernel's."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2304_05430_b200 import RecurrentAttentionTuner, _device, _lib
+    from paper_2304_05430_b200.dist import FusedDataParallelTuner
+    from paper_2304_05430_b200.estimators import _bias_corrections
+    from paper_2304_05430_b200.layout import DevicePrograms
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        rng = np.random.default_rng(4)
+        seqs = random_seqs(rng, rng.integers(1, 11, size=40))
+        y = rng.uniform(0.1, 0.9, size=40)
+        est = RecurrentAttentionTuner(epochs=0, seed=3, loss="ranking")
+        est.precision = "fp32"
+        est.fit(seqs, y)
+        prog = DevicePrograms.from_sequences(seqs, "fp32", 6, 35)
+        yd = _device.to_dev(y, torch.float32)
+        rk = FusedDataParallelTuner.create(est, prog, yd, 8)
+        perm = rng.permutation(40)
+        st = rk.run(perm, 1e-3)
+        torch.cuda.synchronize()
+        assert int(st.item()) < 0
+        dims = est._dims()
+        flat = est._dev_params(dims).clone()
+        m, v = torch.zeros_like(flat), torch.zeros_like(flat)
+        est._launch_train(dims, flat, m, v, prog, yd, _device.to_dev(perm.astype(np.int32)), 8,
+                          _lib.TT_MODE_TRAIN, 1e-3, _device.to_dev(_bias_corrections(0, 5)), None)
+        torch.cuda.synchronize()
+        assert torch.equal(rk.flat, flat)
+        rk.close()
+    finally:
+        dist.destroy_process_group()
