@@ -21,6 +21,7 @@
  */
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+#include <structmember.h>
 #define NPY_NO_DEPRECATED_API NPY_2_0_API_VERSION
 #include <numpy/arrayobject.h>
 #include <pthread.h>
@@ -89,6 +90,39 @@ static void *run_job(void *arg) {
   return NULL;
 }
 
+/* Attribute fast path: objects of one type whose `steps` / `context` are
+ * __slots__ members are read at the members' offsets (what the member
+ * descriptor would do); any other layout goes through PyObject_GetAttr. */
+typedef struct {
+  PyTypeObject *tp;
+  Py_ssize_t off_s, off_c; /* > 0: slot offsets */
+} AttrCache;
+
+static void attr_cache_init(AttrCache *c, PyObject *obj) {
+  c->tp = Py_TYPE(obj);
+  c->off_s = c->off_c = 0;
+  PyObject *d1 = _PyType_Lookup(c->tp, s_steps), *d2 = _PyType_Lookup(c->tp, s_context);
+  if (d1 && d2 && Py_IS_TYPE(d1, &PyMemberDescr_Type) && Py_IS_TYPE(d2, &PyMemberDescr_Type)) {
+    PyMemberDef *m1 = ((PyMemberDescrObject *)d1)->d_member, *m2 = ((PyMemberDescrObject *)d2)->d_member;
+    if (m1->type == Py_T_OBJECT_EX && m2->type == Py_T_OBJECT_EX) {
+      c->off_s = m1->offset;
+      c->off_c = m2->offset;
+    }
+  }
+}
+
+/* new reference or NULL (exception set) */
+static PyObject *get_attr(const AttrCache *c, PyObject *obj, PyObject *name, Py_ssize_t off) {
+  if (Py_TYPE(obj) == c->tp && off > 0) {
+    PyObject *v = *(PyObject **)((char *)obj + off);
+    if (v) {
+      Py_INCREF(v);
+      return v;
+    }
+  }
+  return PyObject_GetAttr(obj, name);
+}
+
 static void release(PyObject **held, Py_ssize_t n) {
   for (Py_ssize_t i = 0; i < n; ++i) Py_XDECREF(held[i]);
   free(held);
@@ -126,9 +160,11 @@ static PyObject *pack(PyObject *self, PyObject *args) {
   int64_t *L = (int64_t *)PyBytes_AS_STRING(lens);
   npy_intp rows = 0;
   int bad = 0;
+  AttrCache ac;
   for (Py_ssize_t i = 0; i < n && !bad; ++i) {
-    PyObject *so = held[2 * i] = PyObject_GetAttr(objs[i], s_steps);
-    PyObject *co = held[2 * i + 1] = so ? PyObject_GetAttr(objs[i], s_context) : NULL;
+    if (i == 0) attr_cache_init(&ac, objs[0]);
+    PyObject *so = held[2 * i] = get_attr(&ac, objs[i], s_steps, ac.off_s);
+    PyObject *co = held[2 * i + 1] = so ? get_attr(&ac, objs[i], s_context, ac.off_c) : NULL;
     if (!so || !co || !PyArray_Check(so) || !PyArray_Check(co)) {
       bad = 1;
       break;
