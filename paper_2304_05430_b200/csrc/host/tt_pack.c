@@ -31,6 +31,7 @@
 #include <unistd.h>
 
 static PyObject *s_steps, *s_context;
+enum { kMaxThreads = 32 }; /* conversion copy threads */
 
 static int float_type(int t) { return t == NPY_DOUBLE || t == NPY_FLOAT; }
 
@@ -227,11 +228,11 @@ static PyObject *pack(PyObject *self, PyObject *args) {
         base.ps = (char *)PyArray_DATA(os);
         base.pc = (char *)PyArray_DATA(oc);
         long ncpu = sysconf(_SC_NPROCESSORS_ONLN);
-        int nth = (int)(ncpu < 1 ? 1 : ncpu > 8 ? 8 : ncpu);
+        int nth = (int)(ncpu < 1 ? 1 : ncpu > kMaxThreads ? kMaxThreads : ncpu);
         if (n < 4096) nth = 1;
-        Job jobs[8];
-        pthread_t tids[8];
-        int started[8] = {0};
+        Job jobs[kMaxThreads];
+        pthread_t tids[kMaxThreads];
+        int started[kMaxThreads] = {0};
         Py_BEGIN_ALLOW_THREADS
         for (int t = 0; t < nth; ++t) {
           jobs[t] = base;
