@@ -276,6 +276,11 @@ __global__ void __launch_bounds__(kMT, 1) mlp_train_kernel(MlpTrainArgs<R> a) {
 // the pre-update W3 / W2; then every gradient entry is formed by a
 // fixed-order sum over the rows and immediately applied by the fused Adam
 // update (or written out in gradient mode).  Deterministic: no atomics.
+__device__ long long g_mlp_prof[16];  // tt_debug_mlp_phase_times
+#define MLP_MARK(i) \
+  do {                                                   \
+    if (step == 64 && threadIdx.x == 0) g_mlp_prof[i] = clock64(); \
+  } while (0)
 constexpr int kMB = 16;   // rows per minibatch of this kernel
 constexpr int kMT2 = 512; // its threads
 
@@ -313,6 +318,52 @@ __device__ __forceinline__ void cp_async4_mlp(float* s, const float* g) {
 }
 
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// Pairwise logistic loss of a <= 16-row minibatch (mlp.py:25-35), one pair
+// per thread: warp k owns row k, lane j the pair (k, j); the same per-pair
+// terms as rank_loss_block, summed in a fixed shuffle / row order.  `red`
+// needs 66 floats.  Returns the loss in every thread.
+__device__ float mlp_rank_loss(const float* y, const float* s, int n, float* dscore, float* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < n) {
+    const float yk = y[warp], sk = s[warp];
+    float d = 0.f, part = 0.f, pairs = 0.f;
+    if (lane < n) {
+      const float yj = y[lane], sj = s[lane];
+      if (yj > yk) d = 1.f / (1.f + Act<float>::exp(sj - sk));
+      if (yk > yj) {
+        const float mg = sk - sj;
+        d -= 1.f / (1.f + Act<float>::exp(mg));
+        part = Act<float>::softplus(-mg);
+        pairs = 1.f;
+      }
+    }
+    d = warp_sum(d);
+    part = warp_sum(part);
+    pairs = warp_sum(pairs);
+    if (lane == 0) {
+      dscore[warp] = d;
+      red[warp] = part;
+      red[32 + warp] = pairs;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tp = 0.f, np = 0.f;
+    for (int k = 0; k < n; ++k) {
+      tp += red[k];
+      np += red[32 + k];
+    }
+    red[64] = tp;
+    red[65] = np;
+  }
+  __syncthreads();
+  const float np = red[65];
+  if ((int)threadIdx.x < n) dscore[threadIdx.x] = np == 0.f ? 0.f : dscore[threadIdx.x] / np;
+  const float loss = np == 0.f ? 0.f : red[64] / np;
+  __syncthreads();
+  return loss;
+}
 
 // optim.py:33-46 in fp32 with one division per parameter: the bias
 // corrections are applied as precomputed reciprocals and the denominator's
@@ -410,6 +461,7 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
     const float* X = smf + L.x + (step & 1) * xf;
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
+    MLP_MARK(0);
     for (int k = tid; k < bn; k += kMT2) ys[k] = yr[(step & 1) * kMB + k];
     stage_order(step + 2);  // overlaps this step
     stage_rows(step + 1);
@@ -454,6 +506,7 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
       for (int i = 0; i < 2; ++i) H2[(2 * rq + i) * kW + c] = Act<float>::tanh(acc[i] + P[o.b2 + c]);
     }
     __syncthreads();
+    MLP_MARK(1);
     // out[r] = H2[r] . W3 + b3: warp w < bn / 2 handles rows 2w, 2w + 1 (lane halves)
     if (tid < 8 * 32) {
       const int r = (tid >> 5) * 2 + (lane >> 4), q = lane & 15;
@@ -467,8 +520,10 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
       if (q == 0 && r < bn) out[r] = s + P[o.b3];
     }
     __syncthreads();
-    const float loss = a.loss_kind == TT_LOSS_RANK ? rank_loss_block<float>(ys, out, bn, dsc, red)
+    MLP_MARK(2);
+    const float loss = a.loss_kind == TT_LOSS_RANK ? mlp_rank_loss(ys, out, bn, dsc, red)
                                                    : mse_block<float>(ys, out, bn, dsc, red);
+    MLP_MARK(3);
     if (tid == 0) a.step_loss[step] = loss;
     if (!isfinite(loss)) {
       if (tid == 0) a.status[0] = step;
@@ -493,6 +548,7 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
       D1[i] = r < bn ? s * (1.f - h * h) : 0.f;
     }
     __syncthreads();
+    MLP_MARK(4);
     // ---- gradients (4x4 register tiles, rows in order) + fused Adam
     const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
     const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;
@@ -530,6 +586,7 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
           for (int j = 0; j < 4; ++j) apply(o.W2 + (int64_t)(k0 + i) * kW + c0 + j, g[i][j]);
       }
     }
+    MLP_MARK(5);
     // biases and W3 (rows in order)
     for (int i = tid; i < 3 * kW + 1; i += kMT2) {
       float g = 0.f;
@@ -550,6 +607,7 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
       apply(p, g);
     }
     __syncthreads();
+    MLP_MARK(6);
   }
   if (a.mode == TT_MODE_TRAIN)
     for (int64_t p = tid; p < o.total; p += kMT2) {
@@ -654,6 +712,12 @@ int tt_mlp_predict_f32(const float* prm, const float* X, int64_t n, int32_t F, f
 int tt_mlp_predict_f64(const double* prm, const double* X, int64_t n, int32_t F, double* out,
                        tt_stream_t st) {
   return mlp_predict<double>(prm, X, n, F, out, st);
+}
+
+int tt_debug_mlp_phase_times(int64_t* h_out, int32_t n) {
+  TT_REQUIRE(h_out != nullptr && n >= 0 && n <= 16, "debug: bad arguments");
+  TT_CUDA(cudaMemcpyFromSymbol(h_out, g_mlp_prof, (size_t)n * sizeof(long long)));
+  return TT_OK;
 }
 
 size_t tt_mlp_train_workspace_bytes(int32_t f64, int32_t F, int32_t B) {

@@ -38,3 +38,12 @@ for F, n in ((164, 65536), (47, 65536)):
     dev = min(ts)
     print(f"F={F}: device {n / dev:,.0f} samples/s ({dev / steps * 1e6:.2f} us per Adam step); "
           f"fit() wall {n / wall:,.0f} samples/s")
+
+# per-phase clock64 marks of minibatch 64 of the last launch (1965 MHz)
+import ctypes  # noqa: E402
+
+buf = (ctypes.c_int64 * 7)()
+_lib.load().tt_debug_mlp_phase_times(buf, 7)
+mk = list(buf)
+names = ["stage+fwd", "out", "loss", "D2/D1", "W tiles+Adam", "bias/W3+Adam"]
+print("phases (us):", ", ".join(f"{nm}={(mk[i + 1] - mk[i]) / 1965.0:.2f}" for i, nm in enumerate(names)))
