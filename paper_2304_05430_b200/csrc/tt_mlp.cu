@@ -538,12 +538,17 @@ __global__ void __launch_bounds__(kMT2, 1) mlp_train_smem_kernel(MlpTrainArgs<fl
     __syncthreads();
     for (int i = tid; i < kMB * kW; i += kMT2) {
       const int r = i / kW, k = i % kW;
-      float s = 0.f;
-      // lane-rotated column order: W2 row k is read without bank conflicts
-      for (int t = 0; t < kW; ++t) {
-        const int cc = (t + lane) & (kW - 1);
-        s = fmaf(D2[r * kW + cc], P[o.W2 + k * kW + cc], s);
+      // lane-rotated column order: W2 row k is read without bank conflicts;
+      // two independent halves, added in a fixed order
+      float s0 = 0.f, s1 = 0.f;
+      const float* d2r = D2 + r * kW;
+      const float* w2r = P + o.W2 + k * kW;
+      for (int t = 0; t < kW / 2; ++t) {
+        const int c0 = (t + lane) & (kW - 1), c1 = (t + kW / 2 + lane) & (kW - 1);
+        s0 = fmaf(d2r[c0], w2r[c0], s0);
+        s1 = fmaf(d2r[c1], w2r[c1], s1);
       }
+      const float s = s0 + s1;
       const float h = H1[i];
       D1[i] = r < bn ? s * (1.f - h * h) : 0.f;
     }
