@@ -43,31 +43,47 @@ __device__ __forceinline__ void adam_update(R& p, R g, R& m, R& v, const AdamHyp
 // sum is reduced in a fixed tree order.  `red` must hold blockDim.x values.
 template <typename R>
 __device__ R rank_loss_block(const R* y, const R* s, int n, R* dscore, R* red) {
-  if (n <= 32) {
-    // one warp, shuffle reductions (fixed order): the B = 16 training case
-    if (threadIdx.x < 32) {
-      const int k = threadIdx.x;
-      R gin = 0, gout = 0, part = 0, pairs = 0;
-      if (k < n) {
-        const R yk = y[k], sk = s[k];
-        for (int j = 0; j < n; ++j) {
-          const R yj = y[j], sj = s[j];
-          if (yj > yk) gin += (R)1 / ((R)1 + Act<R>::exp(sj - sk));
-          if (yk > yj) {
-            const R mg = sk - sj;
-            gout += (R)1 / ((R)1 + Act<R>::exp(mg));
-            part += Act<R>::softplus(-mg);
-            pairs += (R)1;
-          }
+  if (n <= 32 && blockDim.x >= 32 * 4) {
+    // small minibatch (the B = 16 training case): one pair per lane, rows
+    // k = warp, warp + W, ..; per-row shuffle sums, rows summed in order.
+    // `red` needs 2 n + 2 values.
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, W = blockDim.x >> 5;
+    for (int k = warp; k < n; k += W) {
+      const R yk = y[k], sk = s[k];
+      R d = 0, part = 0, pairs = 0;
+      if (lane < n) {
+        const R yj = y[lane], sj = s[lane];
+        if (yj > yk) d = (R)1 / ((R)1 + Act<R>::exp(sj - sk));
+        if (yk > yj) {
+          const R mg = sk - sj;
+          d -= (R)1 / ((R)1 + Act<R>::exp(mg));
+          part = Act<R>::softplus(-mg);
+          pairs = (R)1;
         }
       }
+      d = warp_sum(d);
       part = warp_sum(part);
       pairs = warp_sum(pairs);
-      if (k < n) dscore[k] = pairs == (R)0 ? (R)0 : (gin - gout) / pairs;
-      if (k == 0) red[0] = pairs == (R)0 ? (R)0 : part / pairs;
+      if (lane == 0) {
+        dscore[k] = d;
+        red[k] = part;
+        red[n + k] = pairs;
+      }
     }
     __syncthreads();
-    const R out = red[0];
+    if (threadIdx.x == 0) {
+      R tp = 0, np = 0;
+      for (int k = 0; k < n; ++k) {
+        tp += red[k];
+        np += red[n + k];
+      }
+      red[2 * n] = tp;
+      red[2 * n + 1] = np;
+    }
+    __syncthreads();
+    const R np = red[2 * n + 1];
+    if ((int)threadIdx.x < n) dscore[threadIdx.x] = np == (R)0 ? (R)0 : dscore[threadIdx.x] / np;
+    const R out = np == (R)0 ? (R)0 : red[2 * n] / np;
     __syncthreads();
     return out;
   }
