@@ -1532,6 +1532,50 @@ __device__ float fast_rank_loss(const float* y, const float* s, int n, float* ds
   return loss;
 }
 
+// Minibatches of <= 16: one pair (k, j) per thread (k = tid / 16, j =
+// tid % 16), row sums by half-warp shuffles, the row totals by one warp --
+// the same per-pair terms as fast_rank_loss in a fixed order.  red >= 48.
+__device__ float fast_rank_loss16(const float* y, const float* s, int n, float* dscore, float* red) {
+  const int tid = threadIdx.x, k = tid >> 4, j = tid & 15;
+  float d = 0.f, part = 0.f, pairs = 0.f;
+  if (k < n && j < n) {
+    const float yk = y[k], sk = s[k], yj = y[j], sj = s[j];
+    if (yj > yk) d = 1.f / (1.f + Act<float>::exp(sj - sk));
+    if (yk > yj) {
+      const float mg = sk - sj;
+      d -= 1.f / (1.f + Act<float>::exp(mg));
+      part = Act<float>::softplus(-mg);
+      pairs = 1.f;
+    }
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    part += __shfl_xor_sync(0xffffffffu, part, o);
+    pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
+  }
+  if (j == 0 && k < 16) {
+    red[k] = d;
+    red[16 + k] = part;
+    red[32 + k] = pairs;
+  }
+  __syncthreads();
+  __shared__ float s_l;
+  if (tid < 32) {
+    float tp = tid < n ? red[16 + tid] : 0.f, np = tid < n ? red[32 + tid] : 0.f;
+    const float dk = tid < n ? red[tid] : 0.f;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      tp += __shfl_xor_sync(0xffffffffu, tp, o);
+      np += __shfl_xor_sync(0xffffffffu, np, o);
+    }
+    if (tid < n) dscore[tid] = np == 0.f ? 0.f : dk / np;
+    if (tid == 0) s_l = np == 0.f ? 0.f : tp / np;
+  }
+  __syncthreads();
+  return s_l;
+}
+
 // Multi-round mode: the pair terms of this CTA's own slots only (rows
 // k = r, r + G, ..; warp per row, lanes sweep j), unnormalised dscore into
 // smem and the row's (loss part, pair count) into the global partials.
@@ -1774,7 +1818,8 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_fast_kernel(FastArgs 
         __syncthreads();
       } else {
         loss = a.loss_kind == TT_LOSS_RANK
-                   ? fast_rank_loss(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red)
+                   ? (bn <= 16 ? fast_rank_loss16(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red)
+                               : fast_rank_loss(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red))
                    : mse_block<float>(lb, lb + bn, bn, lb + 2 * bn, sm + a.sl.red);
       }
       if (tid == 0) {
