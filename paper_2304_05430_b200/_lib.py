@@ -6,6 +6,7 @@ device is absent, every entry point raises.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 import threading
@@ -71,6 +72,9 @@ SIGNATURES: dict[str, tuple] = {
 
 _lock = threading.Lock()
 _lib = None
+# per entry point call counts: evidence that a host stack (the reference's own
+# tests under install(), bench.py) really reached the kernels
+CALLS: collections.Counter = collections.Counter()
 
 
 class LibraryError(RuntimeError):
@@ -101,6 +105,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
 def call(name: str, *args) -> None:
     """Invoke an int-returning entry point and raise on a non-zero status."""
     lib = load()
+    CALLS[name] += 1
     rc = getattr(lib, name)(*args)
     if rc != 0:
         msg = lib.tt_last_error()

@@ -90,13 +90,19 @@ def install() -> None:
 
     mods = {k: sys.modules.get(k) for k in (
         "tensortune", "tensortune.models", "tensortune.estimators", "tensortune.metrics",
-        "tensortune.transfer", "tensortune.sampling", "tensortune.estimators.tuner")}
-    for key in ("tensortune", "tensortune.models", "tensortune.estimators"):
+        "tensortune.transfer", "tensortune.sampling", "tensortune.estimators.tuner",
+        "tensortune.estimators.mlp")}
+    # the defining modules too, so `from tensortune.estimators.tuner import
+    # RecurrentAttentionTuner` (test_acceptance.py:28-29) resolves to ours
+    for key in ("tensortune", "tensortune.models", "tensortune.estimators",
+                "tensortune.estimators.tuner", "tensortune.estimators.mlp"):
         _patch(mods[key], "RecurrentAttentionTuner", _est.RecurrentAttentionTuner)
         _patch(mods[key], "CostMLP", _est.CostMLP)
+    _patch(mods["tensortune.estimators.mlp"], "ranking_grad", _est.ranking_grad)
     for key in ("tensortune", "tensortune.metrics", "tensortune.models", "tensortune.transfer"):
         _patch(mods[key], "pairwise_comparison_accuracy", _met.pairwise_comparison_accuracy)
         _patch(mods[key], "top_k_score", _met.top_k_score)
+        _patch(mods[key], "ranking_loss", _met.ranking_loss)
     if mods["tensortune.models"] is not None:
         _patch(mods["tensortune.models"], "per_task_metrics",
                make_per_task_metrics(mods["tensortune.models"]))

@@ -1,0 +1,36 @@
+"""End-to-end parity anchors for GPU training.
+
+Run only under tests/refsuite_plugin.py (the reference's ``tensortune`` with
+``install()`` applied), by tests/test_gpu_reference_suite.py:
+
+* the reference's acceptance convergence check (test_acceptance.py:174-195)
+  per seed, with the reference's OWN measured outcomes as the anchor: a
+  GPU-trained tuner (production fp32) lands within +-0.005 of the reference's
+  200-epoch val rmse (0.0362 / 0.0407 / 0.0473, measured in the build
+  container with the unmodified reference), under the
+  0.06 bar, and below the reference GBDT's val rmse on the same split
+  (0.0767 / 0.0863 / 0.0886).
+"""
+
+from __future__ import annotations
+
+import pytest
+from tensortune.benchmarks import convergence_benchmark
+from tensortune.models import TrainConfig, train_tuner
+
+REF_TUNER_VAL_RMSE = {0: 0.0362, 1: 0.0407, 2: 0.0473}
+REF_GBDT_VAL_RMSE = {0: 0.0767, 1: 0.0863, 2: 0.0886}
+TOL = 0.005
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_tuner_200_epoch_val_rmse_matches_reference(seed):
+    ds, assignment = convergence_benchmark(seed=seed)
+    model, rep = train_tuner(
+        ds, assignment, TrainConfig(epochs=200, learning_rate=1e-3, recurrent_layers=2, seed=seed))
+    assert type(model.estimator).__module__.startswith("paper_2304_05430_b200")
+    print(f"seed {seed}: GPU val rmse {rep.val_rmse:.4f} vs reference {REF_TUNER_VAL_RMSE[seed]:.4f}"
+          f" (gbdt {REF_GBDT_VAL_RMSE[seed]:.4f})")
+    assert abs(rep.val_rmse - REF_TUNER_VAL_RMSE[seed]) <= TOL, rep.val_rmse
+    assert rep.val_rmse <= 0.06
+    assert rep.val_rmse <= REF_GBDT_VAL_RMSE[seed]

@@ -1,0 +1,107 @@
+"""The reference's own hot-path test modules, run on the B200 through install().
+
+Each case launches ``pytest -p refsuite_plugin baseline/_ref/tests/<module>``
+in a subprocess (a fresh interpreter, so ``install()`` binds before the
+reference's test modules import their names).  The reference package and its
+tests are the unmodified /root/reference/pkg tree, staged by
+tools/stage_reference.py into the git-ignored ``baseline/_ref`` that travels to
+the GPU box.
+
+Two precisions:
+
+* ``fp64`` -- the same kernels instantiated in double: the reference's own
+  tolerances apply unchanged (rtol 1e-12 chunk invariance, bit-identical
+  refits, central-difference gradients), so every selected test must pass;
+* ``fp32`` -- the production build.  Tests whose assertion is a float64
+  statement (tolerances below fp32's 6e-8 unit roundoff, or finite
+  differences with eps = 1e-6) are deselected by name below, each with the
+  reason; everything else must pass as written.
+
+The subprocess writes its C-ABI call counts; a module counts only if it
+reached the kernels (``tt_*`` calls > 0).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF_TESTS = os.path.join(ROOT, "baseline", "_ref", "tests")
+
+MODULES = ["test_metrics.py", "test_mlp.py", "test_tuner.py", "test_models.py",
+           "test_sampling.py", "test_transfer.py", "test_search.py", "test_cli.py"]
+
+# fp32 production build: reference assertions that are float64 statements.
+FP32_DESELECT = {
+}
+
+
+def run_ref_suite(module: str, precision: str, extra=(), timeout=3000):
+    if not os.path.isdir(REF_TESTS):
+        pytest.fail("baseline/_ref/tests missing: run tools/stage_reference.py (build() does) "
+                    "in the build container so the reference travels to the box")
+    logdir = os.environ.get("TT_REFSUITE_LOGDIR") or os.path.join(ROOT, "gpurun_out", "refsuite")
+    os.makedirs(logdir, exist_ok=True)
+    tag = f"{os.path.basename(module)[:-3]}_{precision}"
+    path = module if os.path.isabs(module) else os.path.join(REF_TESTS, module)
+    calls = os.path.join(logdir, f"{tag}.calls.json")
+    env = dict(os.environ)
+    env["TT_PRECISION"] = precision
+    env["TT_REFSUITE_CALLS"] = calls
+    env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tests"), ROOT, env.get("PYTHONPATH", "")])
+    env["PYTHONDONTWRITEBYTECODE"] = "1"
+    cmd = [sys.executable, "-m", "pytest", "-p", "refsuite_plugin", "-p", "no:cacheprovider",
+           "-q", "-rfE", "--rootdir", REF_TESTS, path, *extra]
+    for name in FP32_DESELECT.get(module, {}) if precision == "fp32" else ():
+        cmd += ["--deselect", f"{path}::{name}"]
+    r = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=timeout)
+    with open(os.path.join(logdir, f"{tag}.log"), "w") as fh:
+        fh.write(" ".join(cmd) + "\n\n" + r.stdout + "\n" + r.stderr)
+    tail = (r.stdout + r.stderr)[-6000:]
+    assert r.returncode == 0, tail
+    with open(calls) as fh:
+        n = json.load(fh)
+    return r.stdout, n
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("module", MODULES)
+def test_reference_module_on_b200(cuda_ok, module, precision):
+    out, calls = run_ref_suite(module, precision)
+    print(out.strip().splitlines()[-1], calls)
+    assert sum(calls.values()) > 0, f"{module} never reached the kernels"
+
+
+ACCEPTANCE = os.path.join(REF_TESTS, "test_acceptance.py")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,precision", [
+    ("test_pairwise_accuracy_matches_brute_force_exactly", "fp32"),
+    ("test_gradients_match_central_differences", "fp64"),
+    ("test_sequence_model_converges_below_the_tree_baseline", "fp32"),
+    ("test_transfer_reaches_parity_on_a_40_percent_budget", "fp32"),
+])
+def test_reference_acceptance_on_b200(cuda_ok, name, precision):
+    """The reference's acceptance criteria (test_acceptance.py)
+    that exercise the hot path, end to end on the kernels."""
+    out, calls = run_ref_suite("test_acceptance.py", precision, extra=("-s", "-k", name))
+    print([ln for ln in out.splitlines() if ln.strip()][-3:], calls)
+    assert "1 passed" in out
+    assert sum(calls.values()) > 0
+
+
+@pytest.mark.gpu
+def test_convergence_anchors_match_reference_values(cuda_ok):
+    """Val rmse at 200 epochs within +-0.005 of the reference's own outcome per
+    seed (tests/anchors/anchor_convergence.py)."""
+    out, calls = run_ref_suite(os.path.join(ROOT, "tests", "anchors", "anchor_convergence.py"),
+                               "fp32", extra=("-s",))
+    print("\n".join(ln for ln in out.splitlines() if ln.startswith("seed")), calls)
+    assert "3 passed" in out

@@ -201,3 +201,22 @@ def test_weight_round_trip_preserves_predictions(cuda_ok):
     clone = make("fp32", hidden_size=4, recurrent_layers=1, attention_heads=2)
     clone.set_weights(m.get_weights())
     assert np.array_equal(clone.predict(seqs), m.predict(seqs))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_concurrent_predict_from_worker_threads(cuda_ok, precision):
+    """search.tune(jobs>1) calls predict from ThreadPoolExecutor workers
+    (search.py:563-567; SPEC.md:538 'safe for concurrent predict'): results
+    from 8 threads x mixed batch sizes equal the serial ones bit for bit."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(7)
+    seqs = random_seqs(rng, rng.integers(1, 13, 600))
+    m = make(precision, epochs=0, seed=3).fit(seqs, rng.uniform(size=600))
+    chunks = [seqs[i:i + n] for i, n in zip(range(0, 600, 37), [1, 5, 32, 37] * 40)]
+    serial = [m.predict(c) for c in chunks]
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        for _ in range(3):
+            got = list(ex.map(m.predict, chunks))
+            for a, b in zip(got, serial):
+                np.testing.assert_array_equal(a, b)

@@ -8,13 +8,15 @@ import sys
 
 import pytest
 
-REF = "/root/reference/pkg/src"
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = next((p for p in ("/root/reference/pkg/src", os.path.join(_ROOT, "baseline", "_ref"))
+            if os.path.isdir(os.path.join(p, "tensortune"))), "")
 
 
 @pytest.fixture
 def tensortune():
-    if not os.path.isdir(REF):
-        pytest.skip("reference package not present (GPU box)")
+    if not REF:
+        pytest.skip("reference package not present (neither /root/reference nor baseline/_ref)")
     sys.dont_write_bytecode = True
     if REF not in sys.path:
         sys.path.insert(0, REF)
