@@ -195,8 +195,13 @@ int tt_tuner_train_heads_f32(float *d_params, float *d_m, float *d_v, const floa
  *     included, index = rank); buffers zeroed once (tt_ipc_alloc does).
  *   gbase: global index of this launch's first step, monotone across
  *     launches (flags carry gbase + step + 1).
- * A non-finite loss sets *d_status on the rank where it happened, but every
- * rank runs the epoch to its end (the host combines the statuses).
+ * A non-finite loss sets d_status[0] on the rank where it happened, but every
+ * rank runs the epoch to its end (the host combines the statuses).  For
+ * world > 1, d_status points at TWO int32 {first non-finite step or -1,
+ * abort word = 0}: a wait for a peer's slice longer than the timeout
+ * (tt_tuner_dp_set_timeout_ms, default 30 s) sets the abort word to 1, after
+ * which no exchange of the launch waits any more -- the epoch ends quickly
+ * with invalid parameters and the host raises, instead of hanging all ranks.
  * tt_ipc_alloc/open/close, tt_dev_free: the cudaIpc* plumbing (64-B handles).
  * tt_tuner_train_set_grid: CTAs of the latency-path launch (0 = every SM);
  * tests run several ranks concurrently on one GPU by splitting its SMs. */
@@ -216,6 +221,12 @@ int tt_ipc_open(const uint8_t *h_handle, void **d_ptr);
 int tt_ipc_close(void *d_ptr);
 int tt_dev_free(void *d_ptr);
 int tt_tuner_train_set_grid(int32_t grid);
+int tt_tuner_dp_set_timeout_ms(int64_t ms);
+/* 1 if tt_tuner_train_f32 / _dp_f32 would run these dimensions on the
+ * latency-path kernel (the data-parallel launch requires it), else 0. */
+int32_t tt_tuner_train_fast_eligible(int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                                     int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                                     int32_t batch_size);
 
 /* Kernel selection for tt_tuner_train_f32: 0 = automatic (the latency-path
  * kernel when hidden = 32, batch <= #SMs and the per-sample caches fit in

@@ -52,6 +52,8 @@ SIGNATURES: dict[str, tuple] = {
     "tt_ipc_close": (ctypes.c_int, [_P]),
     "tt_dev_free": (ctypes.c_int, [_P]),
     "tt_tuner_train_set_grid": (ctypes.c_int, [_I32]),
+    "tt_tuner_dp_set_timeout_ms": (ctypes.c_int, [_I64]),
+    "tt_tuner_train_fast_eligible": (_I32, [_I32] * 8),
     "tt_tuner_train_set_path": (ctypes.c_int, [_I32]),
     "tt_debug_profile_step": (ctypes.c_int, [_I32]),
     "tt_debug_phase_times": (ctypes.c_int, [_P, _I32]),

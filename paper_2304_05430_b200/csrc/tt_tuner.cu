@@ -326,6 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1) tuner_train_kernel(TrainArgs<R> a
 }
 
 // ------------------------------------------------------------- dispatch --
+// bound on one wait for a peer's gradient slice (tt_tuner_dp_set_timeout_ms)
+static long long g_dp_timeout_ns = 30LL * 1000000000LL;
+
 struct DpArgs {
   int world, rank;
   int64_t gbase;
@@ -480,6 +483,7 @@ struct Launch {
           f.rank = dp->rank;
           f.gbase = dp->gbase;
           f.xb = dp->xb;
+          f.dp_timeout_ns = g_dp_timeout_ns;
         }
         return fast_launch(f, fp, ws, st);
       }
@@ -696,6 +700,19 @@ int tt_ipc_close(void* d_ptr) {
 
 int tt_dev_free(void* d_ptr) {
   TT_CUDA(cudaFree(d_ptr));
+  return TT_OK;
+}
+
+int32_t tt_tuner_train_fast_eligible(int32_t L, int32_t H, int32_t heads, int32_t U, int32_t d0,
+                                     int32_t C, int32_t Tmax, int32_t B) {
+  if (check_dims(L, H, heads, U, d0, C, Tmax) != TT_OK) return 0;
+  FastPlan fp;
+  return fast_plan(make_dims(L, H, heads, U, d0, C, Tmax), B, fast_grid(), fp) ? 1 : 0;
+}
+
+int tt_tuner_dp_set_timeout_ms(int64_t ms) {
+  TT_REQUIRE(ms >= 1, "dp timeout must be >= 1 ms");
+  g_dp_timeout_ns = ms * 1000000LL;
   return TT_OK;
 }
 

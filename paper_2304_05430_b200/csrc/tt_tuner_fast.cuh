@@ -271,6 +271,7 @@ struct FastArgs {
   int64_t gbase;        // global step index of this launch's first minibatch (monotone flags)
   int64_t dp_slice;     // floats per slice slot (>= kap * nbp of every job)
   void* const* xb;      // [world] exchange buffers (fast_dp_buffer_bytes each)
+  long long dp_timeout_ns;  // bound on one wait for a peer's slice (status[1] = 1 past it)
   float* scache;       // [B][sl.red - sl.x0]: per-slot forward caches (multi-round mode)
   float* wcache;       // [grid][attn_floats]: attention/head weight image per CTA (multi-round)
   unsigned int* ctr;   // [0] fwd, [1 + g] bwd, [2 + L + g] adam, [kCtrLoss] loss (monotone)
@@ -1326,8 +1327,15 @@ __host__ __device__ inline int64_t fast_dp_buffer_bytes(int n_jobs, int world, i
 // (it needs their slices of the step in between).
 // (out of line with scalar arguments: keeps the exchange out of the
 // register allocation of the single-GPU kernel body)
+// The spin on a peer's slot is bounded: every 256 polls it checks the
+// launch's abort word (status[1]) and %globaltimer; past `timeout_ns` without
+// the peer's word it raises status[1] = 1 and stops waiting (the slot reads as
+// 0), and once the abort word is set every later exchange skips its waits, so
+// a dead or diverged peer ends the epoch quickly with an error the host
+// raises instead of hanging every rank.
 __device__ __noinline__ void fast_dp_exchange(void* const* xb, int W, int me, int64_t gs,
-                                              int64_t slice, int n_jobs, int j, float* gout, int n) {
+                                              int64_t slice, int n_jobs, int j, float* gout, int n,
+                                              int32_t* status, long long timeout_ns) {
   const int tid = threadIdx.x;
   const unsigned long long tag = (unsigned long long)(unsigned)(gs + 1) << 32;
   const int64_t base = ((gs & 1) * (int64_t)n_jobs + j) * W * slice;
@@ -1342,6 +1350,7 @@ __device__ __noinline__ void fast_dp_exchange(void* const* xb, int W, int me, in
   }
   const unsigned long long* rx = reinterpret_cast<const unsigned long long*>(xb[me]) + base;
   const float inv = 1.f / (float)W;
+  bool aborted = __ldcg(status + 1) != 0;
   for (int i = tid; i < n; i += kThreads) {
     float acc = 0.f;
     for (int p = 0; p < W; ++p) {
@@ -1349,11 +1358,23 @@ __device__ __noinline__ void fast_dp_exchange(void* const* xb, int W, int me, in
       if (p == me) {
         v = gout[i];
       } else {
-        unsigned long long w;
-        do {
+        unsigned long long w = 0;
+        unsigned long long t0 = 0;
+        for (unsigned spin = 0; !aborted; ++spin) {
           asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(w) : "l"(rx + (int64_t)p * slice + i) : "memory");
-        } while ((w & 0xffffffff00000000ull) != tag);
-        v = __uint_as_float((unsigned)w);
+          if ((w & 0xffffffff00000000ull) == tag) break;
+          if ((spin & 255) != 255) continue;
+          unsigned long long now;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+          if (t0 == 0) t0 = now;
+          if (__ldcg(status + 1) != 0) {
+            aborted = true;
+          } else if ((long long)(now - t0) > timeout_ns) {
+            atomicExch(status + 1, 1);
+            aborted = true;
+          }
+        }
+        v = aborted ? 0.f : __uint_as_float((unsigned)w);
       }
       acc += v;
     }
@@ -1430,7 +1451,8 @@ __device__ void fast_run_job(const FastArgs& a, const FastJob& jb, int jidx, int
   __syncthreads();
   if (blockIdx.x == (unsigned)(a.B % gridDim.x)) fmark_any(step, 23);
   if (a.world > 1 && a.mode == TT_MODE_TRAIN)
-    fast_dp_exchange(a.xb, a.world, a.rank, a.gbase + step, a.dp_slice, a.n_jobs, jidx, gout, kap * nbp);
+    fast_dp_exchange(a.xb, a.world, a.rank, a.gbase + step, a.dp_slice, a.n_jobs, jidx, gout, kap * nbp,
+                     a.status, a.dp_timeout_ns);
   // parameter addresses of the slice and the fused Adam update
   const double c1 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step] : 1.0;
   const double c2 = a.mode == TT_MODE_TRAIN ? a.corr[2 * step + 1] : 1.0;

@@ -59,6 +59,18 @@ def dp_steps(n: int, batch: int, world: int) -> int:
     return (n + world * batch - 1) // (world * batch)
 
 
+def global_max_int(x: int, group=None) -> int:
+    """MAX of one integer over the ranks of `group`."""
+    import torch
+    import torch.distributed as dist
+
+    v = torch.tensor([int(x)], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        v = v.cuda()
+    dist.all_reduce(v, op=dist.ReduceOp.MAX, group=group)
+    return int(v.item())
+
+
 def mean_microbatch_gradient(grad, n_local: int, group=None):
     """All-reduce (sum) the local gradient and the count of non-empty
     microbatches; returns the mean over non-empty microbatches (in place).
@@ -113,7 +125,14 @@ class DataParallelTunerEpoch:
 
         n = len(perm)
         perm_dev = self._dev.to_dev(np.asarray(perm, dtype=np.int32))
-        steps = (n + self.B - 1) // self.B if local_shard else dp_steps(n, self.B, self.world)
+        if local_shard:
+            # shards may differ in size: every rank loops to the LONGEST
+            # shard's step count (ranks past their shard contribute zero
+            # gradients and a zero count), so all ranks issue the same
+            # collectives
+            steps = global_max_int((n + self.B - 1) // self.B, self.group)
+        else:
+            steps = dp_steps(n, self.B, self.world)
         stream = self._dev.stream_ptr()
         for k in range(steps):
             lo = k * self.B if local_shard else k * self.world * self.B + self.rank * self.B
@@ -174,13 +193,14 @@ class FusedDataParallelTuner:
     one GPU (tests: the ranks run concurrently on disjoint SMs).
     """
 
-    def __init__(self, est, prog, y_dev, batch: int, world: int, rank: int, xb, owned):
+    def __init__(self, est, prog, y_dev, batch: int, world: int, rank: int, xb, owned, group=None):
         import torch
 
         from . import _device
 
         self.est, self.prog, self.y, self.B = est, prog, y_dev, batch
         self.world, self.rank = world, rank
+        self.group = group  # torch.distributed group (create) or None (local_group)
         self.dims = est._dims()
         self.flat = est._dev_params(self.dims).clone()
         self.m = torch.zeros_like(self.flat)
@@ -255,7 +275,7 @@ class FusedDataParallelTuner:
                     pass
             raise _lib.LibraryError("fused data parallel: peer exchange buffers unavailable on some rank")
         xb = torch.tensor(ptrs, dtype=torch.int64, device=_device.device())
-        return cls(est, prog, y_dev, batch, world, rank, xb, owned)
+        return cls(est, prog, y_dev, batch, world, rank, xb, owned, group=group)
 
     @classmethod
     def local_group(cls, ests, progs, ys, batch: int):
@@ -271,16 +291,55 @@ class FusedDataParallelTuner:
         return [cls(e, p, y, batch, world, r, xb, [(bufs[r], False)])
                 for r, (e, p, y) in enumerate(zip(ests, progs, ys))]
 
+    def preconditions(self, n: int) -> tuple[int, int, int]:
+        """(steps of this launch, global step base, latency-path eligible):
+        every rank's kernel waits on its peers' slices for every step, so
+        these must agree across ranks before anything is launched."""
+        from . import _lib
+
+        d = self.dims
+        ok = _lib.load().tt_tuner_train_fast_eligible(d["L"], d["H"], d["heads"], d["U"], d["d0"],
+                                                       d["C"], self.prog.max_steps, self.B)
+        return (n + self.B - 1) // self.B, self.gstep, int(ok)
+
+    def _agree(self, pre: tuple[int, int, int]) -> None:
+        """All-reduce the preconditions (MIN and MAX in one MAX collective)
+        and raise LibraryError on EVERY rank if any rank differs or is not
+        eligible, so no rank launches a kernel its peers would wait on."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if self.group is None or not dist.is_initialized():
+            return
+        v = torch.tensor(list(pre) + [-x for x in pre], dtype=torch.int64)
+        if dist.get_backend(self.group) == "nccl":
+            v = v.to(self._dev.device())
+        dist.all_reduce(v, op=dist.ReduceOp.MAX, group=self.group)
+        v = v.cpu().tolist()
+        hi, lo = v[:3], [-x for x in v[3:]]
+        if hi != lo or lo[2] != 1:
+            raise _lib.LibraryError(
+                f"fused data parallel: ranks disagree or are not eligible "
+                f"(steps {lo[0]}..{hi[0]}, step base {lo[1]}..{hi[1]}, eligible min {lo[2]}); "
+                "every rank needs an equal-size shard, the same step count so far and programs "
+                "the latency-path kernel accepts")
+
     def run(self, perm: np.ndarray, lr: float):
         """Enqueue one epoch over this rank's shard in the order `perm` (equal
         length on every rank) on the current stream; returns the device
-        status (>= 0: first non-finite step on this rank)."""
+        status [first non-finite step or -1, abort word] (check_status)."""
         from . import _lib
         from .estimators import _BETA1, _BETA2, _EPS, _bias_corrections
 
         d, est, prog = self.dims, self.est, self.prog
         n = len(perm)
-        n_steps = (n + self.B - 1) // self.B
+        pre = self.preconditions(n)
+        self._agree(pre)
+        if pre[2] != 1:
+            raise _lib.LibraryError("fused data parallel: not eligible for the latency-path kernel")
+        n_steps = pre[0]
         lib = _lib.load()
         nbytes = lib.tt_tuner_train_workspace_bytes(0, d["L"], d["H"], d["d0"], d["C"], prog.max_steps,
                                                     self.B)
@@ -288,7 +347,7 @@ class FusedDataParallelTuner:
         order = self._dev.to_dev(np.asarray(perm, dtype=np.int32))
         corr = self._dev.to_dev(_bias_corrections(self.gstep, n_steps))
         self.step_loss = self._dev.empty(n_steps, self.flat.dtype)
-        status = self._dev.to_dev(np.array([-1], dtype=np.int32))
+        status = self._dev.to_dev(np.array([-1, 0], dtype=np.int32))
         loss_kind = _lib.TT_LOSS_RANK if est.loss == "ranking" else _lib.TT_LOSS_MSE
         _lib.call("tt_tuner_train_dp_f32", self.flat.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
                   prog.steps.data_ptr(), prog.offsets.data_ptr(), prog.ctx.data_ptr(), self.y.data_ptr(),
@@ -300,6 +359,18 @@ class FusedDataParallelTuner:
         self.gstep += n_steps
         self._keep = (order, corr)  # alive until the launch completes
         return status
+
+    @staticmethod
+    def check_status(status) -> int:
+        """Raise if the launch's exchange timed out waiting for a peer;
+        return the first non-finite step (-1 if none)."""
+        from . import _lib
+
+        s = status.cpu().tolist()
+        if len(s) > 1 and s[1] != 0:
+            raise _lib.LibraryError("fused data parallel: a peer did not deliver its gradient slice "
+                                    "within the timeout (dead or diverged rank); parameters are invalid")
+        return int(s[0])
 
     def close(self):
         from . import _lib

@@ -20,7 +20,9 @@ from tensortune.models import TrainConfig, train_tuner
 
 REF_TUNER_VAL_RMSE = {0: 0.0362, 1: 0.0407, 2: 0.0473}
 REF_GBDT_VAL_RMSE = {0: 0.0767, 1: 0.0863, 2: 0.0886}
-TOL = 0.005
+import os
+
+TOL = float(os.environ.get("TT_ANCHOR_TOL", "0.005"))
 
 
 @pytest.mark.parametrize("seed", [0, 1, 2])

@@ -180,3 +180,73 @@ def test_dp_buffer_size_covers_every_slot():
     assert lib.tt_tuner_dp_buffer_bytes(3, 16, 6, 35, 2) == 0  # fused path is hidden-32 only
     wide = lib.tt_tuner_dp_buffer_bytes(3, 32, 164, 35, 2)
     assert wide > two  # wider layer-0 slices
+
+
+def _unequal_worker(rank, world, port, out):
+    """Shards of 37 and 20 samples: both ranks must loop to the longer
+    shard's step count (DataParallelTunerEpoch deadlocked)."""
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2304_05430_b200 import dist as tdist
+
+    _init(rank, world, port)
+    n_local, B = (37, 20)[rank], 4
+    steps = tdist.global_max_int((n_local + B - 1) // B)
+    sums = []
+    for k in range(steps):
+        cnt = max(0, min(B, n_local - k * B))
+        g = torch.full((3,), float(cnt), dtype=torch.float64)
+        tdist.mean_microbatch_gradient(g, cnt)
+        sums.append(float(g[0]))
+    out[rank] = (steps, sums)
+    dist.destroy_process_group()
+
+
+def test_dp_unequal_local_shards_take_the_same_number_of_collectives():
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_unequal_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert out[0] == out[1]
+    steps, sums = out[0]
+    assert steps == 10
+    # steps 0-4: both ranks contribute 4; steps 5-8: only rank 0 (4); step 9: rank 0's 1
+    assert sums == [4.0] * 9 + [1.0]
+
+
+def _agree_worker(rank, world, port, pre, out):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2304_05430_b200 import _lib
+    from paper_2304_05430_b200 import dist as tdist
+
+    _init(rank, world, port)
+    r = object.__new__(tdist.FusedDataParallelTuner)
+    r.group = dist.group.WORLD
+    try:
+        r._agree(tuple(pre[rank]))
+        out[rank] = "ok"
+    except _lib.LibraryError as exc:
+        out[rank] = "raised: " + str(exc)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("pre,ok", [
+    ([(10, 0, 1), (10, 0, 1)], True),
+    ([(10, 0, 1), (9, 0, 1)], False),    # a shorter shard
+    ([(10, 5, 1), (10, 0, 1)], False),   # diverged global step base
+    ([(10, 0, 1), (10, 0, 0)], False),   # one rank holds a program too long for the kernel
+])
+def test_fused_dp_preconditions_agree_or_raise_on_every_rank(pre, ok):
+    """a rank that cannot launch (or launches fewer steps) must not
+    leave its peers spinning in the exchange -- all ranks raise together."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_agree_worker, args=(world, _free_port(), pre, out), nprocs=world, join=True)
+    if ok:
+        assert out[0] == out[1] == "ok"
+    else:
+        assert out[0].startswith("raised") and out[1].startswith("raised")
