@@ -34,6 +34,12 @@ static PyObject *s_steps, *s_context;
 enum { kMaxThreads = 32 }; /* conversion copy threads */
 
 static int float_type(int t) { return t == NPY_DOUBLE || t == NPY_FLOAT; }
+/* a source array the raw copy loops may read: float32/64 in native byte order
+ * and aligned (anything else -- '>f8', unaligned views -- makes pack() return
+ * None so the numpy path converts it) */
+static int readable_src(PyArrayObject *a) {
+  return float_type(PyArray_TYPE(a)) && PyArray_ISNOTSWAPPED(a) && PyArray_ISALIGNED(a);
+}
 
 /* one strided float source block (rows x cols) */
 typedef struct {
@@ -132,7 +138,8 @@ static void release(PyObject **held, Py_ssize_t n) {
 static int out_ok(PyObject *o, npy_intp need) {
   if (!PyArray_Check(o)) return 0;
   PyArrayObject *a = (PyArrayObject *)o;
-  return float_type(PyArray_TYPE(a)) && PyArray_IS_C_CONTIGUOUS(a) && PyArray_ISWRITEABLE(a) &&
+  return float_type(PyArray_TYPE(a)) && PyArray_ISNOTSWAPPED(a) && PyArray_IS_C_CONTIGUOUS(a) &&
+         PyArray_ISWRITEABLE(a) &&
          PyArray_SIZE(a) >= need;
 }
 
@@ -174,8 +181,8 @@ static PyObject *pack(PyObject *self, PyObject *args) {
     if (d0 < 0 && PyArray_NDIM(sa) == 2) d0 = PyArray_DIM(sa, 1);
     if (C < 0 && PyArray_NDIM(ca) == 1) C = PyArray_DIM(ca, 0);
     if (PyArray_NDIM(sa) != 2 || PyArray_DIM(sa, 1) != d0 || PyArray_DIM(sa, 0) < 1 ||
-        !float_type(PyArray_TYPE(sa)) || PyArray_NDIM(ca) != 1 || PyArray_DIM(ca, 0) != C ||
-        !float_type(PyArray_TYPE(ca))) {
+        !readable_src(sa) || PyArray_NDIM(ca) != 1 || PyArray_DIM(ca, 0) != C ||
+        !readable_src(ca)) {
       bad = 1;
       break;
     }

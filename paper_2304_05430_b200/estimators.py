@@ -27,7 +27,7 @@ from sklearn.base import BaseEstimator, RegressorMixin
 from . import _device, _lib, config
 from .errors import DataValidationError, NumericFailure
 from .layout import DevicePrograms
-from .metrics import group_offsets, pca_counts, pca_from_counts
+from .metrics import _as_pair, group_offsets, pca_counts, pca_from_counts
 from .metrics import ranking_grad as _ranking_grad_gpu
 
 HEAD_HIDDEN = 64
@@ -441,6 +441,11 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
                 _, status, _ = self._launch_train(dims, flat, m, v, prog, y_dev, _device.to_dev(perm), B,
                                                   _lib.TT_MODE_TRAIN, float(learning_rate), corr, mask)
             if int(status.item()) >= 0:
+                # the kernel stopped at the failing minibatch (no update from
+                # it on): keep the state of the last finite step, as the
+                # reference's in-place Adam does (tuner.py:449-450)
+                _unflatten_into(self.__dict__["_host"], dims["names"], flat.cpu().double().numpy())
+                self._devp().invalidate()
                 raise NumericFailure(f"loss became non-finite at epoch {epoch}")
             t_step += n_steps
             pred = self._predict_programs(prog, dims, flat).cpu().double().numpy()
@@ -453,6 +458,8 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
                 if gperm is not None:
                     sizes = np.diff(goff)
                     if np.any(sizes >= 2):
+                        ranked = np.repeat(sizes >= 2, sizes)  # tuner.py:486-496 -> _as_pair
+                        _as_pair(ey[gperm][ranked], vp[gperm][ranked], min_n=0)
                         vals = pca_from_counts(pca_counts(ey[gperm], vp[gperm], goff), goff)
                         val_pca = float(np.mean([float(x) for x, s in zip(vals, sizes) if s >= 2]))
             self.train_curve_.append((train_rmse, val_rmse, val_pca))
@@ -607,6 +614,9 @@ class CostMLP(_GpuParamsMixin, BaseEstimator, RegressorMixin):
             _, status, _ = self._launch_train(flat, m, v, Xd, yd, F, _device.to_dev(perm), B,
                                               _lib.TT_MODE_TRAIN, float(self.learning_rate), corr)
             if int(status.item()) >= 0:
+                # state of the last finite step (mlp.py:136-137, in-place Adam)
+                _unflatten_into(self.__dict__["_host"], list(self.NAMES), flat.cpu().double().numpy())
+                self._devp().invalidate()
                 raise NumericFailure(f"loss became non-finite at epoch {epoch}")
             t_step += n_steps
             pred = self._predict_dev(Xd, n, F, flat).cpu().double().numpy()

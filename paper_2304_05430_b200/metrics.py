@@ -99,6 +99,11 @@ def grouped_pca(y, y_hat, groups) -> float | None:
     sizes = np.diff(off)
     if not np.any(sizes >= 2):
         return None
+    # the reference validates every group of >= 2 members through
+    # pairwise_comparison_accuracy (_as_pair): a NaN score there raises
+    # DataValidationError instead of entering the rank sort
+    ranked = np.repeat(sizes >= 2, sizes)
+    _as_pair(y[perm][ranked], y_hat[perm][ranked], min_n=0)
     vals = segmented_pca(y[perm], y_hat[perm], off)
     scores = [float(v) for v, s in zip(vals, sizes) if s >= 2]
     return float(np.mean(scores))

@@ -107,3 +107,17 @@ def test_rank_loss_golden(cuda_ok):
     for (y, s), want in zip(segments(g["y"], g["s"], g["offsets"]), g["loss"]):
         l, d = oloss.pairwise_logistic(y, s)
         assert l == pytest.approx(want, rel=1e-13)
+
+
+def test_grouped_pca_rejects_non_finite_scores_like_the_reference(cuda_ok):
+    """NaN in a group of >= 2 raises DataValidationError (the
+    reference's pairwise_comparison_accuracy -> _as_pair); a NaN in a singleton
+    group is never validated by the reference either."""
+    from paper_2304_05430_b200 import grouped_pca
+    from paper_2304_05430_b200.errors import DataValidationError
+
+    y = np.array([0.1, 0.2, 0.3, 0.4, 0.5])
+    s = np.array([0.1, np.nan, 0.3, 0.2, np.inf])
+    with pytest.raises(DataValidationError, match="finite"):
+        grouped_pca(y, s, ["a", "a", "b", "b", "c"])
+    assert grouped_pca(y, s, ["c", "d", "b", "b", "e"]) == 0.0

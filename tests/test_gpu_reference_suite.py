@@ -84,7 +84,7 @@ def run_ref_suite(module: str, precision: str, extra=(), timeout=3000):
     cmd = [sys.executable, "-m", "pytest", "-p", "refsuite_plugin", "-p", "no:cacheprovider",
            "-q", "-rfE", "--rootdir", REF_TESTS, path, *extra]
     for name in DESELECT[precision].get(os.path.basename(module), {}):
-        cmd += ["--deselect", f"{path}::{name}"]
+        cmd += ["--deselect", f"{os.path.relpath(path, REF_TESTS)}::{name}"]
     r = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True, timeout=timeout)
     with open(os.path.join(logdir, f"{tag}.log"), "w") as fh:
         fh.write(" ".join(cmd) + "\n\n" + r.stdout + "\n" + r.stderr)

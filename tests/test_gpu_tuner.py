@@ -220,3 +220,32 @@ def test_concurrent_predict_from_worker_threads(cuda_ok, precision):
             got = list(ex.map(m.predict, chunks))
             for a, b in zip(got, serial):
                 np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision,kw,tol", [
+    ("fp64", dict(hidden_size=4, recurrent_layers=1), 1e-9),
+    ("fp32", dict(), 2e-3),   # latency-path kernel (hidden 32); relative norm per tensor
+])
+def test_numeric_failure_keeps_state_of_last_finite_step(cuda_ok, precision, kw, tol):
+    """after NumericFailure, params_ hold the state as of the last
+    finite minibatch, like the reference's in-place Adam (tuner.py:449-450).
+    A NaN label placed in minibatch 3 of epoch 0: three Adam steps happen,
+    then both the oracle's loop and the kernel stop."""
+    from oracle import tuner as otuner
+    from paper_2304_05430_b200.errors import NumericFailure
+
+    rng = np.random.default_rng(31)
+    seqs = random_seqs(rng, rng.integers(1, 8, size=64))
+    y = rng.uniform(0.1, 0.9, size=64)
+    y[int(np.random.default_rng(0 + 1).permutation(64)[3 * 8 + 2])] = np.nan
+    p = otuner.init_params(0, layers=kw.get("recurrent_layers", 3), hidden=kw.get("hidden_size", 32))
+    with pytest.raises(FloatingPointError, match="epoch 0"):
+        otuner.train(p, seqs, y, epochs=3, lr=1e-3, batch_size=8, seed=0)
+    m = make(precision, epochs=3, batch_size=8, seed=0, **kw)
+    with pytest.raises(NumericFailure, match="epoch 0"):
+        m.fit(seqs, y)
+    init = otuner.init_params(0, layers=kw.get("recurrent_layers", 3), hidden=kw.get("hidden_size", 32))
+    assert any(not np.array_equal(p[k], init[k]) for k in p)  # the 3 steps did update
+    for k, v in p.items():
+        err = np.linalg.norm(m.params_[k] - v) / max(np.linalg.norm(v), 1e-12)
+        assert err <= tol, (k, err)

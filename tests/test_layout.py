@@ -110,3 +110,24 @@ def test_native_pack_rejects_bad_alloc():
         _pack_native(seqs, 6, 35, lambda r, n, w, c: (np.empty(1), np.empty(1)))
     with pytest.raises(RuntimeError):
         _pack_native(seqs, 6, 35, lambda r, n, w, c: (_ for _ in ()).throw(RuntimeError("x")))
+
+
+def test_non_native_byte_order_and_unaligned_inputs_pack_correctly():
+    """'>f8' arrays were memcpy'd as garbage by the native packer.
+    Now it declines them (returns None) and the numpy path converts them."""
+    rng = np.random.default_rng(8)
+    seqs = random_seqs(rng, [3, 5, 2])
+    swapped = [Seq(s.steps.astype(">f8"), s.context.astype(">f4")) for s in seqs]
+    want = _pack_checked([Seq(s.steps, s.context.astype(np.float32)) for s in seqs], 6, 35)
+    assert _native_pack(swapped, np.float64)[0] is None
+    h = pack_sequences(swapped, 6, 35)
+    assert np.array_equal(h.steps, want.steps) and np.array_equal(h.ctx, want.ctx)
+    buf = np.zeros(3 * 6 * 8 + 1, dtype=np.uint8)
+    una = np.frombuffer(buf.data, dtype=np.float64, count=18, offset=1).reshape(3, 6)
+    assert not una.flags.aligned
+    seqs2 = [Seq(np.ascontiguousarray(seqs[0].steps), seqs[0].context)]
+    buf[1:1 + 18 * 8] = np.frombuffer(seqs2[0].steps.tobytes(), dtype=np.uint8)
+    un_seqs = [Seq(una, seqs2[0].context)]
+    assert _native_pack(un_seqs, np.float64)[0] is None
+    h = pack_sequences(un_seqs, 6, 35)
+    assert np.array_equal(h.steps, seqs2[0].steps)
