@@ -378,3 +378,96 @@ class FusedDataParallelTuner:
         for ptr, mapped in self._owned:
             _lib.call("tt_ipc_close" if mapped else "tt_dev_free", ptr)
         self._owned = []
+
+
+# ------------------------------------------------ sharded scoring / PCA --
+
+
+def _group_info(group):
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return 1, 0
+    return dist.get_world_size(group), dist.get_rank(group)
+
+
+def _all_gather_host(obj, group):
+    import torch.distributed as dist
+
+    world, _ = _group_info(group)
+    if world == 1:
+        return [obj]
+    out = [None] * world
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def sharded_predict(est, sequences, group=None, gather: bool = True, predict_fn=None):
+    """Config-3 search-time/bulk scoring sharded by program:
+    every rank passes the same candidate list; rank r packs and scores only
+    its contiguous range of ~equal step rows (shard_by_rows on the step
+    counts) with the estimator's own kernels -- no collective on the data
+    path.  gather=True reassembles the float64 scores on every rank with one
+    host all-gather of the slices (the reference's ``predict`` result,
+    tuner.py:468-476); gather=False returns (lo, hi, local_scores).
+
+    ``predict_fn(est, seqs) -> np.ndarray`` defaults to ``est.predict``
+    (tests inject the oracle to exercise the sharding on CPU)."""
+    world, rank = _group_info(group)
+    n = len(sequences)
+    lens = np.fromiter((len(s.steps) for s in sequences), dtype=np.int64, count=n)
+    off = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=off[1:])
+    lo, hi = shard_by_rows(off, world)[rank]
+    fn = predict_fn or (lambda e, s: e.predict(s))
+    local = np.asarray(fn(est, sequences[lo:hi]), dtype=np.float64) if hi > lo else np.zeros(0)
+    if not gather:
+        return lo, hi, local
+    parts = _all_gather_host((lo, hi, local), group)
+    out = np.empty(n, dtype=np.float64)
+    for a, b, v in parts:
+        out[a:b] = v
+    return out
+
+
+def sharded_pca_counts(y, y_hat, task_offsets, group=None, count_fn=None) -> np.ndarray:
+    """Config-4 PCA sharded by task: tasks are assigned to ranks
+    by LPT on n_t^2 (lpt_assign), every rank counts its tasks' concordant
+    pairs with K1 (one launch over its tasks), and ONE all-reduce of the
+    zero-initialised per-task int64 vector combines them (gather_counts).
+    Counts are exact integers, so the result is identical to the unsharded
+    count whatever the assignment.  Every rank passes the full (y, y_hat,
+    task_offsets); returns the per-task counts on every rank.
+
+    ``count_fn(y, y_hat, offsets) -> int64 counts`` defaults to the GPU
+    pca_counts (tests inject the oracle)."""
+    from .metrics import pca_counts
+
+    world, rank = _group_info(group)
+    off = np.asarray(task_offsets, dtype=np.int64)
+    sizes = np.diff(off)
+    n_tasks = sizes.shape[0]
+    mine = [t for t in lpt_assign(sizes, world)[rank] if sizes[t] >= 2]
+    local: dict = {}
+    if mine:
+        idx = np.concatenate([np.arange(off[t], off[t + 1]) for t in mine])
+        sub = np.zeros(len(mine) + 1, dtype=np.int64)
+        np.cumsum(sizes[mine], out=sub[1:])
+        yy = np.asarray(y, dtype=np.float64)[idx]
+        ss = np.asarray(y_hat, dtype=np.float64)[idx]
+        c = (count_fn or pca_counts)(yy, ss, sub)
+        local = {t: int(v) for t, v in zip(mine, c)}
+    if world == 1:
+        out = np.zeros(n_tasks, dtype=np.int64)
+        for t, v in local.items():
+            out[t] = v
+        return out
+    return gather_counts(local, n_tasks, group)
+
+
+def sharded_segmented_pca(y, y_hat, task_offsets, group=None, count_fn=None) -> np.ndarray:
+    """Per-task PCA values (NaN for tasks with < 2 records) from the sharded
+    counts; float(correct)/float(total) equals the reference's mean bit for bit."""
+    from .metrics import pca_from_counts
+
+    return pca_from_counts(sharded_pca_counts(y, y_hat, task_offsets, group, count_fn), task_offsets)

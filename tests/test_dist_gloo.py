@@ -250,3 +250,66 @@ def test_fused_dp_preconditions_agree_or_raise_on_every_rank(pre, ok):
         assert out[0] == out[1] == "ok"
     else:
         assert out[0].startswith("raised") and out[1].startswith("raised")
+
+
+def _sharded_worker(rank, world, port, out):
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from oracle import metrics as om
+    from oracle import tuner as otuner
+    from paper_2304_05430_b200 import dist as tdist
+
+    _init(rank, world, port)
+    rng = np.random.default_rng(3)
+    seqs = random_seqs(rng, rng.integers(1, 9, size=41))
+    p = otuner.init_params(2, layers=1, hidden=4)
+    calls = []
+
+    def pred(_est, s):
+        calls.append(len(s))
+        return otuner.predict(p, s)
+
+    scores = tdist.sharded_predict(None, seqs, predict_fn=pred)
+    sizes = [50, 3, 120, 1, 77, 64, 2, 200, 9, 0]
+    off = np.zeros(len(sizes) + 1, dtype=np.int64)
+    off[1:] = np.cumsum(sizes)
+    y = np.round(rng.normal(size=off[-1]), 1)
+    s = np.round(rng.normal(size=off[-1]), 1)
+
+    def cnt(yy, ss, sub):
+        return np.array([om.pca_counts(yy[sub[i]:sub[i + 1]], ss[sub[i]:sub[i + 1]])[0]
+                         for i in range(len(sub) - 1)], dtype=np.int64)
+
+    counts = tdist.sharded_pca_counts(y, s, off, count_fn=cnt)
+    out[rank] = (scores, calls, counts)
+    dist.destroy_process_group()
+
+
+def test_sharded_predict_and_pca_equal_unsharded():
+    """e1/e2 entry points (dist.sharded_predict / sharded_pca_counts): each
+    rank computes only its shard, the host gather / one int64 all-reduce
+    reassembles exactly the unsharded result on every rank."""
+    from oracle import metrics as om
+    from oracle import tuner as otuner
+
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sharded_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    rng = np.random.default_rng(3)
+    seqs = random_seqs(rng, rng.integers(1, 9, size=41))
+    want = otuner.predict(otuner.init_params(2, layers=1, hidden=4), seqs)
+    sizes = [50, 3, 120, 1, 77, 64, 2, 200, 9, 0]
+    off = np.zeros(len(sizes) + 1, dtype=np.int64)
+    off[1:] = np.cumsum(sizes)
+    y = np.round(rng.normal(size=off[-1]), 1)
+    s = np.round(rng.normal(size=off[-1]), 1)
+    wc = [om.pca_counts(y[off[t]:off[t + 1]], s[off[t]:off[t + 1]])[0] if sizes[t] >= 2 else 0
+          for t in range(len(sizes))]
+    for r in range(world):
+        scores, calls, counts = out[r]
+        np.testing.assert_allclose(scores, want, rtol=1e-12)
+        assert len(calls) == 1 and 0 < calls[0] < 41  # each rank scored only its shard
+        assert list(counts) == wc
+    assert out[0][1][0] + out[1][1][0] == 41
