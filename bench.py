@@ -490,6 +490,78 @@ def sharded_extra(world, rank, dist, l2, stream, est, dims, flat):
     return out
 
 
+def search_throughput(n_tasks=64, steps=128):
+    """Search-time scoring (SURVEY §8 f2, config 3's real caller): the
+    reference's tune (simulated annealing, one candidate per scorer call)
+    with (a) the reference's own CPU tuner on a few tasks, (b) the GPU tuner
+    through the reference's unbatched scorer, (c) the cross-task batched tune
+    (paper_2304_05430_b200.search) -- whose result must be identical to (b).
+    Wall clock (host search loop included): scored candidates per second."""
+    import refbench
+
+    if not refbench.available():
+        return {}
+    tt = refbench._import_ref()  # noqa: F841
+    import tensortune.cli  # noqa: F401
+    import tensortune.models as tm
+    import tensortune.search as ts
+    from tensortune.benchmarks import convergence_benchmark
+    from tensortune.estimators import RecurrentAttentionTuner as RefTuner
+    from tensortune.features import encode_sequence_batch
+    from tensortune.oracle import OracleConfig, oracle_cost
+
+    from paper_2304_05430_b200 import RecurrentAttentionTuner
+    from paper_2304_05430_b200 import search as bs
+
+    ds, a = convergence_benchmark(seed=0, n_tasks=n_tasks, records_per_task=24)
+    seqs, y = encode_sequence_batch(ds, sorted(a.train_ids))
+    est = RecurrentAttentionTuner(epochs=1, seed=0).fit(seqs, y)
+    model = tm.CostModel(kind="tuner", estimator=est, config=tm.TrainConfig(epochs=1))
+    ocfg = OracleConfig(noise_sigma=0.05, seed=0)
+
+    def oracle_fn(k, sc, hw):
+        return oracle_cost(k, sc, hw, ocfg)
+
+    tids = [t.task_id for t in ds.tasks]
+    cfg = ts.SearchConfig(method="anneal", steps=steps, top_k=8, seed=0)
+    bs.bind_reference()
+    out = {}
+    t0 = time.perf_counter()
+    r_unb = ts.tune(ds, tids, lambda t: tm.make_schedule_scorer(model, ds.task_by_id[t], ds), oracle_fn, cfg)
+    t_unb = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r_bat = bs.tune(ds, tids, lambda t: bs.make_schedule_scorer(model, ds.task_by_id[t], ds), oracle_fn, cfg)
+    t_bat = time.perf_counter() - t0
+    n_scored = r_bat.scoring_stats["programs"]
+    ref_model = tm.CostModel(kind="tuner", estimator=RefTuner(epochs=0, seed=0).fit(seqs[:2], y[:2]),
+                             config=tm.TrainConfig(epochs=0))
+    ref_model.estimator.set_weights(est.get_weights())
+    few = tids[:4]
+    n_cpu = [0]
+
+    def cpu_factory(t):
+        inner = tm.make_schedule_scorer(ref_model, ds.task_by_id[t], ds)
+
+        def scorer(schedules):
+            n_cpu[0] += len(schedules)
+            return inner(schedules)
+        return scorer
+
+    t0 = time.perf_counter()
+    ts.tune(ds, few, cpu_factory, oracle_fn, cfg)
+    t_cpu = time.perf_counter() - t0
+    out.update({
+        "search_tasks": n_tasks, "search_sa_steps": steps, "search_candidates_scored": n_scored,
+        "search_identical_to_reference_tune": r_bat.to_json() == r_unb.to_json(),
+        "search_gpu_unbatched_candidates_per_s": n_scored / t_unb,
+        "search_gpu_batched_candidates_per_s": n_scored / t_bat,
+        "search_gpu_batched_predict_calls": r_bat.scoring_stats["predict_calls"],
+        "search_reference_cpu_candidates_per_s_4_tasks": n_cpu[0] / t_cpu,
+        "search_batched_speedup_vs_unbatched": t_unb / t_bat,
+    })
+    return out
+
+
 def print_phases(est, dims, flat, m, v, prog, yd, rng, n, n_steps, t_adam, batch=BATCH):
     """Per-phase marks of one minibatch inside the train kernel (CTA 0 clock64
     at 1965 MHz; the first gradient-job CTA in %globaltimer ns)."""
@@ -787,6 +859,7 @@ def run_b200(args, world, rank):
         extra.update(survey_configs(est, dims, flat, l2, stream, n_steps, prog, yd, rng))
         extra.update(mlp_training())
         extra.update(dp_exchange_cost())
+        extra.update(search_throughput())
 
     if rank == 0:
         cpu = None

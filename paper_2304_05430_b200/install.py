@@ -15,6 +15,11 @@ the search scorer (models.py:364-378) and the CLI -- through the kernels:
   tensortune.sampling.filter_invalid             -> sampling.filter_invalid (K2)
   tensortune.features / .models / .transfer
       encode_sequence_batch, encode_flat_batch   -> featurize (batched labels)
+  tensortune.models / .cli / tensortune
+      make_schedule_scorer                       -> search.BatchableScorer
+  tensortune.search / .cli / tensortune
+      tune                                       -> search.tune (cross-task
+                                                    batched scoring, f2)
 
 ``uninstall()`` restores the originals.
 """
@@ -29,6 +34,7 @@ from . import estimators as _est
 from . import featurize as _feat
 from . import metrics as _met
 from . import sampling as _samp
+from . import search as _search
 
 _saved: list = []
 
@@ -108,6 +114,16 @@ def install() -> None:
                make_per_task_metrics(mods["tensortune.models"]))
     _patch(mods["tensortune.transfer"], "_grouped_pca", _met.grouped_pca)
     _patch(mods["tensortune.sampling"], "filter_invalid", _samp.filter_invalid)
+    # search-time batched scoring (f2): tune batches its scorer calls across
+    # tasks when the scorers come from make_schedule_scorer
+    import tensortune.cli  # noqa: F401  (imports tune / make_schedule_scorer by name)
+    import tensortune.search  # noqa: F401
+
+    _search.bind_reference()
+    for key in ("tensortune.models", "tensortune.cli", "tensortune"):
+        _patch(sys.modules.get(key), "make_schedule_scorer", _search.make_schedule_scorer)
+    for key in ("tensortune.search", "tensortune.cli", "tensortune"):
+        _patch(sys.modules.get(key), "tune", _search.tune)
     import tensortune.features as features
 
     enc_seq, enc_flat = _feat.make_encoders(features)

@@ -101,7 +101,10 @@ def run_ref_suite(module: str, precision: str, extra=(), timeout=3000):
 def test_reference_module_on_b200(cuda_ok, module, precision):
     out, calls = run_ref_suite(module, precision)
     print(out.strip().splitlines()[-1], calls)
-    assert sum(calls.values()) > 0, f"{module} never reached the kernels"
+    # test_search.py scores with its own stub scorers (it exercises the
+    # installed batched `tune` and its fallback, not the estimators)
+    if module != "test_search.py":
+        assert sum(calls.values()) > 0, f"{module} never reached the kernels"
 
 
 ACCEPTANCE = os.path.join(REF_TESTS, "test_acceptance.py")
