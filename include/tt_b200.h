@@ -286,6 +286,35 @@ int tt_prune_stats(const int64_t *d_flops, const double *d_cost, const uint8_t *
                    int32_t min_records, double *d_thr, uint8_t *d_keep, int32_t *d_survivors,
                    uint8_t *d_task_keep, void *d_ws, size_t ws_bytes, tt_stream_t stream);
 
+/* ---------------------------------------------------------------- GBDT --
+ * replaces estimators/gbdt.py:51-265 GradientBoostedTrees._grow / fit's
+ * update / predict, bit-exact in float64.
+ * tt_gbdt_grow: one tree on residuals d_g.  d_Xc is the n x F training matrix
+ *   in COLUMN-major order (F rows of n), d_root_order the F x n stable
+ *   argsort of its columns (gbdt.py:109).  Outputs the tree in LEVEL order
+ *   (root 0; the host renumbers into the reference's stack order): node
+ *   arrays of capacity 2n+1, *d_node_count, and d_incr[r] = the leaf value of
+ *   row r's leaf.  Workspace: tt_gbdt_workspace_bytes(n, F, max_depth).
+ * tt_gbdt_update: pred += lr * incr; g = y - pred (incr = NULL: g = y - pred).
+ * tt_gbdt_predict: out[r] = (accumulate ? out[r] : base) + sum over trees in
+ *   order of lr * leaf (one round-to-nearest add per tree, gbdt.py:242-244);
+ *   trees concatenated with d_tree_offsets[t] = first node of tree t
+ *   (child indices are tree-local); X row-major (col_major = 0) or
+ *   column-major. */
+size_t tt_gbdt_workspace_bytes(int64_t n, int32_t n_features, int32_t max_depth);
+int tt_gbdt_grow(const double *d_Xc, const double *d_g, const int32_t *d_root_order, int64_t n,
+                 int32_t n_features, int32_t max_depth, int32_t min_samples_leaf, int32_t *d_feature,
+                 double *d_threshold, int32_t *d_left, int32_t *d_right, double *d_value,
+                 int32_t *d_node_count, double *d_incr, void *d_ws, size_t ws_bytes,
+                 tt_stream_t stream);
+int tt_gbdt_update(double *d_pred, const double *d_incr, const double *d_y, double *d_g, double lr,
+                   int64_t n, tt_stream_t stream);
+int tt_gbdt_predict(const int32_t *d_feature, const double *d_threshold, const int32_t *d_left,
+                    const int32_t *d_right, const double *d_value, const int64_t *d_tree_offsets,
+                    int32_t n_trees, double base, double lr, const double *d_X, int64_t n,
+                    int32_t n_features, int32_t col_major, double *d_out, int32_t accumulate,
+                    tt_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

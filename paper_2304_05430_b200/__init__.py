@@ -4,6 +4,7 @@ Drop-in replacements with the reference's names (paths relative to
 /root/reference/pkg/src/tensortune):
 
     RecurrentAttentionTuner, CostMLP, ranking_grad   estimators/tuner.py, mlp.py
+    GradientBoostedTrees                             estimators/gbdt.py
     pairwise_comparison_accuracy, top_k_score,        metrics.py
     ranking_loss, rmse
     filter_invalid, task_weights, prune_dataset       sampling.py
@@ -18,6 +19,7 @@ from __future__ import annotations
 from . import config
 from .errors import DataValidationError, NumericFailure, TensorTuneError
 from .estimators import CostMLP, RecurrentAttentionTuner, ranking_grad
+from .gbdt import GradientBoostedTrees
 from .metrics import (
     grouped_pca,
     pairwise_comparison_accuracy,
@@ -35,6 +37,7 @@ __all__ = [
     "NumericFailure",
     "RecurrentAttentionTuner",
     "CostMLP",
+    "GradientBoostedTrees",
     "ranking_grad",
     "pairwise_comparison_accuracy",
     "pca_counts",

@@ -68,6 +68,12 @@ SIGNATURES: dict[str, tuple] = {
                                                    _P, _P, _P, _P, _SZ, _P]),
     "tt_mlp_train_f64": (ctypes.c_int, [_P] * 5 + [_I32, _P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P,
                                                    _P, _P, _P, _P, _SZ, _P]),
+    "tt_gbdt_workspace_bytes": (_SZ, [_I64, _I32, _I32]),
+    "tt_gbdt_grow": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
+                                    _SZ, _P]),
+    "tt_gbdt_update": (ctypes.c_int, [_P, _P, _P, _P, _D, _I64, _P]),
+    "tt_gbdt_predict": (ctypes.c_int, [_P, _P, _P, _P, _P, _P, _I32, _D, _D, _P, _I64, _I32, _I32, _P, _I32,
+                                       _P]),
     "tt_prune_workspace_bytes": (_SZ, [_I64]),
     "tt_prune_stats": (ctypes.c_int, [_P, _P, _P, _P, _I32, _D, _I32, _P, _P, _P, _P, _P, _SZ, _P]),
 }

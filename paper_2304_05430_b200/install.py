@@ -8,6 +8,7 @@ the search scorer (models.py:364-378) and the CLI -- through the kernels:
 
   tensortune.models / tensortune.estimators / tensortune
       RecurrentAttentionTuner, CostMLP           -> estimators.*
+      GradientBoostedTrees                       -> gbdt.* (f3)
   tensortune.metrics / .models / .transfer / tensortune
       pairwise_comparison_accuracy, top_k_score  -> metrics.*
   tensortune.models.per_task_metrics             -> one batched K1 + K10 launch
@@ -32,6 +33,7 @@ import numpy as np
 
 from . import estimators as _est
 from . import featurize as _feat
+from . import gbdt as _gbdt
 from . import metrics as _met
 from . import sampling as _samp
 from . import search as _search
@@ -105,6 +107,10 @@ def install() -> None:
         _patch(mods[key], "RecurrentAttentionTuner", _est.RecurrentAttentionTuner)
         _patch(mods[key], "CostMLP", _est.CostMLP)
     _patch(mods["tensortune.estimators.mlp"], "ranking_grad", _est.ranking_grad)
+    import tensortune.estimators.gbdt  # noqa: F401
+
+    for key in ("tensortune.models", "tensortune.estimators", "tensortune.estimators.gbdt"):
+        _patch(sys.modules.get(key), "GradientBoostedTrees", _gbdt.GradientBoostedTrees)
     for key in ("tensortune", "tensortune.metrics", "tensortune.models", "tensortune.transfer"):
         _patch(mods[key], "pairwise_comparison_accuracy", _met.pairwise_comparison_accuracy)
         _patch(mods[key], "top_k_score", _met.top_k_score)

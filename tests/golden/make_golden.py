@@ -21,6 +21,9 @@ Every fixture records the reference call that produced it:
                 fit/continue_fit (small and default sizes)
   sampling.npz  sampling.filter_invalid / task_weights / prune_dataset on
                 benchmarks.pruning_benchmark-style data
+  gbdt.npz      estimators.gbdt.GradientBoostedTrees fit (get_weights,
+                train_curve_) and predict on the convergence benchmark's flat
+                features plus tie-heavy / adjacent-double / tiny cases
 """
 
 from __future__ import annotations
@@ -35,7 +38,9 @@ if REF not in sys.path:
 
 import numpy as np  # noqa: E402
 
-from tensortune.benchmarks import pruning_benchmark  # noqa: E402
+from tensortune.benchmarks import convergence_benchmark, pruning_benchmark  # noqa: E402
+from tensortune.estimators.gbdt import GradientBoostedTrees  # noqa: E402
+from tensortune.features import encode_flat_batch  # noqa: E402
 from tensortune.estimators.mlp import CostMLP, ranking_grad  # noqa: E402
 from tensortune.estimators.optim import Adam  # noqa: E402
 from tensortune.estimators.tuner import RecurrentAttentionTuner  # noqa: E402
@@ -328,7 +333,49 @@ def gen_sampling():
     save("sampling.npz", **out)
 
 
+def gen_gbdt():
+    out = {}
+    cases = []
+    ds, a = convergence_benchmark(seed=0, n_tasks=6, records_per_task=40)
+    Xtr, ytr = encode_flat_batch(ds, sorted(a.train_ids))
+    Xte, yte = encode_flat_batch(ds, sorted(a.test_ids))
+    cases.append(("conv", Xtr, ytr, Xte, yte, dict(num_trees=12, max_depth=4, learning_rate=0.1,
+                                                      min_samples_leaf=4)))
+    rng = np.random.default_rng(7)
+    X = np.round(rng.normal(size=(300, 5)), 1)   # heavy ties: x[i] < x[i+1] gating
+    y = rng.normal(size=300)
+    cases.append(("ties", X, y, X[:50] + 0.05, y[:50], dict(num_trees=8, max_depth=6, learning_rate=0.3,
+                                                             min_samples_leaf=2)))
+    b = np.nextafter(1.0, 2.0)                   # (a + b) / 2 rounds to b: x <= cut takes both
+    X = np.array([[1.0, 0.0], [b, 1.0], [1.0, 2.0], [b, 3.0], [2.0, 4.0], [1.0, 5.0]])
+    y = np.array([0.0, 1.0, 0.2, 1.1, 3.0, 0.1])
+    cases.append(("adjacent", X, y, X, y, dict(num_trees=3, max_depth=3, learning_rate=1.0,
+                                                min_samples_leaf=1)))
+    cases.append(("single", np.array([[0.5, 1.0]]), np.array([2.0]), np.array([[0.0, 0.0]]),
+                  np.array([1.0]), dict(num_trees=2, max_depth=2, learning_rate=0.5, min_samples_leaf=1)))
+    X = rng.normal(size=(2000, 12))
+    y = np.sin(X[:, 0]) + 0.1 * rng.normal(size=2000)
+    cases.append(("deep", X, y, X[:100], y[:100], dict(num_trees=4, max_depth=12, learning_rate=0.2,
+                                                        min_samples_leaf=3)))
+    for name, Xa, ya, Xb, yb, kw in cases:
+        m = GradientBoostedTrees(**kw).fit(Xa, ya, eval_set=(Xb, yb))
+        for k, v in m.get_weights().items():
+            out[f"{name}_w_{k}"] = v
+        out[f"{name}_curve"] = np.array([[t, np.nan if v is None else v] for t, v in m.train_curve_])
+        out[f"{name}_pred"] = m.predict(Xb)
+        out[f"{name}_X"], out[f"{name}_y"], out[f"{name}_Xv"], out[f"{name}_yv"] = Xa, ya, Xb, yb
+        out[f"{name}_params"] = np.array([kw["num_trees"], kw["max_depth"], kw["learning_rate"],
+                                          kw["min_samples_leaf"]], dtype=np.float64)
+    out["names"] = np.array([c[0] for c in cases])
+    save("gbdt.npz", **out)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()["gen_" + name]()
+        sys.exit(0)
+    gen_gbdt()
     gen_pca()
     gen_topk()
     gen_ranking()

@@ -35,7 +35,7 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF_TESTS = os.path.join(ROOT, "baseline", "_ref", "tests")
 
-MODULES = ["test_metrics.py", "test_mlp.py", "test_tuner.py", "test_models.py",
+MODULES = ["test_metrics.py", "test_mlp.py", "test_tuner.py", "test_gbdt.py", "test_models.py",
            "test_sampling.py", "test_transfer.py", "test_search.py", "test_cli.py"]
 
 # Reference assertions that are statements about float64 numpy arithmetic.
@@ -116,6 +116,9 @@ ACCEPTANCE = os.path.join(REF_TESTS, "test_acceptance.py")
     ("test_gradients_match_central_differences", "fp64"),
     ("test_sequence_model_converges_below_the_tree_baseline", "fp32"),
     ("test_transfer_reaches_parity_on_a_40_percent_budget", "fp32"),
+    # GBDT (f3) on the GPU: 3 split strategies x 3 seeds of pruned vs full training
+    ("test_pruning_preserves_ranking_quality", "fp32"),
+    ("test_search_recovers_the_enumerated_optimum", "fp32"),
 ])
 def test_reference_acceptance_on_b200(cuda_ok, name, precision):
     """The reference's acceptance criteria (test_acceptance.py)

@@ -143,3 +143,23 @@ def test_filter_stats_match_reference():
     raw = osamp.raw_task_weights(g["task_flops"], list(g["task_ops"]))
     tot = sum(raw)
     np.testing.assert_array_equal([w / tot for w in raw], g["weights"])
+
+
+def test_gbdt_oracle_matches_reference_trees_bitwise():
+    """oracle/gbdt.py (level-wise growth + DFS renumbering, the GPU's
+    construction) reproduces the reference's trees, curves and predictions
+    bit for bit on every golden case."""
+    from oracle import gbdt as ogbdt
+
+    g = golden("gbdt.npz")
+    for name in g["names"]:
+        nt, md, lr, ml = g[f"{name}_params"]
+        base, trees, curve = ogbdt.fit(g[f"{name}_X"], g[f"{name}_y"], num_trees=int(nt), max_depth=int(md),
+                                       learning_rate=float(lr), min_samples_leaf=int(ml),
+                                       eval_set=(g[f"{name}_Xv"], g[f"{name}_yv"]))
+        assert base == g[f"{name}_w_base"][0]
+        assert np.array_equal([t[0].shape[0] for t in trees], g[f"{name}_w_node_counts"]), name
+        for i, key in enumerate(("feature", "threshold", "left", "right", "value")):
+            assert np.array_equal(np.concatenate([t[i] for t in trees]), g[f"{name}_w_{key}"]), (name, key)
+        assert np.array_equal(np.array(curve, dtype=np.float64), g[f"{name}_curve"]), name
+        assert np.array_equal(ogbdt.predict(base, trees, float(lr), g[f"{name}_Xv"]), g[f"{name}_pred"]), name
