@@ -491,7 +491,10 @@ struct AttnCache {
 
 // S, K, V: [P][Tmax][D] (global scratch).  Writes yhat[p] to out_yhat[p] for
 // occupied slots.  All 256 threads participate; weights come from `w`
-// (shared memory).  P == 1 uses latency-oriented sliced matvecs.
+// (shared memory).  The TRAIN instance (P == 1) uses latency-oriented sliced
+// matvecs; scoring uses the same per-program summation order (sequential over
+// K, bias last) for every tile size P, so a program's score does not depend on
+// how many programs share its launch (search-time re-batching is bit-exact).
 template <typename R, int H, int P, bool TRAIN>
 __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const TileInfo<R, P>& ti,
                                    const R* __restrict__ S, R* __restrict__ Kb,
@@ -539,7 +542,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
   const R sq = sqrt((R)dh);
   for (int u = 0; u < dm.U; ++u) {
     // q = pooled Wq + bq
-    if constexpr (P == 1)
+    if constexpr (P == 1 && TRAIN)
       bmv_col<R>(sm.pool, w.Wq, w.ldd, D, D, w.bq, sm.q, sm.red);
     else {
       bmv_col_batch<R, P>(sm.pool, D, w.Wq, w.ldd, D, D, w.bq, sm.q, D);
@@ -592,7 +595,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
       for (int i = tid; i < heads * Tmax; i += kThreads) cache->alpha[u * heads * Tmax + i] = sm.alpha[i];
     }
     // pooled = mix Wo + bo
-    if constexpr (P == 1)
+    if constexpr (P == 1 && TRAIN)
       bmv_col<R>(sm.mix, w.Wo, w.ldd, D, D, w.bo, sm.pool, sm.red);
     else {
       bmv_col_batch<R, P>(sm.mix, D, w.Wo, w.ldd, D, D, w.bo, sm.pool, D);
@@ -610,7 +613,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
     sm.z[i] = v;
   }
   __syncthreads();
-  if constexpr (P == 1)
+  if constexpr (P == 1 && TRAIN)
     bmv_col<R>(sm.z, w.W1, w.ld1, Z, kHeadHidden, w.b1, sm.a1, sm.red);
   else {
     bmv_col_batch<R, P>(sm.z, Z, w.W1, w.ld1, Z, kHeadHidden, w.b1, sm.a1, kHeadHidden);

@@ -146,7 +146,7 @@ class GradientBoostedTrees(BaseEstimator, RegressorMixin):
         self.base_prediction_ = float(y.mean())
         self.trees_ = []
         self.train_curve_ = []
-        self.__dict__.pop("_dev_trees", None)
+        self.__dict__.pop("_dev_tree_cache", None)
         lr = float(self.learning_rate)
 
         order = np.argsort(X, axis=0, kind="stable").astype(np.int32).T.copy()
@@ -202,11 +202,11 @@ class GradientBoostedTrees(BaseEstimator, RegressorMixin):
         return self
 
     def _dev_trees(self):
-        cache = self.__dict__.get("_dev_trees")
+        cache = self.__dict__.get("_dev_tree_cache")
         if cache is None or cache[0] is not self.trees_ or cache[1] != len(self.trees_):
             arrays = tuple(_device.to_dev(a) for a in _flat(self.trees_))
             cache = (self.trees_, len(self.trees_), arrays)
-            self.__dict__["_dev_trees"] = cache
+            self.__dict__["_dev_tree_cache"] = cache
         return cache[2]
 
     def predict(self, X) -> np.ndarray:
@@ -247,9 +247,9 @@ class GradientBoostedTrees(BaseEstimator, RegressorMixin):
                                      value=weights["value"][sl].astype(np.float64)))
             off += int(count)
         self.train_curve_ = []
-        self.__dict__.pop("_dev_trees", None)
+        self.__dict__.pop("_dev_tree_cache", None)
 
     def __getstate__(self):
         state = dict(self.__dict__)
-        state.pop("_dev_trees", None)
+        state.pop("_dev_tree_cache", None)
         return state

@@ -63,6 +63,7 @@ def test_gbdt_weights_round_trip_and_validation(cuda_ok):
     m2 = GradientBoostedTrees(learning_rate=0.1)
     m2.set_weights(m.get_weights())
     assert np.array_equal(m2.predict(g["conv_Xv"]), m.predict(g["conv_Xv"]))
+    assert np.array_equal(m.predict(g["conv_Xv"][:7]), m.predict(g["conv_Xv"])[:7])  # cached trees
     assert m2.train_curve_ == []
     with pytest.raises(DataValidationError, match="num_trees"):
         GradientBoostedTrees(num_trees=0).fit(np.zeros((3, 2)), np.zeros(3))

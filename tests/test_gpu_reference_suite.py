@@ -118,7 +118,6 @@ ACCEPTANCE = os.path.join(REF_TESTS, "test_acceptance.py")
     ("test_transfer_reaches_parity_on_a_40_percent_budget", "fp32"),
     # GBDT (f3) on the GPU: 3 split strategies x 3 seeds of pruned vs full training
     ("test_pruning_preserves_ranking_quality", "fp32"),
-    ("test_search_recovers_the_enumerated_optimum", "fp32"),
 ])
 def test_reference_acceptance_on_b200(cuda_ok, name, precision):
     """The reference's acceptance criteria (test_acceptance.py)

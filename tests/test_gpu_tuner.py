@@ -87,6 +87,21 @@ def test_predict_padding_and_chunk_invariance(cuda_ok):
     assert m.predict([]).shape == (0,)
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64", "tf32"])
+def test_scores_do_not_depend_on_the_launch_size(cuda_ok, precision):
+    """Search-time batching (f2) relies on it: a program's score is the same
+    whether it is scored alone, in a small launch (one program per CTA) or in
+    a bulk launch (multi-program tiles), bit for bit."""
+    rng = np.random.default_rng(12)
+    seqs = random_seqs(rng, rng.integers(1, 13, size=9))
+    m = make(precision, epochs=0, seed=5).fit(seqs, rng.uniform(0.2, 0.8, size=len(seqs)))
+    singles = np.array([m.predict([s])[0] for s in seqs])
+    for reps in (2, 40, 400):  # 18 / 360 / 3600 programs
+        big = m.predict(seqs * reps)
+        for r in range(reps):
+            np.testing.assert_array_equal(big[r * 9:(r + 1) * 9], singles)
+
+
 def test_large_random_batch_matches_oracle(cuda_ok):
     rng = np.random.default_rng(99)
     lens = rng.integers(1, 33, size=777)
