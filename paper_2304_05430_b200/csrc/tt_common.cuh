@@ -78,6 +78,13 @@ struct Act<double> {
   static __device__ __forceinline__ double rsqrt(double x) { return 1.0 / ::sqrt(x); }
 };
 
+// Explicitly fused multiply-add: an expression like a*b + c*d leaves the
+// compiler free to contract either product, and the choice can differ between
+// template instances (tile sizes) -- spelling the FMA out keeps a program's
+// arithmetic identical in every instance.
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
 // ------------------------------------------------------------- reductions --
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

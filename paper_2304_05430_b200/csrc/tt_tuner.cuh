@@ -316,8 +316,8 @@ __device__ void bmv_col_batch(const R* v, int ldv, const R* W, int ld, int K, in
     const R* v1 = v + (p1 < P ? p1 : p0) * ldv;
     for (int k = 0; k < K; ++k) {
       const R wk = W[k * ld + c];
-      a0 += v0[k] * wk;
-      a1 += v1[k] * wk;
+      a0 = fma_rn(v0[k], wk, a0);
+      a1 = fma_rn(v1[k], wk, a1);
     }
     const R b = bias ? bias[c] : (R)0;
     out[p0 * ldo + c] = a0 + b;
@@ -427,7 +427,7 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
         } else {
           const R* x = ti.step0[p] + (int64_t)t * dm.d0;
           z = bc;
-          for (int k = 0; k < d_in; ++k) z += x[k] * ldw<TRAIN>(Wx + k * G + c);
+          for (int k = 0; k < d_in; ++k) z = fma_rn(x[k], ldw<TRAIN>(Wx + k * G + c), z);
         }
         z += dot_reg<H>(hbase + p * H, wh);
         const int gate = c / H;
@@ -447,7 +447,7 @@ __device__ void lstm_layer_fwd(const TDims& dm, const R* __restrict__ prm, int l
           const int t = dir == 0 ? s : n - 1 - s;
           const R* gp = gbase + p * G;
           const R gi = gp[j], gf = gp[H + j], gg = gp[2 * H + j], go = gp[3 * H + j];
-          const R cn = gf * creg[ci] + gi * gg;
+          const R cn = fma_rn(gf, creg[ci], gi * gg);
           const R tc = Act<R>::tanh(cn);
           const R hn = go * tc;
           creg[ci] = cn;
@@ -564,7 +564,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
       for (int t = lane; t < n; t += 32) {
         const R* kr = Kb + ((int64_t)p * Tmax + t) * D + h * dh;
         R acc = 0;
-        for (int d = 0; d < dh; ++d) acc += qh[d] * kr[d];
+        for (int d = 0; d < dh; ++d) acc = fma_rn(qh[d], kr[d], acc);
         acc = acc / sq;  // tuner.py:264 divides by sqrt(dh)
         al[t] = acc;
         mx = acc > mx ? acc : mx;
@@ -586,7 +586,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
       const int n = ti.len[p];
       const R* al = sm.alpha + ((int64_t)p * heads + h) * Tmax;
       R acc = 0;
-      for (int t = 0; t < n; ++t) acc += al[t] * Vb[((int64_t)p * Tmax + t) * D + c];
+      for (int t = 0; t < n; ++t) acc = fma_rn(al[t], Vb[((int64_t)p * Tmax + t) * D + c], acc);
       sm.mix[i] = acc;
     }
     __syncthreads();
@@ -623,7 +623,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
   __syncthreads();
   for (int p = warp; p < P; p += kThreads / 32) {
     R acc = 0;
-    for (int c = lane; c < kHeadHidden; c += 32) acc += sm.a1[p * kHeadHidden + c] * w.W2[c];
+    for (int c = lane; c < kHeadHidden; c += 32) acc = fma_rn(sm.a1[p * kHeadHidden + c], w.W2[c], acc);
     acc = warp_sum(acc);
     if (lane == 0 && ti.len[p] > 0) {
       const R yh = Act<R>::sigmoid(acc + w.b2);
