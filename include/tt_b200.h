@@ -259,6 +259,15 @@ int tt_mlp_predict_f64(const double *d_params, const double *d_X, int64_t n,
  * float64 reference: max |d| <= 1e-2, mean |d| <= 1e-3 (tests). */
 int tt_mlp_predict_tf32(const float *d_params, const float *d_X, int64_t n, int32_t n_features,
                         float *d_out, tt_stream_t stream);
+/* The default fp32 scorer on the tensor cores: split-precision tf32 (each
+ * operand = tf32 hi + tf32 lo, three products per layer accumulated in fp32,
+ * ~2^-21 relative layer error; accurate exp-based tanh), same tcgen05/TMA
+ * pipeline as tt_mlp_predict_tf32.  Eligible (tt_mlp_f32tc_eligible) when
+ * F*4 is a multiple of 16, d_X is 16-B aligned and the split weights fit in
+ * shared memory (F <= ~190); replaces mlp.py:146-155 predict at fp32. */
+int tt_mlp_predict_f32tc(const float *d_params, const float *d_X, int64_t n, int32_t n_features,
+                         float *d_out, tt_stream_t stream);
+int32_t tt_mlp_f32tc_eligible(int32_t n_features, const float *d_X);
 size_t tt_mlp_train_workspace_bytes(int32_t f64, int32_t n_features, int32_t batch_size);
 int tt_mlp_train_f32(float *d_params, float *d_m, float *d_v, const float *d_X, const float *d_y,
                      int32_t n_features, const int32_t *d_order, int64_t n_order,

@@ -93,6 +93,7 @@ def real_dtype(precision: str):
     t = torch()
     if precision == "fp64":
         return t.float64
-    if precision in ("fp32", "tf32"):  # tf32: tensor-core scoring, fp32 storage
+    if precision in ("fp32", "tf32", "fp32_cuda"):  # tf32: tensor-core scoring, fp32 storage;
+        # fp32_cuda: the fp32 CUDA-core kernels even where a tensor-core fp32 path exists
         return t.float32
-    raise ValueError(f"precision must be 'fp32', 'tf32' or 'fp64', got {precision!r}")
+    raise ValueError(f"precision must be 'fp32', 'tf32', 'fp32_cuda' or 'fp64', got {precision!r}")

@@ -63,6 +63,8 @@ SIGNATURES: dict[str, tuple] = {
     "tt_mlp_predict_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
     "tt_mlp_predict_f64": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
     "tt_mlp_predict_tf32": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    "tt_mlp_predict_f32tc": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
+    "tt_mlp_f32tc_eligible": (_I32, [_I32, _P]),
     "tt_mlp_train_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
     "tt_mlp_train_f32": (ctypes.c_int, [_P] * 5 + [_I32, _P, _I64, _I32, _I32, _I32, _D, _D, _D, _D, _P,
                                                    _P, _P, _P, _P, _SZ, _P]),

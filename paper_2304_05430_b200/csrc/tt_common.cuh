@@ -104,8 +104,13 @@ __device__ __forceinline__ T warp_max(T v) {
 }
 
 // Named barrier over `count` threads (multiple of 32); id 0 is __syncthreads.
+// The non-.aligned form: warp-specialised kernels meet on one barrier id from
+// different code locations (e.g. recurrence warps and prefetch warps), which
+// the .aligned form (bar.sync) does not allow (PTX ISA: every thread of the
+// CTA must execute the same aligned barrier instruction; compute-sanitizer
+// synccheck flags it).
 __device__ __forceinline__ void named_barrier(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // Software grid barrier for cooperative (co-resident) launches.  `ctr` is a

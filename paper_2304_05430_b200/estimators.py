@@ -533,8 +533,12 @@ class CostMLP(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         flat = self._device_flat(list(self.NAMES)) if flat is None else flat
         out = _device.empty(n, _device.real_dtype(prec))
         fn = "tt_mlp_predict_f64" if prec == "fp64" else "tt_mlp_predict_f32"
-        if prec == "tf32" and (F * 4) % 16 == 0:
-            fn = "tt_mlp_predict_tf32"  # tcgen05 tensor-core path
+        if (F * 4) % 16 == 0 and prec in ("fp32", "tf32"):
+            # tcgen05 tensor-core paths (TMA needs 16-B rows): "fp32" = split
+            # tf32 (3 products, fp32 accuracy), "tf32" = plain tf32.  The
+            # choice depends on F only, never on n, so a row's score does not
+            # depend on its batch (search-time re-batching stays bit-exact).
+            fn = "tt_mlp_predict_f32tc" if prec == "fp32" else "tt_mlp_predict_tf32"
         _lib.call(fn, flat.data_ptr(), Xd.data_ptr(), n, F, out.data_ptr(), _device.stream_ptr())
         return out
 

@@ -107,6 +107,32 @@ def test_mlp_tenset_width_scoring_fp32(cuda_ok):
 
 
 @pytest.mark.parametrize("n,F", [(1, 164), (127, 164), (128, 164), (129, 164), (70000, 164),
+                                 (300, 32), (257, 8), (1000, 100), (513, 4), (2000, 192)])
+def test_mlp_fp32_tensor_core_scoring_meets_fp32_tolerance(cuda_ok, n, F):
+    """The default fp32 scorer on tcgen05 (split tf32: hi/lo operands, three
+    products per layer): same stated fp32 tolerance as the CUDA-core kernel
+    (|d| <= 2e-5 vs the float64 reference), every tile/tail shape, and
+    bit-identical scores for a row whatever its batch (search re-batching)."""
+    from paper_2304_05430_b200 import _lib
+
+    rng = np.random.default_rng(n + F)
+    X = rng.normal(size=(n, F))
+    m = mlp("fp32", epochs=0, seed=0).fit(X[: min(n, 64)], rng.uniform(size=min(n, 64)))
+    before = _lib.CALLS["tt_mlp_predict_f32tc"]
+    got = m.predict(X)
+    assert _lib.CALLS["tt_mlp_predict_f32tc"] == before + 1  # the tensor-core kernel ran
+    want = omlp.predict(omlp.init_params(F, 0), X)
+    d = np.abs(got - want)
+    assert d.max() <= 2e-5, (d.max(), d.mean())
+    m.precision = "fp32_cuda"
+    cuda = m.predict(X)
+    assert np.abs(cuda - want).max() <= 2e-5
+    m.precision = "fp32"
+    k = min(n, 5)
+    np.testing.assert_array_equal(m.predict(X[:k]), got[:k])
+
+
+@pytest.mark.parametrize("n,F", [(1, 164), (127, 164), (128, 164), (129, 164), (70000, 164),
                                  (300, 32), (257, 8), (1000, 100)])
 def test_mlp_tf32_tensor_core_scoring(cuda_ok, n, F):
     """tcgen05 kind::tf32 path: stated tolerance max |d| <= 1e-2, mean <= 1e-3
