@@ -404,8 +404,9 @@ def mlp_training(n=65536, F=164):
 
 def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
     """CostMLP bulk scoring at TenSet width (configs[0]/[2] shape): the
-    tcgen05 tf32 kernel and the fp32 CUDA-core kernel, HBM roofline
-    (algorithmic bytes 4F + 4 per row)."""
+    tcgen05 kernels -- "fp32" (the default: split-precision tf32 at fp32
+    accuracy) and "tf32" -- and the fp32 CUDA-core kernel ("fp32_cuda"), HBM
+    roofline (algorithmic bytes 4F + 4 per row)."""
     import torch
 
     from paper_2304_05430_b200 import CostMLP, _lib
@@ -415,7 +416,8 @@ def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
     est = CostMLP(epochs=0, seed=0)
     est._init_params(F)
     out = {}
-    for prec, fn in (("tf32", "tt_mlp_predict_tf32"), ("fp32", "tt_mlp_predict_f32")):
+    for prec, fn in (("tf32", "tt_mlp_predict_tf32"), ("fp32", "tt_mlp_predict_f32tc"),
+                     ("fp32_cuda", "tt_mlp_predict_f32")):
         est.precision = prec
         flat = est._device_flat(list(est.NAMES))
         y = torch.empty(n, device="cuda")

@@ -228,41 +228,49 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
 // ---------------------------------------------------- split precision --
 // The same scorer at fp32 accuracy ("fp32" precision, the default): every
-// operand is split into a tf32 head and a tf32 tail, v = hi + lo with
-// hi = round_tf32(v) and lo = v - hi (exact in fp32), and each dense layer
-// runs as three tensor-core products accumulated in fp32,
-//     A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi      (Alo.Blo ~ 2^-22 |A.B| dropped)
-// so the layer error is ~2^-21 relative instead of tf32's 2^-11.
+// operand is split into a tf32 head and a tf32 tail, v = hi + lo, and each
+// dense layer runs as three tensor-core products accumulated in fp32,
+//     A.B ~= Ahi.Bhi + Ahi.Blo + Alo.Bhi      (Alo.Blo ~ 2^-20 |A.B| dropped)
+// so the layer error is ~2^-19 relative instead of tf32's 2^-10.
+// kind::tf32 TRUNCATES its fp32 operands to tf32 (measured,
+// tools/tf32_rounding_probe.py), so the raw fp32 X tile in shared memory IS
+// Xhi = trunc(X) for the MMA, and only Xlo = X - trunc(X) (exact in fp32) has
+// to be formed: by the converter warps, into TMEM operand slots.
 //
-//   warp 0      TMA producer: raw fp32 X atoms into an NST-stage ring
-//   warp 1      TMEM allocator + MMA issuer (3 MMAs per K step)
-//   warps 2..5  converters: one TMEM lane (tile row) per thread -- read the
-//               row's 32 values of an X atom from shared memory, split, and
-//               store hi | lo (32 + 32 columns) into a TMEM operand slot
-//               (GEMM1's A operands come from TMEM); the X stage is released
-//               as soon as it is read
-//   warps 6..13 epilogue: h1 = tanh(acc1 + b1) split into hi | lo in TMEM
-//               (GEMM2's A), then tanh(acc2 + b2) . W3 + b3 -> score.
+//   warp 0       TMA producer: raw fp32 X atoms into an NST-stage ring
+//   warp 1       TMEM allocator + GEMM1 issuer: per K step
+//                  [acc1a | acc1b] += X.[W1hi | W1lo]   (one N = 128 MMA,
+//                                                     A = X atom in smem)
+//                  acc1a += Xlo.W1hi                     (A = Xlo in TMEM)
+//                the epilogue adds the two halves
+//   warp 2       GEMM2 issuer: [acc2a | acc2b] = h1hi.[W2hi | W2lo] (N = 128),
+//                acc2a += h1lo.W2hi
+//                (its own warp, so a ready tile's GEMM2 does not queue behind
+//                the issue of the next tiles' GEMM1)
+//   warps 3..10  converters: two per TMEM lane quarter, thread = tile row,
+//                16 columns of the atom each: Xlo -> TMEM slot
+//   warps 11..18 epilogue: h1 = tanh(acc1 + b1) -> (h1hi | h1lo) in place,
+//                then tanh(acc2 + b2) . W3 + b3 -> score.
 // Activations use the accurate exp-based tanh of the fp32 CUDA-core kernel
 // (Act<float>::tanh), not tanh.approx.
-// TMEM: 2 operand slots x 64 columns + 2 tile buffers x 192 columns
-// (acc1 -> h1hi | h1lo | acc2) = 512.
+// TMEM (512 columns): 4 Xlo slots x 32 | 2 tile buffers x 128 (acc1a |
+// acc1b -> h1hi | h1lo in place) | 1 acc2a | acc2b x 128 (read out right
+// away by the epilogue).
 constexpr int kX3Nst = 5;
-constexpr int kX3Slots = 2;
+constexpr int kX3Slots = 4;
 constexpr int kX3Bufs = 2;
-constexpr int kX3Threads = 448;
+constexpr int kX3Threads = 608;
+constexpr int kX3Conv = 256;  // converter threads
 
-__device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
-  // round to the nearest tf32 (10 explicit mantissa bits), ties away from zero
-  const uint32_t u = __float_as_uint(v);
-  hi = __uint_as_float((u + 0x1000u) & 0xffffe000u);
-  lo = v - hi;
+__device__ __forceinline__ float trunc_tf32(float v) {
+  return __uint_as_float(__float_as_uint(v) & 0xffffe000u);
 }
 
 struct __align__(8) X3Bars {
   uint64_t full[kX3Nst], empty[kX3Nst];
   uint64_t op_full[kX3Slots], op_free[kX3Slots];
-  uint64_t acc1_full[kX3Bufs], h1_full[kX3Bufs], acc2_full[kX3Bufs], acc_free[kX3Bufs];
+  uint64_t acc1_full[kX3Bufs], h1_full[kX3Bufs], buf_free[kX3Bufs];
+  uint64_t acc2_full, acc2_free;
   uint32_t tmem_base;
 };
 
@@ -272,14 +280,12 @@ __global__ void __launch_bounds__(kX3Threads, 1)
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* xs = base;                                  // [NST] X atoms
-  unsigned char* w1h = xs + kX3Nst * kAtomBytesX;            // [kat] W1 hi atoms
-  unsigned char* w1l = w1h + p.kat * kAtomBytesW;            // [kat] W1 lo atoms
-  unsigned char* w2h = w1l + p.kat * kAtomBytesW;            // [2]
-  unsigned char* w2l = w2h + 2 * kAtomBytesW;                // [2]
-  X3Bars* bars = reinterpret_cast<X3Bars*>(w2l + 2 * kAtomBytesW);
+  unsigned char* w1s = xs + kX3Nst * kAtomBytesX;            // [kat] [W1hi | W1lo]^T atoms (128 rows)
+  unsigned char* w2s = w1s + p.kat * 2 * kAtomBytesW;        // [2] [W2hi | W2lo]^T atoms (128 rows)
+  X3Bars* bars = reinterpret_cast<X3Bars*>(w2s + 4 * kAtomBytesW);
   __shared__ float s_b1[kTcHid], s_b2[kTcHid], s_w3[kTcHid];
   __shared__ float s_b3;
-  __shared__ float s_part[kX3Bufs][2][kTcRows];
+  __shared__ float s_part[2][2][kTcRows];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_tiles = (p.n + kTcRows - 1) / kTcRows;
@@ -291,38 +297,38 @@ __global__ void __launch_bounds__(kX3Threads, 1)
     prefetch_tmap(&tmap_x);
     for (int s = 0; s < kX3Nst; ++s) {
       mbar_init(&bars->full[s], 1);
-      mbar_init(&bars->empty[s], 128);
+      mbar_init(&bars->empty[s], kX3Conv + 1);  // converters read it + the MMAs retire
     }
     for (int s = 0; s < kX3Slots; ++s) {
-      mbar_init(&bars->op_full[s], 128);
+      mbar_init(&bars->op_full[s], kX3Conv);
       mbar_init(&bars->op_free[s], 1);
     }
     for (int b = 0; b < kX3Bufs; ++b) {
       mbar_init(&bars->acc1_full[b], 1);
       mbar_init(&bars->h1_full[b], 256);
-      mbar_init(&bars->acc2_full[b], 1);
-      mbar_init(&bars->acc_free[b], 256);
+      mbar_init(&bars->buf_free[b], 1);
     }
+    mbar_init(&bars->acc2_full, 1);
+    mbar_init(&bars->acc2_free, 256);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(&bars->tmem_base);
-  // weights: hi / lo halves, K-major SW128 (W^T rows = hidden unit n)
+  // weights: hi = trunc_tf32(w) (what the MMA sees of w anyway), lo = w - hi
   for (int i = threadIdx.x; i < p.kat * 32 * kTcHid; i += kX3Threads) {
     const int nrow = i % kTcHid, k = i / kTcHid;
     const float v = k < F ? p.prm[(int64_t)k * kTcHid + nrow] : 0.0f;
-    float hi, lo;
-    split_tf32(v, hi, lo);
-    const uint32_t off = (k >> 5) * kAtomBytesW + sw128_offset(nrow, k & 31);
-    *reinterpret_cast<float*>(w1h + off) = hi;
-    *reinterpret_cast<float*>(w1l + off) = lo;
+    const float hi = trunc_tf32(v);
+    unsigned char* atom = w1s + (k >> 5) * 2 * kAtomBytesW;
+    *reinterpret_cast<float*>(atom + sw128_offset(nrow, k & 31)) = hi;
+    *reinterpret_cast<float*>(atom + sw128_offset(nrow + kTcHid, k & 31)) = v - hi;
   }
   for (int i = threadIdx.x; i < kTcHid * kTcHid; i += kX3Threads) {
     const int nrow = i % kTcHid, k = i / kTcHid;
-    float hi, lo;
-    split_tf32(p.prm[oW2 + (int64_t)k * kTcHid + nrow], hi, lo);
-    const uint32_t off = (k >> 5) * kAtomBytesW + sw128_offset(nrow, k & 31);
-    *reinterpret_cast<float*>(w2h + off) = hi;
-    *reinterpret_cast<float*>(w2l + off) = lo;
+    const float v = p.prm[oW2 + (int64_t)k * kTcHid + nrow];
+    const float hi = trunc_tf32(v);
+    unsigned char* atom = w2s + (k >> 5) * 2 * kAtomBytesW;
+    *reinterpret_cast<float*>(atom + sw128_offset(nrow, k & 31)) = hi;
+    *reinterpret_cast<float*>(atom + sw128_offset(nrow + kTcHid, k & 31)) = v - hi;
   }
   for (int i = threadIdx.x; i < kTcHid; i += kX3Threads) {
     s_b1[i] = p.prm[ob1 + i];
@@ -335,11 +341,11 @@ __global__ void __launch_bounds__(kX3Threads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = bars->tmem_base;
-  // column map: operand slot s at [64 s, 64 s + 64) (hi | lo);
-  // tile buffer b at 128 + 192 b: acc1/h1hi [0,64) h1lo [64,128) acc2 [128,192)
-  constexpr uint32_t kOpCols = 64, kBufBase = kX3Slots * kOpCols, kBufCols = 192;
+  constexpr uint32_t kOpCols = 32, kBufBase = kX3Slots * kOpCols, kBufCols = 128;
+  constexpr uint32_t kAcc2 = kBufBase + kX3Bufs * kBufCols;  // 384
   const uint32_t my_tiles =
       (uint32_t)(n_tiles > blockIdx.x ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
+  constexpr uint32_t idesc = idesc_tf32(kTcRows, kTcHid);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -355,53 +361,63 @@ __global__ void __launch_bounds__(kX3Threads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(kTcRows, kTcHid);
-      const uint32_t w1ha = smem_u32(w1h), w1la = smem_u32(w1l), w2ha = smem_u32(w2h),
-                     w2la = smem_u32(w2l);
+      constexpr uint32_t idesc2 = idesc_tf32(kTcRows, 2 * kTcHid);
+      const uint32_t xa = smem_u32(xs), w1a = smem_u32(w1s);
       uint32_t it = 0;
-      auto gemm1 = [&](uint32_t t) {
+      for (uint32_t t = 0; t < my_tiles; ++t) {
         const uint32_t b = t % kX3Bufs, bph = (t / kX3Bufs) & 1;
         const uint32_t acc1 = tmem + kBufBase + b * kBufCols;
-        mbar_wait(&bars->acc_free[b], bph ^ 1);
+        mbar_wait(&bars->buf_free[b], bph ^ 1);
         tc_fence_after();
         for (int kc = 0; kc < p.kat; ++kc, ++it) {
-          const uint32_t s = it % kX3Slots, ph = (it / kX3Slots) & 1;
-          mbar_wait(&bars->op_full[s], ph);
+          const uint32_t s = it % kX3Nst, ph = (it / kX3Nst) & 1;
+          const uint32_t os = it % kX3Slots, oph = (it / kX3Slots) & 1;
+          mbar_wait(&bars->full[s], ph);
+          mbar_wait(&bars->op_full[os], oph);
           tc_fence_after();
-          const uint32_t ahi = tmem + s * kOpCols, alo = ahi + 32;
+          const uint32_t alo = tmem + os * kOpCols;
+          // K steps of 8 that hold real columns (the last atom of F = 164
+          // has 4: one step instead of four)
+          const int ksteps = min(4, (F - kc * 32 + 7) >> 3);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t bh = sw128_desc(w1ha + kc * kAtomBytesW + kk * 32);
-            const uint64_t bl = sw128_desc(w1la + kc * kAtomBytesW + kk * 32);
-            mma_tf32_ts(acc1, ahi + kk * 8, bh, idesc, (kc | kk) != 0);
-            mma_tf32_ts(acc1, ahi + kk * 8, bl, idesc, 1);
-            mma_tf32_ts(acc1, alo + kk * 8, bh, idesc, 1);
+            if (kk >= ksteps) break;
+            const uint64_t ad = sw128_desc(xa + s * kAtomBytesX + kk * 32);
+            const uint64_t bd = sw128_desc(w1a + kc * 2 * kAtomBytesW + kk * 32);
+            mma_tf32_ss(acc1, ad, bd, idesc2, (kc | kk) != 0);     // rows 0-63: W1hi, 64-127: W1lo
+            mma_tf32_ts(acc1, alo + kk * 8, bd, idesc, 1);          // first 64 rows = W1hi
           }
-          mma_commit(&bars->op_free[s]);
+          mma_commit(&bars->empty[s]);
+          mma_commit(&bars->op_free[os]);
         }
         mma_commit(&bars->acc1_full[b]);
-      };
-      if (my_tiles > 0) gemm1(0);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      constexpr uint32_t idesc2 = idesc_tf32(kTcRows, 2 * kTcHid);
+      const uint32_t w2a = smem_u32(w2s);
+      const uint32_t acc2 = tmem + kAcc2;
       for (uint32_t t = 0; t < my_tiles; ++t) {
-        if (t + 1 < my_tiles) gemm1(t + 1);
         const uint32_t b = t % kX3Bufs, bph = (t / kX3Bufs) & 1;
-        const uint32_t hhi = tmem + kBufBase + b * kBufCols, hlo = hhi + 64, acc2 = hhi + 128;
+        const uint32_t hhi = tmem + kBufBase + b * kBufCols, hlo = hhi + 64;
         mbar_wait(&bars->h1_full[b], bph);
+        mbar_wait(&bars->acc2_free, (t & 1) ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t woff = (kk >> 2) * kAtomBytesW + (kk & 3) * 32;
-          const uint64_t bh = sw128_desc(w2ha + woff), bl = sw128_desc(w2la + woff);
-          mma_tf32_ts(acc2, hhi + kk * 8, bh, idesc, kk != 0);
-          mma_tf32_ts(acc2, hhi + kk * 8, bl, idesc, 1);
-          mma_tf32_ts(acc2, hlo + kk * 8, bh, idesc, 1);
+          const uint64_t bd = sw128_desc(w2a + (kk >> 2) * 2 * kAtomBytesW + (kk & 3) * 32);
+          mma_tf32_ts(acc2, hhi + kk * 8, bd, idesc2, kk != 0);  // [W2hi | W2lo]
+          mma_tf32_ts(acc2, hlo + kk * 8, bd, idesc, 1);         // W2hi rows
         }
-        mma_commit(&bars->acc2_full[b]);
+        mma_commit(&bars->acc2_full);
+        mma_commit(&bars->buf_free[b]);  // h1 consumed: the buffer may take a new acc1
       }
     }
-  } else if (warp < 6) {
-    // converters: thread = tile row (TMEM lane); 32 values per X atom
+  } else if (warp < 11) {
+    // converters: two warps per lane quarter, 16 columns of the atom each
     const int quarter = warp & 3;
+    const int hc = (warp - 3) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     uint32_t it = 0;
@@ -411,50 +427,49 @@ __global__ void __launch_bounds__(kX3Threads, 1)
         const uint32_t os = it % kX3Slots, oph = (it / kX3Slots) & 1;
         mbar_wait(&bars->full[s], ph);
         const unsigned char* atom = xs + s * kAtomBytesX;
-        float hv[32], lv[32];
+        float lv[16];
 #pragma unroll
-        for (int c4 = 0; c4 < 8; ++c4) {
-          const float4 v = *reinterpret_cast<const float4*>(atom + sw128_offset(row, c4 * 4));
-          split_tf32(v.x, hv[4 * c4 + 0], lv[4 * c4 + 0]);
-          split_tf32(v.y, hv[4 * c4 + 1], lv[4 * c4 + 1]);
-          split_tf32(v.z, hv[4 * c4 + 2], lv[4 * c4 + 2]);
-          split_tf32(v.w, hv[4 * c4 + 3], lv[4 * c4 + 3]);
+        for (int c4 = 0; c4 < 4; ++c4) {
+          const float4 v = *reinterpret_cast<const float4*>(atom + sw128_offset(row, hc * 16 + c4 * 4));
+          lv[4 * c4 + 0] = v.x - trunc_tf32(v.x);
+          lv[4 * c4 + 1] = v.y - trunc_tf32(v.y);
+          lv[4 * c4 + 2] = v.z - trunc_tf32(v.z);
+          lv[4 * c4 + 3] = v.w - trunc_tf32(v.w);
         }
-        mbar_arrive(&bars->empty[s]);  // the X stage is free for the next TMA
+        mbar_arrive(&bars->empty[s]);
         mbar_wait(&bars->op_free[os], oph ^ 1);
         tc_fence_after();
-        const uint32_t dst = tmem + lane_off + os * kOpCols;
-        tmem_st16(dst, *reinterpret_cast<const float(*)[16]>(hv));
-        tmem_st16(dst + 16, *reinterpret_cast<const float(*)[16]>(hv + 16));
-        tmem_st16(dst + 32, *reinterpret_cast<const float(*)[16]>(lv));
-        tmem_st16(dst + 48, *reinterpret_cast<const float(*)[16]>(lv + 16));
+        tmem_st16(tmem + lane_off + os * kOpCols + hc * 16, lv);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&bars->op_full[os]);
       }
     }
   } else {
-    // epilogue: warps 6..13, two per lane quarter, column half hf
+    // epilogue: warps 11..18, two per lane quarter, column half hf
     const int quarter = warp & 3;
-    const int hf = (warp - 6) >> 2;
+    const int hf = (warp - 11) >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t acc2 = tmem + lane_off + kAcc2;
     uint32_t t = 0;
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++t) {
       const uint32_t b = t % kX3Bufs, bph = (t / kX3Bufs) & 1;
       const uint32_t acc1 = tmem + lane_off + kBufBase + b * kBufCols;
-      const uint32_t hlo = acc1 + 64, acc2 = acc1 + 128;
+      const uint32_t hlo = acc1 + 64;
       mbar_wait(&bars->acc1_full[b], bph);
       tc_fence_after();
 #pragma unroll
       for (int c0 = hf * 32; c0 < hf * 32 + 32; c0 += 16) {
         float v[16], lo[16];
         tmem_ld16(acc1 + c0, v);
+        tmem_ld16(hlo + c0, lo);   // acc1b = X.W1lo
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float h = Act<float>::tanh(v[i] + s_b1[c0 + i]);
-          split_tf32(h, v[i], lo[i]);
+          const float h = Act<float>::tanh((v[i] + lo[i]) + s_b1[c0 + i]);
+          v[i] = trunc_tf32(h);
+          lo[i] = h - v[i];
         }
         tmem_st16(acc1 + c0, v);
         tmem_st16(hlo + c0, lo);
@@ -462,23 +477,25 @@ __global__ void __launch_bounds__(kX3Threads, 1)
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bars->h1_full[b]);
-      mbar_wait(&bars->acc2_full[b], bph);
+      mbar_wait(&bars->acc2_full, t & 1);
       tc_fence_after();
+      float a2[32], b2[32];
+      tmem_ld16(acc2 + hf * 32, *reinterpret_cast<float(*)[16]>(a2));
+      tmem_ld16(acc2 + hf * 32 + 16, *reinterpret_cast<float(*)[16]>(a2 + 16));
+      tmem_ld16(acc2 + 64 + hf * 32, *reinterpret_cast<float(*)[16]>(b2));
+      tmem_ld16(acc2 + 64 + hf * 32 + 16, *reinterpret_cast<float(*)[16]>(b2 + 16));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&bars->acc2_free);  // acc2 read out: the next tile's GEMM2 may write it
       float acc = 0.f;
 #pragma unroll
-      for (int c0 = hf * 32; c0 < hf * 32 + 32; c0 += 16) {
-        float v[16];
-        tmem_ld16(acc2 + c0, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc = fmaf(Act<float>::tanh(v[i] + s_b2[c0 + i]), s_w3[c0 + i], acc);
-      }
-      tc_fence_before();
-      mbar_arrive(&bars->acc_free[b]);
-      s_part[b][hf][row] = acc;
+      for (int i = 0; i < 32; ++i)
+        acc = fmaf(Act<float>::tanh((a2[i] + b2[i]) + s_b2[hf * 32 + i]), s_w3[hf * 32 + i], acc);
+      const int pb = t & 1;
+      s_part[pb][hf][row] = acc;
       named_barrier(1, 256);
       const int64_t r = tile * kTcRows + row;
-      if (hf == 0 && r < p.n) p.out[r] = (s_part[b][0][row] + s_part[b][1][row]) + s_b3;
+      if (hf == 0 && r < p.n) p.out[r] = (s_part[pb][0][row] + s_part[pb][1][row]) + s_b3;
     }
   }
   __syncthreads();
@@ -546,7 +563,7 @@ int mlp_predict_tc(const float* prm, const float* X, int64_t n, int F, float* ou
 
 static size_t x3_smem_bytes(int kat) {
   return 1024 + (size_t)kX3Nst * kAtomBytesX + (size_t)(2 * kat + 4) * kAtomBytesW + sizeof(X3Bars) + 64;
-}
+}  // W1: kat atoms of 128 rows (= 2 kat 64-row atoms); W2 hi + lo: 4 atoms
 
 // 1 if the split-precision tensor-core scorer covers this shape
 int mlp_x3_eligible(int F, const float* X) {
