@@ -58,25 +58,32 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
-def build_host(force: bool = False) -> str:
-    """The CPython host module (csrc/host/tt_pack.c -> _ttpack*.so, gcc -O3)."""
+def _build_host_module(name: str, src_name: str, force: bool, numpy_inc: bool) -> str:
     import sysconfig
 
-    src = os.path.join(CSRC, "host", "tt_pack.c")
-    out = os.path.join(PKG, "_ttpack" + sysconfig.get_config_var("EXT_SUFFIX"))
+    src = os.path.join(CSRC, "host", src_name)
+    out = os.path.join(PKG, name + sysconfig.get_config_var("EXT_SUFFIX"))
     if not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src):
         return out
     cc = os.environ.get("CC") or shutil.which("gcc") or "cc"
-    import numpy
+    cmd = [cc, "-O3", "-shared", "-fPIC", "-Wall", "-pthread", "-I", sysconfig.get_paths()["include"]]
+    if numpy_inc:
+        import numpy
 
-    cmd = [cc, "-O3", "-shared", "-fPIC", "-Wall", "-pthread", "-I", sysconfig.get_paths()["include"],
-           "-I", numpy.get_include(), src,
-           "-o", out + ".tmp"]
+        cmd += ["-I", numpy.get_include()]
+    cmd += [src, "-o", out + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"host module build failed:\n{r.stdout}\n{r.stderr}")
+        raise RuntimeError(f"host module {name} build failed:\n{r.stdout}\n{r.stderr}")
     os.replace(out + ".tmp", out)
     return out
+
+
+def build_host(force: bool = False) -> str:
+    """The CPython host modules: csrc/host/tt_pack.c -> _ttpack (K9 packer) and
+    csrc/host/tt_jsonl.c -> _ttjsonl (dataset record codec), gcc -O3."""
+    _build_host_module("_ttjsonl", "tt_jsonl.c", force, numpy_inc=False)
+    return _build_host_module("_ttpack", "tt_pack.c", force, numpy_inc=True)
 
 
 def build(verbose: bool = False, force: bool = False) -> str:

@@ -21,6 +21,9 @@ the search scorer (models.py:364-378) and the CLI -- through the kernels:
   tensortune.search / .cli / tensortune
       tune                                       -> search.tune (cross-task
                                                     batched scoring, f2)
+  tensortune.data / .cli / .models / tensortune
+      loads/load/dumps/save_dataset              -> dataio (native record
+                                                    codec, f4)
 
 ``uninstall()`` restores the originals.
 """
@@ -32,6 +35,7 @@ import sys
 import numpy as np
 
 from . import estimators as _est
+from . import dataio as _dataio
 from . import featurize as _feat
 from . import gbdt as _gbdt
 from . import metrics as _met
@@ -130,6 +134,13 @@ def install() -> None:
         _patch(sys.modules.get(key), "make_schedule_scorer", _search.make_schedule_scorer)
     for key in ("tensortune.search", "tensortune.cli", "tensortune"):
         _patch(sys.modules.get(key), "tune", _search.tune)
+    # dataset I/O (f4): the native record codec behind the reference's names
+    import tensortune.data  # noqa: F401
+
+    _dataio.bind_reference()
+    for name in ("loads_dataset", "load_dataset", "dumps_dataset", "save_dataset"):
+        for key in ("tensortune.data", "tensortune.cli", "tensortune.models", "tensortune"):
+            _patch(sys.modules.get(key), name, getattr(_dataio, name))
     import tensortune.features as features
 
     enc_seq, enc_flat = _feat.make_encoders(features)
