@@ -16,7 +16,10 @@
 //   row threads   tcgen05.ld the row's 128 gate pre-activations per
 //                 direction, + bias, sigmoid/tanh, cell update (c in
 //                 registers), h -> TMEM (next step's A) and the layer output
-//                 (L2 scratch); programs shorter than the tile hold state
+//                 (L2 scratch, fp16: the tf32 MMA keeps 10 mantissa bits of
+//                 it anyway; 48 MB for 148 tiles of 128 x 10 steps instead of
+//                 97 MB, so it stays in L2 instead of being written back to
+//                 HBM); programs shorter than the tile hold state
 //                 (tuner.py:97-98 masked hold).
 // Attention per pass (tuner.py:259-274) without materialising K and V:
 //   q = pooled Wq + bq ; r_h = Wk[:, h] q_h          (two GEMMs)
@@ -29,6 +32,8 @@
 // mode with its own stated tolerance (tests/test_gpu_tuner_tc.py); the
 // CUDA-core kernel (tt_tuner.cu) is the strict fp32 path.
 #define TT_TC_TANH_APPROX 1
+#include <cuda_fp16.h>
+
 #include "tt_sm100.cuh"
 #include "tt_tuner.cuh"
 
@@ -91,9 +96,9 @@ struct ScArgs {
   const float* ctx;
   int64_t n;
   float* yhat;
-  float* scratch;       // per CTA: [2][128][Tmax][64] layer outputs (ping-pong)
+  __half* scratch;      // per CTA: [2][128][Tmax][64] layer outputs (ping-pong, fp16)
   const unsigned char* img;  // prepared B^T images (tuner_tc_prepare_kernel)
-  int64_t scr_per_cta;  // floats
+  int64_t scr_per_cta;  // halves
 };
 
 struct __align__(8) ScBars {
@@ -143,12 +148,35 @@ __device__ __forceinline__ float4 ld_keep(const float* g, uint64_t pol) {
                : "l"(g), "l"(pol));
   return v;
 }
-// the next step's 256-B layer-output row into L1 ahead of its loads (the
+__device__ __forceinline__ void st_keep_u4(void* g, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(g), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_keep_u4(const void* g, uint64_t pol) {
+  uint4 v;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(g), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_h2(uint32_t u) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&u));
+}
+// 8 fp16 layer-output values (16 B) -> fp32
+__device__ __forceinline__ void h8_to_f(uint4 u, float* f) {
+  const float2 a = unpack_h2(u.x), b = unpack_h2(u.y), c = unpack_h2(u.z), d = unpack_h2(u.w);
+  f[0] = a.x, f[1] = a.y, f[2] = b.x, f[3] = b.y, f[4] = c.x, f[5] = c.y, f[6] = d.x, f[7] = d.y;
+}
+// the next step's 128-B layer-output row into L1 ahead of its loads (the
 // per-row attention loops otherwise wait one L2 round trip per step)
 constexpr int kPf = 1;  // rows prefetched ahead (deeper measured no better)
-__device__ __forceinline__ void prefetch_row_l1(const float* g) {
+__device__ __forceinline__ void prefetch_row_l1(const __half* g) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(g));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(g + 32));
 }
 __device__ __forceinline__ void cp_async16_keep(float* s, const float* g, uint64_t pol) {
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(s)),
@@ -274,7 +302,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
   uint32_t ph = 0;
   uint32_t pd[2] = {0, 0};  // phase bits of the per-direction LSTM hand-offs
   const uint64_t pol_keep = l2_keep_policy();
-  float* scr0 = a.scratch + (int64_t)blockIdx.x * a.scr_per_cta;
+  __half* scr0 = a.scratch + (int64_t)blockIdx.x * a.scr_per_cta;
 
   // one GEMM hand-off: row threads have written A; the MMA lane issues.
   auto gemm = [&](uint32_t d, uint32_t aa, uint32_t b_smem, int N, int K) {
@@ -343,24 +371,25 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
       for (int d = 0; d < 2; ++d)
         for (int i = threadIdx.x; i < kG; i += blockDim.x) sbias[d * kG + i] = __ldg(a.prm + dm.bb[l][d] + i);
       __syncthreads();
-      const float* xin = scr0 + (int64_t)((l - 1) & 1) * kRows * TM * kD + (int64_t)row * TM * kD;
-      float* xout = scr0 + (int64_t)(l & 1) * kRows * TM * kD + (int64_t)row * TM * kD;
+      const __half* xin = scr0 + (int64_t)((l - 1) & 1) * kRows * TM * kD + (int64_t)row * TM * kD;
+      __half* xout = scr0 + (int64_t)(l & 1) * kRows * TM * kD + (int64_t)row * TM * kD;
       // x row of direction d at step s (zeros past the program's end):
       // layer 0 reads the raw step row into registers; layers >= 1 copy the
       // previous layer's output row into this thread's shared-memory slot
       // with async 16-B copies (issued one half-step ahead, no registers).
-      float* xslot = sxs + (int64_t)row * 2 * kD;
+      float* xslot = sxs + (int64_t)row * 2 * kD;  // per direction 64 fp16 (128 B) used
       auto fetch_x = [&](int d, int s) {
         if (l == 0) return;
         const bool ok = live && s < T;
         float* dst = xslot + d * kD;
         if (ok) {
-          const float* src = xin + (int64_t)(d == 0 ? s : T - 1 - s) * kD;
+          const __half* src = xin + (int64_t)(d == 0 ? s : T - 1 - s) * kD;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) cp_async16_keep(dst + 4 * q, src + 4 * q, pol_keep);
+          for (int q = 0; q < 8; ++q)
+            cp_async16_keep(dst + 4 * q, reinterpret_cast<const float*>(src + 8 * q), pol_keep);
         } else {
 #pragma unroll
-          for (int q = 0; q < 16; ++q) reinterpret_cast<float4*>(dst)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = 0; q < 8; ++q) reinterpret_cast<uint4*>(dst)[q] = make_uint4(0u, 0u, 0u, 0u);
         }
         cp_async_commit();
       };
@@ -377,15 +406,12 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           }
         } else {
           cp_async_wait0();
-          const float4* x4 = reinterpret_cast<const float4*>(xslot + d * kD);
+          const uint4* x8 = reinterpret_cast<const uint4*>(xslot + d * kD);
 #pragma unroll
           for (int j0 = 0; j0 < kD; j0 += 16) {
             float v[16];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const float4 f = x4[j0 / 4 + q];
-              v[4 * q] = f.x, v[4 * q + 1] = f.y, v[4 * q + 2] = f.z, v[4 * q + 3] = f.w;
-            }
+            h8_to_f(x8[j0 / 8], v);
+            h8_to_f(x8[j0 / 8 + 1], v + 8);
             tmem_st16(Ad + j0, v);
           }
         }
@@ -421,7 +447,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           tc_fence_after();
           TC_MARK(pms, 24);
           const int t = d == 0 ? s : T - 1 - s;
-          float* orow = xout + (int64_t)t * kD + d * kH;
+          __half* orow = xout + (int64_t)t * kD + d * kH;
 #pragma unroll
           for (int j0 = 0; j0 < kH; j0 += 16) {
             float gi[16], gf[16], gg[16], go[16], cc[16], h[16];
@@ -445,9 +471,11 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
             tmem_st16(Ad + kx + j0, h);
             if (valid) {
 #pragma unroll
-              for (int q = 0; q < 4; ++q)
-                st_keep(orow + j0 + 4 * q, make_float4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]),
-                        pol_keep);
+              for (int q = 0; q < 2; ++q)
+                st_keep_u4(orow + j0 + 8 * q,
+                           make_uint4(pack_h2(h[8 * q], h[8 * q + 1]), pack_h2(h[8 * q + 2], h[8 * q + 3]),
+                                      pack_h2(h[8 * q + 4], h[8 * q + 5]), pack_h2(h[8 * q + 6], h[8 * q + 7])),
+                           pol_keep);
             }
           }
           if (s + 1 < Tt) {
@@ -476,7 +504,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
     // =========================================================== attention
     __syncthreads();
     const int L1 = (dm.L - 1) & 1;
-    const float* Srow = scr0 + (int64_t)L1 * kRows * TM * kD + (int64_t)row * TM * kD;
+    const __half* Srow = scr0 + (int64_t)L1 * kRows * TM * kD + (int64_t)row * TM * kD;
     // B layout: Wq^T | Bk^T | Bv^T | Wo^T | W1^T (image built by the prepare kernel)
     const int NK = heads * kD;  // r width and u width
     unsigned char* bq_t = Bs;
@@ -509,12 +537,14 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
       if (live) {
         for (int t = 0; t < kPf && t < T; ++t) prefetch_row_l1(Srow + (int64_t)t * kD);
         for (int t = 0; t < T; ++t) {
-          const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
+          const __half* sr = Srow + (int64_t)t * kD;
           if (t + kPf < T) prefetch_row_l1(Srow + (int64_t)(t + kPf) * kD);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const float4 f = ld_keep(reinterpret_cast<const float*>(sr + q), pol_keep);
-            pool[4 * q] += f.x, pool[4 * q + 1] += f.y, pool[4 * q + 2] += f.z, pool[4 * q + 3] += f.w;
+          for (int q = 0; q < 8; ++q) {
+            float f[8];
+            h8_to_f(ld_keep_u4(sr + 8 * q, pol_keep), f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) pool[8 * q + i] += f[i];
           }
         }
       }
@@ -562,16 +592,18 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           float mx = -INFINITY, sum = 0.f;
           for (int t = 0; t < kPf && t < T; ++t) prefetch_row_l1(Srow + (int64_t)t * kD);
           for (int t = 0; t < T; ++t) {
-            const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
+            const __half* sr = Srow + (int64_t)t * kD;
             if (t + kPf < T) prefetch_row_l1(Srow + (int64_t)(t + kPf) * kD);
             float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const float4 f = ld_keep(reinterpret_cast<const float*>(sr + q), pol_keep);
-              a0 = fmaf(f.x, r[4 * q], a0);
-              a1 = fmaf(f.y, r[4 * q + 1], a1);
-              a0 = fmaf(f.z, r[4 * q + 2], a0);
-              a1 = fmaf(f.w, r[4 * q + 3], a1);
+            for (int q = 0; q < 8; ++q) {
+              float f[8];
+              h8_to_f(ld_keep_u4(sr + 8 * q, pol_keep), f);
+#pragma unroll
+              for (int i = 0; i < 8; i += 2) {
+                a0 = fmaf(f[i], r[8 * q + i], a0);
+                a1 = fmaf(f[i + 1], r[8 * q + i + 1], a1);
+              }
             }
             const float v = (a0 + a1) / sq;
             lg[(t * kMaxHeads + grp) * kRows] = v;
@@ -587,15 +619,14 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
           for (int t = 0; t < kPf && t < T; ++t) prefetch_row_l1(Srow + (int64_t)t * kD);
           for (int t = 0; t < T; ++t) {
             const float al = lg[(t * kMaxHeads + grp) * kRows] / sum;
-            const float4* sr = reinterpret_cast<const float4*>(Srow + (int64_t)t * kD);
+            const __half* sr = Srow + (int64_t)t * kD;
             if (t + kPf < T) prefetch_row_l1(Srow + (int64_t)(t + kPf) * kD);
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
-              const float4 f = ld_keep(reinterpret_cast<const float*>(sr + q), pol_keep);
-              uvec[4 * q] = fmaf(al, f.x, uvec[4 * q]);
-              uvec[4 * q + 1] = fmaf(al, f.y, uvec[4 * q + 1]);
-              uvec[4 * q + 2] = fmaf(al, f.z, uvec[4 * q + 2]);
-              uvec[4 * q + 3] = fmaf(al, f.w, uvec[4 * q + 3]);
+            for (int q = 0; q < 8; ++q) {
+              float f[8];
+              h8_to_f(ld_keep_u4(sr + 8 * q, pol_keep), f);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) uvec[8 * q + i] = fmaf(al, f[i], uvec[8 * q + i]);
             }
           }
         }
@@ -677,7 +708,7 @@ static size_t sc_smem_bytes(int Tmax) {
 constexpr size_t kScImageBytes = 1u << 20;  // >= every LSTM image (L <= 8) + the attention image
 
 size_t tuner_predict_tc_ws(int Tmax) {
-  return (size_t)sm_count() * 2 * sc::kRows * Tmax * sc::kD * sizeof(float) + kScImageBytes;
+  return align_up((size_t)sm_count() * 2 * sc::kRows * Tmax * sc::kD * sizeof(__half), 1024) + kScImageBytes;
 }
 
 int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff, const float* ctx,
@@ -702,10 +733,10 @@ int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff
   a.ctx = ctx;
   a.n = n;
   a.yhat = yhat;
-  a.scratch = static_cast<float*>(ws);
+  a.scratch = static_cast<__half*>(ws);
   a.scr_per_cta = (int64_t)2 * sc::kRows * Tmax * sc::kD;
   unsigned char* img = static_cast<unsigned char*>(ws) +
-                       align_up((size_t)sm_count() * a.scr_per_cta * sizeof(float), 1024);
+                       align_up((size_t)sm_count() * a.scr_per_cta * sizeof(__half), 1024);
   TT_REQUIRE(sc_attn_image_off(a.dm) + sc_attn_image_bytes(a.dm) <= (int64_t)kScImageBytes - 1024,
              "tuner tf32 scoring: weight images exceed the workspace");
   a.img = img;

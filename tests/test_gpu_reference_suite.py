@@ -74,6 +74,8 @@ def run_ref_suite(module: str, precision: str, extra=(), timeout=3000):
                              or os.path.join(ROOT, "gpurun_out", "refsuite"))
     os.makedirs(logdir, exist_ok=True)
     tag = f"{os.path.basename(module)[:-3]}_{precision}"
+    if "-k" in extra:  # one log per selected acceptance criterion
+        tag += "_" + extra[list(extra).index("-k") + 1][:48]
     path = module if os.path.isabs(module) else os.path.join(REF_TESTS, module)
     calls = os.path.join(logdir, f"{tag}.calls.json")
     env = dict(os.environ)

@@ -1,7 +1,8 @@
 // Issue-rate peaks of the pipes the scoring / PCA kernels are bound by
 // (BASELINE.md §3 asks for the MUFU peak to be measured, not assumed):
-//   MUFU.TANH (tanh.approx.f32), MUFU.EX2 (ex2.approx.f32), MUFU.RCP
-//   (rcp.approx.f32), FP32 FFMA and FP64 DFMA -- ops/s for the whole GPU.
+//   MUFU.TANH (tanh.approx.f32), MUFU.EX2 (ex2.approx.f32), FP32 FFMA and
+//   FP64 DFMA -- ops/s for the whole GPU.  (The rcp chain v = 1/v is folded
+//   to a 2-cycle identity by the compiler and is not reported.)
 // Every thread runs 8 independent dependency chains (enough ILP to saturate
 // the pipe), all SMs x 8 CTAs x 256 threads, timed with CUDA events.
 // Note: cudaDevAttrClockRate reports the boost clock; the run's actual SM
