@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtt_b200.so")
+# TT_LIB overrides the library path (kernel-variant experiments, tools/)
+LIB_PATH = os.environ.get("TT_LIB") or os.path.join(_HERE, "libtt_b200.so")
 
 _P, _I32, _I64, _D, _SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_size_t
 

@@ -10,9 +10,12 @@ namespace tt {
 
 static int g_train_path = 0;  // 0 auto, 1 generic kernel only, 2 fast kernel only (tests)
 
+#ifndef TT_SCORE_P32
+#define TT_SCORE_P32 8
+#endif
 template <typename R>
 struct ScoreP {
-  static constexpr int value = sizeof(R) == 4 ? 8 : 4;  // programs per CTA tile
+  static constexpr int value = sizeof(R) == 4 ? TT_SCORE_P32 : 4;  // programs per CTA tile
 };
 
 // ----------------------------------------------------------- scoring --
