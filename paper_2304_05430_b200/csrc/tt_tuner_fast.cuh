@@ -35,6 +35,14 @@
 #include "tt_sm100.cuh"
 #include "tt_tuner_train.cuh"
 
+// 1: every LSTM layer >= 1 reads its weight block from shared memory and the
+// attention/head block lands during the last layer's recurrence (A/B on the
+// box: 55.05 -> 54.6 us per step, tools/ab_train.sh); 0: the round-1 layout
+// (the last layer reads L2 directly, the attention block lands a layer earlier)
+#ifndef TT_ATTN_LAST
+#define TT_ATTN_LAST 1
+#endif
+
 namespace tt {
 
 constexpr int kFH = 32, kFD = 64, kFG = 128;  // hidden, 2H, 4H
@@ -667,7 +675,14 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
   // Layers 1..L-2 read their block from W; layer 0 and the last layer read
   // L2 directly, so the attention block can be prefetched during layer L-2
   // (two recurrences to land).
+#if TT_ATTN_LAST
+  // every layer >= 1 reads its block from W (bulk-copied during the previous
+  // layer's recurrence); the attention/head block lands during the LAST
+  // layer's recurrence
+  const int att_l = dm.L - 1;
+#else
   const int att_l = dm.L >= 2 ? dm.L - 2 : 0;  // layer during which attention is prefetched
+#endif
   const int blk0 = (dm.d0 + kFH + 1) * kFG;     // layer-0 direction block (a.l0_smem)
   if (a.l0_smem && !a.s_frozen) {
     const uint32_t wph = s_wph;
@@ -712,8 +727,12 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
     for (int i = tid; i < T * kFD; i += kThreads) xs[i] = Sl[i];
   }
   for (int l = a.s_frozen ? dm.L : 0; l < dm.L; ++l) {
+#if TT_ATTN_LAST
+    const bool direct = l == 0;
+#else
     const bool direct = l == 0 || l == dm.L - 1;  // (the last layer's update was
                                                   //  awaited during layer att_l)
+#endif
     {
       // ---- input projection xz[dir][t][c] = b[c] + x_t Wx[:, c], thread = column
       const int dir = tid >> 7, c = tid & 127;
@@ -787,7 +806,11 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
       named_barrier(1, kThreads);
       // what this recurrence overlaps: layer l+1's block (if it reads W) or,
       // during layer att_l, the attention/head block
+#if TT_ATTN_LAST
+      const bool pf_lstm = l + 1 < dm.L;
+#else
       const bool pf_lstm = l + 1 < dm.L - 1;
+#endif
       const bool pf_attn = l == att_l;
       if (pf_lstm || pf_attn) {
         const int g = pf_lstm ? l + 1 : dm.L;
@@ -813,7 +836,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
           copy_attn(tid - 128, kThreads - 128);
           // the last layer reads L2 directly at its start: await its update
           // here, off the critical path
-          if (step > 0 && l + 1 == dm.L - 1) {
+          if (!TT_ATTN_LAST && step > 0 && l + 1 == dm.L - 1) {
             if (tid == 128) {
               const unsigned target = (unsigned)(step * group_jobs(dm, dm.L - 1));
               while (ld_acquire(a.ctr + ctr_adam(dm, dm.L - 1)) < target) {
@@ -826,7 +849,7 @@ __device__ float fast_sample_fwd(const FastArgs& a, float* sm, int64_t rs, int s
       if (l == dm.L - 1) cp_async_wait_all();
     }
     __syncthreads();
-    if (l + 1 < dm.L - 1) {
+    if (l + 1 < dm.L - (TT_ATTN_LAST ? 0 : 1)) {
       // the bulk copy issued during this layer's recurrence must have landed
       const uint32_t wph = s_wph;
       sm100::mbar_wait(&s_wbar, wph);
