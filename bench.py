@@ -441,6 +441,16 @@ def mlp_scoring(l2, stream, peaks, n=4 * 1024 * 1024, F=164):
     return out
 
 
+def allreduce_max(dist, x: float) -> float:
+    """MAX of one float over the ranks (a CUDA tensor under NCCL, CPU under gloo)."""
+    import torch
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    v = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(v, op=dist.ReduceOp.MAX)
+    return float(v.item())
+
+
 def sharded_extra(world, rank, dist, l2, stream, est, dims, flat):
     """Configs 3 and 4 across the ranks (SURVEY §8e, weak scaling): every rank
     scores its own 1 M-program shard (no collective on the data path), and the
@@ -453,9 +463,7 @@ def sharded_extra(world, rank, dist, l2, stream, est, dims, flat):
     from paper_2304_05430_b200.layout import DevicePrograms, HostPrograms
 
     def tmax(t):
-        v = torch.tensor([t], device="cuda")
-        dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        return float(v.item())
+        return allreduce_max(dist, t)
 
     out = {}
     st, of, cx, _, _ = synth(n_tasks=256, per_task=4096, seed=100 + rank)
@@ -716,9 +724,7 @@ def run_b200(args, world, rank):
         FusedDataParallelTuner.check_status(status)
     t_mean = float(np.mean(ms)) / 1e3
     if dist is not None:
-        tt = torch.tensor([t_mean], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_mean = float(tt.item())
+        t_mean = allreduce_max(dist, t_mean)
     value = world * n / t_mean
     flops = train_flops(lens)
     peaks = {}

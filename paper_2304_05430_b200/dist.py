@@ -265,7 +265,8 @@ class FusedDataParallelTuner:
                     owned.append((int(p.value), True))
             except Exception:  # noqa: BLE001
                 ok = False
-        flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device=_device.device())
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                            device=_device.device() if dist.get_backend(group) == "nccl" else "cpu")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
         if int(flag.item()) == 0:
             for ptr, mapped in owned:
