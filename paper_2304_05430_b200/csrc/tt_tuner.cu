@@ -29,7 +29,14 @@ static size_t score_smem_bytes(const TDims& d) {
 }
 
 template <typename R, int H, int P>
-__global__ void __launch_bounds__(kThreads, 2) tuner_predict_kernel(
+// CTAs per SM the scorer is compiled for: 3 for fp32 (80 registers, a few
+// hundred bytes of spills, but 24 warps per SM to hide the recurrence's
+// latency: 11.9 -> 14.0 M programs/s on the box; 1, 2 and 4 CTAs and tiles
+// of 4 / 16 programs measured slower), 2 for the fp64 parity build
+#ifndef TT_PRED_MINB
+#define TT_PRED_MINB (sizeof(R) == 4 ? 3 : 2)
+#endif
+__global__ void __launch_bounds__(kThreads, TT_PRED_MINB) tuner_predict_kernel(
     TDims dm, const R* __restrict__ prm, const R* __restrict__ steps,
     const int64_t* __restrict__ rowoff, const R* __restrict__ ctx, int64_t n,
     R* __restrict__ yhat, R* __restrict__ scratch, int64_t slot_elems, R* __restrict__ s_out) {
