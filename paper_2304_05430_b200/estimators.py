@@ -55,6 +55,27 @@ def _seq_widths() -> tuple[int, int]:
     return 6, 35
 
 
+class PerformanceWarning(UserWarning):
+    """A configuration runs on a slower (still exact) kernel."""
+
+
+def _warn_if_slow_path(dims, prec: str, max_steps: int, B: int) -> None:
+    """Say so when hidden-32 fp32 training leaves the latency-path kernel
+    (programs longer than its shared-memory caches hold, ~14 steps at the
+    default widths; the reference allows 32): the generic kernel is exact but
+    2.4-7x slower per step."""
+    if prec != "fp32" or dims["H"] != 32:
+        return
+    ok = _lib.load().tt_tuner_train_fast_eligible(dims["L"], dims["H"], dims["heads"], dims["U"], dims["d0"],
+                                                   dims["C"], int(max_steps), int(B))
+    if not ok:
+        import warnings
+
+        warnings.warn(f"training runs on the generic kernel (longest program {max_steps} steps, "
+                      f"minibatch {B}): exact, but 2.4-7x slower per step than the latency-path "
+                      "kernel", PerformanceWarning, stacklevel=3)
+
+
 def _bias_corrections(t0: int, n: int) -> np.ndarray:
     """(1 - b1^t, 1 - b2^t) for t = t0+1 .. t0+n, as optim.py:35-36 computes them."""
     out = np.empty(2 * n, dtype=np.float64)
@@ -412,6 +433,7 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         B = min(int(self.batch_size), n)
         if B > config.MAX_BATCH:
             raise DataValidationError(f"batch_size above {config.MAX_BATCH} is not supported")
+        _warn_if_slow_path(dims, prec, prog.max_steps, B)
         ev = None
         if eval_set is not None:
             eprog = DevicePrograms.from_sequences(eval_set[0], prec, dims["d0"], dims["C"])

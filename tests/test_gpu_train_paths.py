@@ -221,3 +221,23 @@ def test_heads_only_finetune_matches_oracle(cuda_ok, batch):
     for k in heads:
         err = np.linalg.norm(base.params_[k] - full.params_[k]) / max(np.linalg.norm(full.params_[k]), 1e-12)
         assert err <= (1e-3 if batch <= 16 else 1e-2), (k, err)
+
+
+def test_long_programs_warn_about_the_generic_kernel(cuda_ok):
+    """the 2.4-7x slowdown for programs longer than the latency
+    path's shared-memory caches was silent; it now says so (and stays exact)."""
+    import warnings
+
+    from conftest import random_seqs
+    from paper_2304_05430_b200 import RecurrentAttentionTuner
+    from paper_2304_05430_b200.estimators import PerformanceWarning
+
+    rng = np.random.default_rng(1)
+    short = random_seqs(rng, rng.integers(1, 8, size=24))
+    long_ = random_seqs(rng, [30] + list(rng.integers(1, 8, size=23)))
+    y = rng.uniform(0.1, 0.9, size=24)
+    with warnings.catch_warnings():
+        warnings.simplefilter("error", PerformanceWarning)
+        RecurrentAttentionTuner(epochs=1, batch_size=8).fit(short, y)
+    with pytest.warns(PerformanceWarning, match="generic kernel"):
+        RecurrentAttentionTuner(epochs=1, batch_size=8).fit(long_, y)
