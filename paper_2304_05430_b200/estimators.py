@@ -166,6 +166,7 @@ class _GpuParamsMixin:
     def __getstate__(self):
         state = dict(self.__dict__)
         state.pop("_dev", None)
+        state.pop("_pad_cache", None)
         return state
 
     def __setstate__(self, state):
@@ -552,16 +553,42 @@ class CostMLP(_GpuParamsMixin, BaseEstimator, RegressorMixin):
 
     def _predict_dev(self, Xd, n, F, flat=None):
         prec = self._prec()
+        cacheable = flat is None  # the model's own parameters (a training vector changes in place)
         flat = self._device_flat(list(self.NAMES)) if flat is None else flat
         out = _device.empty(n, _device.real_dtype(prec))
         fn = "tt_mlp_predict_f64" if prec == "fp64" else "tt_mlp_predict_f32"
-        if (F * 4) % 16 == 0 and prec in ("fp32", "tf32"):
-            # tcgen05 tensor-core paths (TMA needs 16-B rows): "fp32" = split
-            # tf32 (3 products, fp32 accuracy), "tf32" = plain tf32.  The
-            # choice depends on F only, never on n, so a row's score does not
-            # depend on its batch (search-time re-batching stays bit-exact).
+        if prec in ("fp32", "tf32") and F <= 256:
+            # tcgen05 tensor-core paths: "fp32" = split tf32 (3 products, fp32
+            # accuracy), "tf32" = plain tf32.  TMA needs 16-B rows, so a width
+            # like the reference's flat 47 is zero-padded on the device to the
+            # next multiple of 4 together with zero rows of W1 -- the extra
+            # products are exact zeros inside the same K step, so the scores
+            # equal an unpadded evaluation.  The choice depends on F only,
+            # never on n, so a row's score does not depend on its batch
+            # (search-time re-batching stays bit-exact).
             fn = "tt_mlp_predict_f32tc" if prec == "fp32" else "tt_mlp_predict_tf32"
+            if F % 4:
+                Fp = F + (4 - F % 4)
+                Xp = _device.zeros(n * Fp, Xd.dtype).view(n, Fp)
+                Xp[:, :F] = Xd.view(n, F)
+                Xd, flat, F = Xp.view(-1), self._padded_flat(flat, F, Fp, cacheable), Fp
         _lib.call(fn, flat.data_ptr(), Xd.data_ptr(), n, F, out.data_ptr(), _device.stream_ptr())
+        return out
+
+    def _padded_flat(self, flat, F, Fp, cacheable: bool):
+        """The parameter vector with W1 [F][64] extended by zero rows to
+        [Fp][64]; cached for the model's own device parameters (re-uploaded,
+        hence a new tensor, whenever the host weights change)."""
+        key = (flat.data_ptr(), flat._version, flat.numel(), F, Fp)
+        cache = self.__dict__.get("_pad_cache")
+        if cacheable and cache is not None and cache[0] == key and cache[2] is flat:
+            return cache[1]
+        t = _device.torch()
+        h = HIDDEN_WIDTH
+        pad = t.zeros((Fp - F) * h, dtype=flat.dtype, device=flat.device)
+        out = t.cat([flat[:F * h], pad, flat[F * h:]])
+        if cacheable:
+            self.__dict__["_pad_cache"] = (key, out, flat)
         return out
 
     def _launch_train(self, flat, m, v, Xd, yd, F, order, B, mode, lr, corr):

@@ -107,12 +107,15 @@ def test_mlp_tenset_width_scoring_fp32(cuda_ok):
 
 
 @pytest.mark.parametrize("n,F", [(1, 164), (127, 164), (128, 164), (129, 164), (70000, 164),
-                                 (300, 32), (257, 8), (1000, 100), (513, 4), (2000, 192)])
+                                 (300, 32), (257, 8), (1000, 100), (513, 4), (2000, 192),
+                                 (4096, 47), (129, 1), (300, 7), (1000, 163)])
 def test_mlp_fp32_tensor_core_scoring_meets_fp32_tolerance(cuda_ok, n, F):
     """The default fp32 scorer on tcgen05 (split tf32: hi/lo operands, three
     products per layer): same stated fp32 tolerance as the CUDA-core kernel
     (|d| <= 2e-5 vs the float64 reference), every tile/tail shape, and
-    bit-identical scores for a row whatever its batch (search re-batching)."""
+    bit-identical scores for a row whatever its batch (search re-batching).
+    Widths that are not a multiple of 4 (the reference's flat 47) are padded
+    with zeros on the device."""
     from paper_2304_05430_b200 import _lib
 
     rng = np.random.default_rng(n + F)
