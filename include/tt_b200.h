@@ -124,6 +124,23 @@ int tt_tuner_predict_tf32(const float *d_params, const float *d_steps,
                           int32_t step_width, int32_t ctx_len, int32_t max_steps,
                           float *d_yhat, void *d_ws, size_t ws_bytes, tt_stream_t stream);
 
+/* fp32-accurate tensor-core scoring (csrc/tt_tuner_x3.cu): the biLSTM stack
+ * as split-precision tcgen05 GEMMs (x.w = x_hi.w_hi + x_lo.w_hi + x_hi.w_lo,
+ * fp32 accumulation, the Act<float> activations of tt_tuner_predict_f32),
+ * then attention + head on the CUDA cores of tt_tuner_predict_f32.  Same
+ * signature and outputs as tt_tuner_predict_f32 (within its fp32 tolerance);
+ * a program's score does not depend on the batch it is scored in.
+ * tt_tuner_f32tc_eligible says whether the shapes are covered (hidden = 32,
+ * step_width <= 32). */
+size_t tt_tuner_predict_f32tc_workspace_bytes(int32_t layers, int32_t hidden, int32_t max_steps);
+int tt_tuner_f32tc_eligible(int32_t layers, int32_t hidden, int32_t heads, int32_t step_width,
+                            int32_t max_steps);
+int tt_tuner_predict_f32tc(const float *d_params, const float *d_steps,
+                           const int64_t *d_row_offsets, const float *d_ctx, int64_t n,
+                           int32_t layers, int32_t hidden, int32_t heads, int32_t unroll,
+                           int32_t step_width, int32_t ctx_len, int32_t max_steps,
+                           float *d_yhat, void *d_ws, size_t ws_bytes, tt_stream_t stream);
+
 /* Training (tuner.py:427-466) / gradients (tuner.py:364-376).
  * d_order lists sample indices; minibatch k is d_order[k*B, min((k+1)*B, n_order)).
  * TT_MODE_TRAIN: every minibatch runs forward, loss, backward, a deterministic

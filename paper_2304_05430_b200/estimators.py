@@ -296,6 +296,13 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         if prec == "tf32" and self._tc_eligible(dims, prog):
             fn = "tt_tuner_predict_tf32"  # tcgen05 tensor-core scoring
             nbytes = lib.tt_tuner_predict_tf32_workspace_bytes(prog.max_steps)
+        elif prec == "fp32" and lib.tt_tuner_f32tc_eligible(dims["L"], dims["H"], dims["heads"], dims["d0"],
+                                                             max(prog.max_steps, 1)):
+            # fp32 accuracy on the tensor cores: split-precision LSTM GEMMs +
+            # fp32 attention (csrc/tt_tuner_x3.cu); eligibility depends on the
+            # model's shapes only, so a score never depends on its batch
+            fn = "tt_tuner_predict_f32tc"
+            nbytes = lib.tt_tuner_predict_f32tc_workspace_bytes(dims["L"], dims["H"], max(prog.max_steps, 1))
         else:
             nbytes = lib.tt_tuner_predict_workspace_bytes(int(prec == "fp64"), dims["L"],
                                                           dims["H"], prog.max_steps)
