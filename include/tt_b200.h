@@ -257,6 +257,9 @@ int tt_debug_profile_step(int32_t step);
 int tt_debug_phase_times(int64_t *h_out, int32_t n);
 /* Debug aid: clock64 marks of the tensor-core scoring kernel's first tile. */
 int tt_debug_tc_phase_times(int64_t *h_out, int32_t n);
+/* Same for the fp32 tensor-core LSTM kernel (tt_tuner_x3.cu: layer 1,
+ * forward direction, steps 2 and 3 of CTA 0's first tile). */
+int tt_debug_x3_phase_times(int64_t *h_out, int32_t n);
 /* Same for the shared-memory CostMLP training kernel (clock64 of CTA 0,
  * thread 0, at its phase boundaries of minibatch 64 of the last launch). */
 int tt_debug_mlp_phase_times(int64_t *h_out, int32_t n);

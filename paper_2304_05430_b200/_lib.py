@@ -62,6 +62,7 @@ SIGNATURES: dict[str, tuple] = {
     "tt_debug_profile_step": (ctypes.c_int, [_I32]),
     "tt_debug_phase_times": (ctypes.c_int, [_P, _I32]),
     "tt_debug_tc_phase_times": (ctypes.c_int, [_P, _I32]),
+    "tt_debug_x3_phase_times": (ctypes.c_int, [_P, _I32]),
     "tt_debug_mlp_phase_times": (ctypes.c_int, [_P, _I32]),
     "tt_mlp_param_count": (_I64, [_I32]),
     "tt_mlp_predict_f32": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),

@@ -86,6 +86,16 @@ __global__ void __launch_bounds__(256) tuner_x3_prepare_kernel(TDims dm, const f
   }
 }
 
+// clock64 marks (debug aid, tt_debug_x3_phase_times): CTA 0, first tile,
+// layer 1, forward direction, steps 2 and 3 (9 marks each): row thread 0
+// [0] d_full [1] x_{s+1} arrived [2] gates loaded [3] activations done
+// [4] h arrived; MMA lane [5] x ready [6] (unused) [7] h ready [8] committed
+static __device__ long long g_x3_phase[32];
+#define X3_MARK(cond, i) \
+  do {                   \
+    if (cond) g_x3_phase[i] = clock64(); \
+  } while (0)
+
 struct X3Args {
   TDims dm;
   const float* prm;
@@ -95,6 +105,7 @@ struct X3Args {
   float* S;        // [n][Tmax][64]
   float* scratch;  // per CTA [128][Tmax][64]
   const unsigned char* img;
+  const int32_t* perm;  // program of each tile slot (x3_sort_kernel)
 };
 
 struct __align__(8) X3Bars {
@@ -112,6 +123,37 @@ __device__ __forceinline__ void cp_async4(float* s, const float* g) {
 __device__ __forceinline__ void cp_async_commit_x() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait_x() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ float rcp_approx(float x) {  // MUFU.RCP, <= 1 ulp
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2, flush-to-zero
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// LSTM cell from the gate pre-activations (tuner.py:86-96): 5 exponentials
+// and 3 reciprocals (two of them shared by a pair: 1/a = b/(ab), 1/b = a/(ab);
+// the clamps keep ab finite and move each activation by < 1e-18).
+__device__ __forceinline__ void lstm_cell(float zi, float zf, float zg, float zo, float& c, float& h) {
+  constexpr float kL = 43.f;       // e^43 squared < FLT_MAX
+  constexpr float kLog2e = 1.4426950408889634f;
+  const float ai = 1.f + ex2_approx(-kLog2e * fminf(fmaxf(zi, -kL), kL));
+  const float af = 1.f + ex2_approx(-kLog2e * fminf(fmaxf(zf, -kL), kL));
+  const float ag = 1.f + ex2_approx(2.f * kLog2e * fminf(fmaxf(zg, -0.5f * kL), 0.5f * kL));
+  const float ao = 1.f + ex2_approx(-kLog2e * fminf(fmaxf(zo, -kL), kL));
+  const float r1 = rcp_approx(ai * af);
+  const float r2 = rcp_approx(ag * ao);
+  const float gi = af * r1, gf = ai * r1;                // sigmoid(zi), sigmoid(zf)
+  const float gg = fma_rn(-2.f, ao * r2, 1.f), go = ag * r2;  // tanh(zg), sigmoid(zo)
+  c = fma_rn(gf, c, gi * gg);
+  const float ac = 1.f + ex2_approx(2.f * kLog2e * fminf(fmaxf(c, -0.5f * kL), 0.5f * kL));
+  h = go * fma_rn(-2.f, rcp_approx(ac), 1.f);  // tanh(c)
+}
 
 __device__ __forceinline__ void split16(const float* v, float (&hi)[16], float (&lo)[16]) {
 #pragma unroll
@@ -156,7 +198,10 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
 
   const int64_t n_tiles = (a.n + kRows - 1) / kRows;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t p = tile * kRows + row;
+    // tiles are filled in order of program length (a.perm): a tile runs for
+    // its longest program, so mixing lengths would waste steps
+    const int64_t slot = tile * kRows + row;
+    const int64_t p = slot < a.n ? (int64_t)a.perm[slot] : a.n;
     const bool live = rowt && p < a.n;
     int64_t r0 = 0;
     int T = 0;
@@ -169,6 +214,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
     if (live && hw == 0) atomicMax(&bars->tmax, T);
     __syncthreads();
     const int Tt = bars->tmax;
+    const bool mk0 = blockIdx.x == 0 && tile == blockIdx.x && (threadIdx.x == 32 || threadIdx.x == 0);
     float* srow = a.S + (live ? p : 0) * TM * kD;
 
     for (int l = 0; l < dm.L; ++l) {
@@ -176,6 +222,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
       float* out = ((dm.L - 1 - l) & 1) == 0 ? srow : xrow_cta;
       const float* in = ((dm.L - l) & 1) == 0 ? srow : xrow_cta;  // layer l-1's output
       for (int d = 0; d < 2; ++d) {
+        const bool mk = mk0 && l == 1 && d == 0;
         // ---- stacked image of (l, d) -> Bs (every MMA reading Bs has completed)
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -255,31 +302,39 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
           float c[16], h[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) c[i] = 0.f, h[i] = 0.f;
+          // steps this warp's rows still need: past them (short or no
+          // programs) the warp only keeps the barrier counts; its TMEM rows
+          // then hold stale values, which only feed its own (unused) rows
+          const int wT = __reduce_max_sync(0xffffffffu, live ? T : 0);
           if (Tt > 0) {
-            fetch_x(0);
-            if (Tt > 1) {
-              fetch_x(1);
-              cp_async_wait_x<1>();
-            } else {
-              cp_async_wait_x<0>();
+            if (wT > 0) {
+              fetch_x(0);
+              if (wT > 1) {
+                fetch_x(1);
+                cp_async_wait_x<1>();
+              } else {
+                cp_async_wait_x<0>();
+              }
+              put_x(0);
+              put_h(h);
             }
-            put_x(0);
             arrive(&bars->ax_full);
-            put_h(h);
             arrive(&bars->ah_full);
           }
           const float* bj = sbias + 16 * hw;
           for (int s = 0; s < Tt; ++s) {
             mbar_wait(&bars->d_full, pd);
+            X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 0);
             pd ^= 1;
             tc_fence_after();
-            if (s + 1 < Tt) {
-              // x part of step s+1: its MMAs run during this step's epilogue
-              cp_async_wait_x<0>();
-              put_x(s + 1);
-              arrive(&bars->ax_full);
-              if (s + 2 < Tt) fetch_x(s + 2);
+            if (s >= wT) {  // this warp's programs have ended
+              if (s + 1 < Tt) {
+                arrive(&bars->ax_full);
+                arrive(&bars->ah_full);
+              }
+              continue;
             }
+            // gates first: once the next x MMAs run, TMEM loads queue behind them
             const uint32_t Gt = tmem + lane_off + kColG + (uint32_t)(s & 1) * kG + 16 * hw;
             float zi[16], zf[16], zg[16], zo[16];
             tmem_ld16(Gt + 0 * kH, zi);
@@ -288,16 +343,30 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
             tmem_ld16(Gt + 3 * kH, zo);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float gi = Act<float>::sigmoid(bj[i] + zi[i]), gf = Act<float>::sigmoid(bj[kH + i] + zf[i]);
-              const float gg = Act<float>::tanh(bj[2 * kH + i] + zg[i]);
-              const float go = Act<float>::sigmoid(bj[3 * kH + i] + zo[i]);
-              c[i] = fma_rn(gf, c[i], gi * gg);
-              h[i] = go * Act<float>::tanh(c[i]);
+            for (int i = 0; i < 16; ++i) {  // bias now: shared-memory reads stall while the MMAs run
+              zi[i] += bj[i];
+              zf[i] += bj[kH + i];
+              zg[i] += bj[2 * kH + i];
+              zo[i] += bj[3 * kH + i];
             }
+            X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 2);
             if (s + 1 < Tt) {
-              put_h(h);
+              // x part of step s+1: its MMAs run during this step's activations
+              if (s + 1 < wT) {
+                cp_async_wait_x<0>();
+                put_x(s + 1);
+              }
+              arrive(&bars->ax_full);
+              X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 1);
+              if (s + 2 < wT) fetch_x(s + 2);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) lstm_cell(zi[i], zf[i], zg[i], zo[i], c[i], h[i]);
+            if (s + 1 < Tt) {
+              X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 3);
+              if (s + 1 < wT) put_h(h);
               arrive(&bars->ah_full);
+              X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 4);
             }
             if (live && s < T) {
               const int t = d == 0 ? s : T - 1 - s;
@@ -314,6 +383,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
           for (int s = 0; s < Tt; ++s) {
             const uint32_t Gs = tmem + kColG + (uint32_t)(s & 1) * kG;
             mbar_wait(&bars->ax_full, pa);
+            X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 5);
             tc_fence_after();
             for (int part = 0; part < 3; ++part) {
               const uint32_t A = tmem + (part == 1 ? kColXl : kColXh);
@@ -324,6 +394,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
               }
             }
             mbar_wait(&bars->ah_full, pa);
+            X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 7);
             pa ^= 1;
             tc_fence_after();
             for (int part = 0; part < 3; ++part) {
@@ -335,6 +406,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
               }
             }
             mma_commit(&bars->d_full);
+            X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 8);
           }
         }
       }
@@ -345,6 +417,50 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
+  }
+}
+
+// Counting sort of a chunk's programs by length (one CTA): perm lists the
+// programs longest first.  Which tile a program lands in does not change its
+// arithmetic (every row is independent), only how many padded steps its
+// tile runs.
+__global__ void __launch_bounds__(1024) x3_sort_kernel(const int64_t* __restrict__ rowoff, int64_t n, int Tmax,
+                                                       int32_t* __restrict__ perm) {
+  extern __shared__ int hist[];  // [Tmax + 1]
+  for (int i = threadIdx.x; i <= Tmax; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int64_t stride = blockDim.x;
+  for (int64_t p0 = threadIdx.x; p0 < n; p0 += 4 * stride) {
+    int len[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t p = p0 + u * stride;
+      len[u] = p < n ? (int)(rowoff[p + 1] - rowoff[p]) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (len[u] >= 0) atomicAdd(&hist[len[u]], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive offsets, longest first
+    int run = 0;
+    for (int t = Tmax; t >= 0; --t) {
+      const int c = hist[t];
+      hist[t] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int64_t p0 = threadIdx.x; p0 < n; p0 += 4 * stride) {
+    int len[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t p = p0 + u * stride;
+      len[u] = p < n ? (int)(rowoff[p + 1] - rowoff[p]) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (len[u] >= 0) perm[atomicAdd(&hist[len[u]], 1)] = (int32_t)(p0 + u * stride);
   }
 }
 
@@ -555,6 +671,193 @@ __global__ void __launch_bounds__(x3::kAttnThreads, 1) tuner_attn_rows_kernel(At
   }
 }
 
+// Warp-per-program variant for small launches (search-time scoring): each
+// scalar goes through the same operations in the same order as in
+// tuner_attn_rows_kernel -- lane j owns outputs j and j + 32 of a matvec,
+// lane t owns logit t, the online softmax's running max / sum are
+// recomputed identically in every lane, lane 0 sums the head's 64-term dot
+// product -- so both kernels give the same bits and a score does not depend
+// on which one ran (tests/test_gpu_tuner_f32tc.py).
+namespace x3 {
+constexpr int kAttnWarps = 8;
+constexpr int64_t kAttnWarpMax = 16384;  // programs per launch up to which the warp kernel runs
+}
+
+__host__ __device__ inline size_t x3_attn_warp_smem_floats(const TDims& dm) {
+  return 5 * 64 * 64 + 4 * 64 + 4 + (size_t)x3::kAttnWarps * (128 + dm.Tmax);
+}
+
+template <int HEADS>
+__global__ void __launch_bounds__(32 * x3::kAttnWarps) tuner_attn_warp_kernel(AttnRowsArgs a) {
+  using namespace x3;
+  constexpr int DH = 64 / HEADS;
+  extern __shared__ __align__(16) float sw[];
+  const TDims& dm = a.dm;
+  const int C = dm.C, TM = dm.Tmax, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* Wq = sw;
+  float* WkT = Wq + 4096;
+  float* Wv = WkT + 4096;
+  float* Wo = Wv + 4096;
+  float* W1 = Wo + 4096;
+  float* bq = W1 + 4096;
+  float* bo = bq + 64;
+  float* b1 = bo + 64;
+  float* W2 = b1 + 64;
+  float* b2 = W2 + 64;
+  float* xs = b2 + 4 + warp * (128 + TM);  // per warp: x[64] y[64] logits[Tmax]
+  float* ys = xs + 64;
+  float* lg = ys + 64;
+  for (int i = tid; i < 4096; i += blockDim.x) {
+    Wq[i] = __ldg(a.prm + dm.Wq + i);
+    WkT[(i % 64) * 64 + i / 64] = __ldg(a.prm + dm.Wk + i);
+    Wv[i] = __ldg(a.prm + dm.Wv + i);
+    Wo[i] = __ldg(a.prm + dm.Wo + i);
+    W1[i] = __ldg(a.prm + dm.W1 + i);
+  }
+  for (int i = tid; i < 64; i += blockDim.x) {
+    bq[i] = __ldg(a.prm + dm.bq + i);
+    bo[i] = __ldg(a.prm + dm.bo + i);
+    b1[i] = __ldg(a.prm + dm.b1 + i);
+    W2[i] = __ldg(a.prm + dm.W2 + i);
+  }
+  if (tid == 0) b2[0] = __ldg(a.prm + dm.b2);
+  __syncthreads();
+  const float sq = sqrtf((float)DH);
+  const float* W1c = a.prm + dm.W1 + 64 * kHeadHidden;
+  const int j0 = lane, j1 = lane + 32;
+  for (int64_t p = (int64_t)blockIdx.x * kAttnWarps + warp; p < a.n; p += (int64_t)gridDim.x * kAttnWarps) {
+    const int T = (int)(a.rowoff[p + 1] - a.rowoff[p]);
+    const float* Sp = a.S + p * TM * 64;
+    float v0 = 0.f, v1 = 0.f;
+    for (int t = 0; t < T; ++t) {
+      v0 += Sp[t * 64 + j0];
+      v1 += Sp[t * 64 + j1];
+    }
+    const float den = (float)(T > 1 ? T : 1);
+    __syncwarp();
+    xs[j0] = v0 / den;
+    xs[j1] = v1 / den;
+    __syncwarp();
+    for (int u = 0; u < dm.U; ++u) {
+      float q0 = 0.f, q1 = 0.f;
+      for (int k = 0; k < 64; ++k) {
+        const float xk = xs[k];
+        q0 = fma_rn(xk, Wq[k * 64 + j0], q0);
+        q1 = fma_rn(xk, Wq[k * 64 + j1], q1);
+      }
+      ys[j0] = q0 + bq[j0];
+      ys[j1] = q1 + bq[j1];
+      __syncwarp();
+#pragma unroll 1
+      for (int h = 0; h < HEADS; ++h) {
+        float r0 = 0.f, r1 = 0.f;
+        for (int c = h * DH; c < h * DH + DH; ++c) {
+          const float qc = ys[c];
+          r0 = fma_rn(qc, WkT[c * 64 + j0], r0);
+          r1 = fma_rn(qc, WkT[c * 64 + j1], r1);
+        }
+        __syncwarp();
+        xs[j0] = r0;
+        xs[j1] = r1;
+        __syncwarp();
+        for (int t = lane; t < T; t += 32) {
+          const float4* Sr = reinterpret_cast<const float4*>(Sp + t * 64);
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) {
+            const float4 f = Sr[q], g = Sr[q + 1];
+            a0 = fma_rn(f.x, xs[4 * q], a0);
+            a0 = fma_rn(f.y, xs[4 * q + 1], a0);
+            a0 = fma_rn(f.z, xs[4 * q + 2], a0);
+            a0 = fma_rn(f.w, xs[4 * q + 3], a0);
+            a1 = fma_rn(g.x, xs[4 * q + 4], a1);
+            a1 = fma_rn(g.y, xs[4 * q + 5], a1);
+            a1 = fma_rn(g.z, xs[4 * q + 6], a1);
+            a1 = fma_rn(g.w, xs[4 * q + 7], a1);
+          }
+          lg[t] = (a0 + a1) / sq;
+        }
+        __syncwarp();
+        float mx = -INFINITY, sum = 0.f, u0 = 0.f, u1 = 0.f;
+        for (int t = 0; t < T; ++t) {
+          const float l = lg[t];
+          if (l > mx) {
+            const float sc = Act<float>::exp(mx - l);
+            sum *= sc;
+            u0 *= sc;
+            u1 *= sc;
+            mx = l;
+          }
+          const float e = Act<float>::exp(l - mx);
+          sum += e;
+          u0 = fma_rn(e, Sp[t * 64 + j0], u0);
+          u1 = fma_rn(e, Sp[t * 64 + j1], u1);
+        }
+        const float is = T > 0 ? 1.f / sum : 0.f;
+        __syncwarp();
+        xs[j0] = u0 * is;
+        xs[j1] = u1 * is;
+        __syncwarp();
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = lane + 32 * cc;
+          if (c < DH) {
+            float ch = 0.f;
+            for (int k = 0; k < 64; ++k) ch = fma_rn(xs[k], Wv[k * 64 + h * DH + c], ch);
+            ys[h * DH + c] = ch;
+          }
+        }
+        __syncwarp();
+      }
+      float p0 = 0.f, p1 = 0.f;
+      for (int k = 0; k < 64; ++k) {
+        const float ck = ys[k];
+        p0 = fma_rn(ck, Wo[k * 64 + j0], p0);
+        p1 = fma_rn(ck, Wo[k * 64 + j1], p1);
+      }
+      __syncwarp();
+      xs[j0] = p0 + bo[j0];
+      xs[j1] = p1 + bo[j1];
+      __syncwarp();
+    }
+    float a0 = 0.f, a1 = 0.f;
+    for (int k = 0; k < 64; ++k) {
+      const float xk = xs[k];
+      a0 = fma_rn(xk, W1[k * 64 + j0], a0);
+      a1 = fma_rn(xk, W1[k * 64 + j1], a1);
+    }
+    const float* cp = a.ctx + p * C;
+    for (int k = 0; k < C; ++k) {
+      const float xk = __ldg(cp + k);
+      a0 = fma_rn(xk, __ldg(W1c + k * 64 + j0), a0);
+      a1 = fma_rn(xk, __ldg(W1c + k * 64 + j1), a1);
+    }
+    ys[j0] = Act<float>::tanh(a0 + b1[j0]);
+    ys[j1] = Act<float>::tanh(a1 + b1[j1]);
+    __syncwarp();
+    if (lane == 0) {
+      float acc = 0.f;
+      for (int j = 0; j < 64; ++j) acc = fma_rn(ys[j], W2[j], acc);
+      a.yhat[p] = Act<float>::sigmoid(acc + b2[0]);
+    }
+    __syncwarp();
+  }
+}
+
+template <int HEADS>
+static int launch_attn_warp(const AttnRowsArgs& a, cudaStream_t st) {
+  const size_t smem = x3_attn_warp_smem_floats(a.dm) * sizeof(float);
+  auto kern = tuner_attn_warp_kernel<HEADS>;
+  TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int per_sm = 0;
+  TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * x3::kAttnWarps, smem));
+  TT_REQUIRE(per_sm >= 1, "tuner attention: kernel cannot be resident (smem %zu)", smem);
+  const int64_t blocks = (a.n + x3::kAttnWarps - 1) / x3::kAttnWarps;
+  const int grid = (int)std::min<int64_t>(blocks, (int64_t)sm_count() * per_sm);
+  kern<<<grid, 32 * x3::kAttnWarps, smem, st>>>(a);
+  return check_launch("tuner attention warp");
+}
+
 template <int HEADS>
 static int launch_attn_rows(const AttnRowsArgs& a, cudaStream_t st) {
   const size_t smem = x3_attn_smem_floats(a.dm) * sizeof(float);
@@ -570,10 +873,17 @@ static int launch_attn_rows(const AttnRowsArgs& a, cudaStream_t st) {
 }
 
 static int attn_rows(const AttnRowsArgs& a, cudaStream_t st) {
+  // both kernels give identical bits; the warp kernel wins while a launch
+  // cannot fill the GPU with one program per thread
+  static const int64_t warp_max = [] {
+    const char* e = getenv("TT_X3_ATTN_WARP_MAX");
+    return e ? (int64_t)atoll(e) : (int64_t)x3::kAttnWarpMax;
+  }();
+  const bool w = a.n <= warp_max;
   switch (a.dm.heads) {
-    case 1: return launch_attn_rows<1>(a, st);
-    case 2: return launch_attn_rows<2>(a, st);
-    case 4: return launch_attn_rows<4>(a, st);
+    case 1: return w ? launch_attn_warp<1>(a, st) : launch_attn_rows<1>(a, st);
+    case 2: return w ? launch_attn_warp<2>(a, st) : launch_attn_rows<2>(a, st);
+    case 4: return w ? launch_attn_warp<4>(a, st) : launch_attn_rows<4>(a, st);
   }
   set_error("tuner fp32 tensor-core scoring: heads must be 1, 2 or 4");
   return TT_EINVAL;
@@ -595,6 +905,7 @@ size_t tuner_predict_x3_ws(int L, int H, int Tmax) {
   size_t b = align_up((size_t)x3_chunk(Tmax) * rowb, 1024);              // S
   b += align_up((size_t)x3_grid_max(Tmax) * x3::kRows * rowb, 1024);     // layer scratch
   b += align_up((size_t)x3_image_off(L, 0), 1024);                      // B images
+  b += align_up((size_t)x3_chunk(Tmax) * sizeof(int32_t), 1024);         // length order
   return b;
 }
 
@@ -623,6 +934,8 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   w += align_up((size_t)x3_grid_max(Tmax) * x3::kRows * rowb, 1024);
   unsigned char* img = w;
   w += align_up((size_t)x3_image_off(L, 0), 1024);
+  int32_t* perm = reinterpret_cast<int32_t*>(w);
+  w += align_up((size_t)chunk * sizeof(int32_t), 1024);
   a.img = img;
   tuner_x3_prepare_kernel<<<2 * L, 256, 0, st>>>(a.dm, prm, img);
   TT_CUDA(cudaFuncSetAttribute(tuner_lstm_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -630,6 +943,9 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   for (int64_t p0 = 0; p0 < n; p0 += chunk) {
     const int64_t nc = std::min<int64_t>(chunk, n - p0);
     a.rowoff = rowoff + p0;
+    x3_sort_kernel<<<1, 1024, (size_t)(Tmax + 1) * sizeof(int), st>>>(a.rowoff, nc, Tmax, perm);
+    if (int rc = check_launch("tuner lstm length sort")) return rc;
+    a.perm = perm;
     a.n = nc;
     const int grid = (int)std::min<int64_t>((nc + x3::kRows - 1) / x3::kRows, x3_grid_max(Tmax));
     tuner_lstm_x3_kernel<<<grid, x3::kThreads, x3::kSmem, st>>>(a);
@@ -643,6 +959,12 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
 }  // namespace tt
 
 extern "C" {
+
+int tt_debug_x3_phase_times(int64_t* out, int32_t n) {
+  TT_REQUIRE(n >= 0 && n <= 32, "debug: n must be in [0, 32]");
+  TT_CUDA(cudaMemcpyFromSymbol(out, tt::g_x3_phase, sizeof(long long) * n));
+  return TT_OK;
+}
 
 size_t tt_tuner_predict_f32tc_workspace_bytes(int32_t L, int32_t H, int32_t max_steps) {
   return tt::tuner_predict_x3_ws(L, H, max_steps);

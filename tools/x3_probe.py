@@ -61,7 +61,24 @@ def main():
                       "f32tc_err": float(np.abs(otc - ref).max()),
                       "f32tc_mean_err": float(np.abs(otc - ref).mean()),
                       "fp32_cuda_per_s": prog.n / t32, "f32tc_per_s": prog.n / ttc}), flush=True)
-    if "--quick" in sys.argv:
+    if "--phases" in sys.argv:
+        f32tc(est, prog, dims, flat)
+        torch.cuda.synchronize()
+        buf = np.zeros(18, dtype=np.int64)
+        _lib.call("tt_debug_x3_phase_times", buf.ctypes.data, 18)
+        names = ["d_full", "x_arrived", "gates_loaded", "act_done", "h_arrived", "mma_x_ready", "-",
+                 "mma_h_ready", "mma_committed"]
+        t0 = buf[0]
+        print(json.dumps({f"s{2 + i // 9}_{names[i % 9]}": int(buf[i] - t0) for i in range(18) if i % 9 != 6}))
+    if "--fixed" in sys.argv:  # per-call time at uniform program lengths (TT_X3_VARIANT=4: LSTM only)
+        m = 4 * 148 * 128
+        for T in (1, 2, 4, 7, 10):
+            off = np.arange(0, (m + 1) * T, T, dtype=np.int64)
+            hpf = HostPrograms(np.resize(st, (m * T, st.shape[1])), off, np.resize(cx, (m, cx.shape[1])))
+            pf = DevicePrograms(hpf, "fp32")
+            _, t = timed(lambda: f32tc(est, pf, dims, flat))
+            print(json.dumps({"T": T, "programs": m, "us_per_call": t * 1e6}), flush=True)
+    if "--quick" in sys.argv or "--phases" in sys.argv or "--fixed" in sys.argv:
         return
     # launch-size invariance and small-batch latency
     for m in (1, 8, 100, 148, 149, 1000, 20000):
