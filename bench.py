@@ -800,6 +800,18 @@ def run_b200(args, world, rank):
         sc_t = s0.elapsed_time(s1) / 1e3
         extra["scoring_programs_per_s"] = n / sc_t
         extra["scoring_tflops"] = float(np.sum(134656.0 * lens + 45568.0)) / sc_t / 1e12
+        extra["scoring_fp32_path"] = ("tt_tuner_predict_f32tc: split-precision tcgen05 biLSTM "
+                                      "(x_hi.w_hi + x_lo.w_hi + x_hi.w_lo) + fp32 CUDA-core attention")
+        # the strict CUDA-core fp32 kernel ("fp32_cuda", the round-1 default)
+        est.precision = "fp32_cuda"
+        est._predict_programs(prog, dims, flat)
+        flush_l2(l2)
+        s0.record(stream)
+        est._predict_programs(prog, dims, flat)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        extra["scoring_fp32_cuda_programs_per_s"] = n / (s0.elapsed_time(s1) / 1e3)
+        est.precision = "fp32"
         # the same scoring on the tensor cores (tcgen05 kind::tf32, "tf32" mode)
         est.precision = "tf32"
         for _ in range(2):
@@ -883,6 +895,8 @@ def run_b200(args, world, rank):
                     if "scoring_programs_per_s" in extra:
                         extra["vs_best_of_host"] = {
                             "tuner_scoring_fp32": extra["scoring_programs_per_s"] / sc["tuner"]["value"],
+                            "tuner_scoring_fp32_cuda": (extra["scoring_fp32_cuda_programs_per_s"]
+                                                        / sc["tuner"]["value"]),
                             "tuner_scoring_tf32": extra["scoring_tc_tf32_programs_per_s"] / sc["tuner"]["value"],
                             "mlp_scoring_fp32": extra["mlp_fp32_rows_per_s"] / sc["mlp"]["value"],
                             "mlp_scoring_tf32": extra["mlp_tf32_rows_per_s"] / sc["mlp"]["value"],

@@ -1,5 +1,6 @@
 """Config 3: bulk scoring of 1 M / 4 M / 16 M / 64 M programs on
-one B200, fp32 (CUDA cores, the strict default) and tf32 (tcgen05), T drawn
+one B200: fp32 (the default: split-precision tcgen05 LSTM + fp32 attention),
+tf32 (tcgen05) and, up to 4 M, fp32_cuda (the CUDA-core kernel); T drawn
 from the generator histogram (4..10, mean 7.1) and fixed T = 8.
 
 Inputs are generated ON THE DEVICE (torch, seeded) in the CSR layout the
@@ -69,7 +70,7 @@ def main():
         for fixed in (0, 8):
             prog, lens = make(n, fixed, g)
             flops = float((134656.0 * lens.double() + 45568.0).sum().item())
-            for prec in ("fp32", "tf32"):
+            for prec in ("fp32", "tf32") + (("fp32_cuda",) if m <= 4 else ()):
                 est.precision = prec
                 flat = est._dev_params(dims)
                 est._predict_programs(prog, dims, flat)
