@@ -99,6 +99,7 @@ struct ScArgs {
   __half* scratch;      // per CTA: [2][128][Tmax][64] layer outputs (ping-pong, fp16)
   const unsigned char* img;  // prepared B^T images (tuner_tc_prepare_kernel)
   int64_t scr_per_cta;  // halves
+  const int32_t* perm;  // program of each tile slot, longest first (sort_programs_by_length)
 };
 
 struct __align__(8) ScBars {
@@ -338,7 +339,8 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
 
   const int64_t n_tiles = (a.n + kRows - 1) / kRows;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t p = tile * kRows + row;
+    const int64_t slot = tile * kRows + row;
+    const int64_t p = slot < a.n ? (int64_t)a.perm[slot] : a.n;  // length-ordered tiles
     const bool live = rowt && p < a.n;
     int64_t r0 = 0;
     int T = 0;
@@ -707,8 +709,11 @@ static size_t sc_smem_bytes(int Tmax) {
 
 constexpr size_t kScImageBytes = 1u << 20;  // >= every LSTM image (L <= 8) + the attention image
 
+static int64_t tc_chunk() { return 4 * (int64_t)sm_count() * sc::kRows; }
+
 size_t tuner_predict_tc_ws(int Tmax) {
-  return align_up((size_t)sm_count() * 2 * sc::kRows * Tmax * sc::kD * sizeof(__half), 1024) + kScImageBytes;
+  return align_up((size_t)sm_count() * 2 * sc::kRows * Tmax * sc::kD * sizeof(__half), 1024) + kScImageBytes +
+         align_up((size_t)tc_chunk() * sizeof(int32_t), 1024);
 }
 
 int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff, const float* ctx,
@@ -743,10 +748,24 @@ int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff
   tuner_tc_prepare_kernel<<<L + 1, 256, 0, st>>>(a.dm, prm, img);
   TT_CUDA(cudaFuncSetAttribute(tuner_predict_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
-  const int64_t tiles = (n + sc::kRows - 1) / sc::kRows;
-  const int grid = (int)std::min<int64_t>(tiles, sm_count());
-  tuner_predict_tc_kernel<<<grid, sc::kThreads, smem, st>>>(a);
-  return check_launch("tuner predict tf32");
+  // chunks of 4 tiles per SM, each ordered by program length so a tile runs
+  // for about its own programs' length (the result of a row does not depend
+  // on its tile)
+  int32_t* perm = reinterpret_cast<int32_t*>(img + kScImageBytes);
+  const int64_t chunk = tc_chunk();
+  for (int64_t p0 = 0; p0 < n; p0 += chunk) {
+    const int64_t nc = std::min<int64_t>(chunk, n - p0);
+    if (int rc = sort_programs_by_length(rowoff + p0, nc, Tmax, perm, st)) return rc;
+    a.rowoff = rowoff + p0;
+    a.ctx = ctx + p0 * C;
+    a.yhat = yhat + p0;
+    a.n = nc;
+    a.perm = perm;
+    const int grid = (int)std::min<int64_t>((nc + sc::kRows - 1) / sc::kRows, sm_count());
+    tuner_predict_tc_kernel<<<grid, sc::kThreads, smem, st>>>(a);
+    if (int rc = check_launch("tuner predict tf32")) return rc;
+  }
+  return TT_OK;
 }
 
 }  // namespace tt

@@ -109,7 +109,7 @@ struct X3Args {
 };
 
 struct __align__(8) X3Bars {
-  uint64_t ax_full, ah_full, d_full, w_full;
+  uint64_t ax_full, ah_full[2], d_full, w_full;  // ah_full[q]: h of units [8q, 8q + 8) of each half
   uint32_t tmem_base;
   int tmax;
 };
@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
 
   if (threadIdx.x == 0) {
     mbar_init(&bars->ax_full, 2 * kRows);
-    mbar_init(&bars->ah_full, 2 * kRows);
+    mbar_init(&bars->ah_full[0], 2 * kRows);
+    mbar_init(&bars->ah_full[1], 2 * kRows);
     mbar_init(&bars->d_full, 1);
     mbar_init(&bars->w_full, 1);
     fence_barrier_init();
@@ -195,6 +196,16 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
   const uint32_t tmem = bars->tmem_base;
   uint32_t pa = 0, pd = 0, pw = 0;
   float* xrow_cta = a.scratch + (int64_t)blockIdx.x * kRows * TM * kD + (int64_t)row * TM * kD;
+
+  auto issue_image = [&](int l, int d) {  // thread 0; Bs is not read by any MMA in flight
+    const uint32_t bytes = x3_image_bytes(l);
+    const unsigned char* src = a.img + x3_image_off(l, d);
+    mbar_expect_tx(&bars->w_full, bytes);
+    for (uint32_t off = 0; off < bytes; off += 32768)
+      bulk_g2s(Bs + off, src + off, bytes - off < 32768 ? bytes - off : 32768, &bars->w_full);
+  };
+  bool img_issued = false;
+  uint32_t pdm = 0;  // MMA lane: parity of the next d_full completion
 
   const int64_t n_tiles = (a.n + kRows - 1) / kRows;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -223,15 +234,11 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
       const float* in = ((dm.L - l) & 1) == 0 ? srow : xrow_cta;  // layer l-1's output
       for (int d = 0; d < 2; ++d) {
         const bool mk = mk0 && l == 1 && d == 0;
-        // ---- stacked image of (l, d) -> Bs (every MMA reading Bs has completed)
+        // ---- stacked image of (l, d) -> Bs: issued by the MMA lane as soon as
+        // the previous (layer, direction)'s last MMA completed, else here
         __syncthreads();
-        if (threadIdx.x == 0) {
-          const uint32_t bytes = x3_image_bytes(l);
-          const unsigned char* src = a.img + x3_image_off(l, d);
-          mbar_expect_tx(&bars->w_full, bytes);
-          for (uint32_t off = 0; off < bytes; off += 32768)
-            bulk_g2s(Bs + off, src + off, bytes - off < 32768 ? bytes - off : 32768, &bars->w_full);
-        }
+        if (threadIdx.x == 0 && !img_issued) issue_image(l, d);
+        img_issued = false;
         for (int i = threadIdx.x; i < kG; i += blockDim.x) sbias[i] = __ldg(a.prm + dm.bb[l][d] + i);
         mbar_wait(&bars->w_full, pw);
         pw ^= 1;
@@ -294,6 +301,16 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
             tmem_st16(Hh + 16 * hw, hi);
             tmem_st16(Hl + 16 * hw, lo);
           };
+          auto put_h8 = [&](const float (&h)[16], int o) {  // units [o, o + 8)
+            float hi[8], lo[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              hi[i] = tf32_hi(h[o + i]);
+              lo[i] = h[o + i] - hi[i];
+            }
+            tmem_st8(Hh + 16 * hw + o, hi);
+            tmem_st8(Hl + 16 * hw + o, lo);
+          };
           auto arrive = [&](uint64_t* bar) {
             tmem_wait_st();
             tc_fence_before();
@@ -319,7 +336,8 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
               put_h(h);
             }
             arrive(&bars->ax_full);
-            arrive(&bars->ah_full);
+            arrive(&bars->ah_full[0]);
+            arrive(&bars->ah_full[1]);
           }
           const float* bj = sbias + 16 * hw;
           for (int s = 0; s < Tt; ++s) {
@@ -330,7 +348,8 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
             if (s >= wT) {  // this warp's programs have ended
               if (s + 1 < Tt) {
                 arrive(&bars->ax_full);
-                arrive(&bars->ah_full);
+                arrive(&bars->ah_full[0]);
+                arrive(&bars->ah_full[1]);
               }
               continue;
             }
@@ -360,12 +379,20 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
               X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 1);
               if (s + 2 < wT) fetch_x(s + 2);
             }
+            // two halves: the h MMAs of the first 8 units of each thread run
+            // while the second 8 are computed
 #pragma unroll
-            for (int i = 0; i < 16; ++i) lstm_cell(zi[i], zf[i], zg[i], zo[i], c[i], h[i]);
+            for (int i = 0; i < 8; ++i) lstm_cell(zi[i], zf[i], zg[i], zo[i], c[i], h[i]);
+            if (s + 1 < Tt) {
+              if (s + 1 < wT) put_h8(h, 0);
+              arrive(&bars->ah_full[0]);
+            }
+#pragma unroll
+            for (int i = 8; i < 16; ++i) lstm_cell(zi[i], zf[i], zg[i], zo[i], c[i], h[i]);
             if (s + 1 < Tt) {
               X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 3);
-              if (s + 1 < wT) put_h(h);
-              arrive(&bars->ah_full);
+              if (s + 1 < wT) put_h8(h, 8);
+              arrive(&bars->ah_full[1]);
               X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 4);
             }
             if (live && s < T) {
@@ -393,20 +420,39 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
                 mma_tf32_ts(Gs, A + kk * 8, bd, id, part != 0 || kk != 0);
               }
             }
-            mbar_wait(&bars->ah_full, pa);
-            X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 7);
-            pa ^= 1;
-            tc_fence_after();
-            for (int part = 0; part < 3; ++part) {
-              const uint32_t A = tmem + (part == 1 ? kColHl : kColHh);
-              const uint32_t boff = part == 2 ? kG * 128 : 0;
-              for (int kk = 0; kk < kH / 8; ++kk) {
-                const uint64_t bd = sw128_desc(bs_addr + (kx >> 5) * (kN * 128) + boff + kk * 32);
-                mma_tf32_ts(Gs, A + kk * 8, bd, id, 1);
+            // h columns 8q..8q+7 and 16+8q..16+8q+7 (units [8q, 8q+8) of both halves)
+            for (int q = 0; q < 2; ++q) {
+              mbar_wait(&bars->ah_full[q], pa);
+              if (q == 1) X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 7);
+              tc_fence_after();
+              for (int part = 0; part < 3; ++part) {
+                const uint32_t A = tmem + (part == 1 ? kColHl : kColHh);
+                const uint32_t boff = part == 2 ? kG * 128 : 0;
+                for (int kk = q; kk < kH / 8; kk += 2) {
+                  const uint64_t bd = sw128_desc(bs_addr + (kx >> 5) * (kN * 128) + boff + kk * 32);
+                  mma_tf32_ts(Gs, A + kk * 8, bd, id, 1);
+                }
               }
             }
+            pa ^= 1;
             mma_commit(&bars->d_full);
+            pdm ^= 1;
             X3_MARK(mk && s >= 2 && s < 4, 9 * (s - 2) + 8);
+          }
+          // next (layer, direction)'s weights while the row threads finish
+          if (Tt > 0) mbar_wait(&bars->d_full, pdm ^ 1);
+          int nl = l, nd = d + 1;
+          bool next = true;
+          if (nd == 2) {
+            nd = 0;
+            if (++nl == dm.L) {
+              nl = 0;
+              next = tile + gridDim.x < n_tiles;
+            }
+          }
+          if (next) {
+            issue_image(nl, nd);
+            img_issued = true;
           }
         }
       }
@@ -462,6 +508,11 @@ __global__ void __launch_bounds__(1024) x3_sort_kernel(const int64_t* __restrict
     for (int u = 0; u < 4; ++u)
       if (len[u] >= 0) perm[atomicAdd(&hist[len[u]], 1)] = (int32_t)(p0 + u * stride);
   }
+}
+
+int sort_programs_by_length(const int64_t* rowoff, int64_t n, int Tmax, int32_t* perm, cudaStream_t st) {
+  x3_sort_kernel<<<1, 1024, (size_t)(Tmax + 1) * sizeof(int), st>>>(rowoff, n, Tmax, perm);
+  return check_launch("tuner length sort");
 }
 
 // ---------------------------------------------------------------------------
@@ -943,8 +994,7 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   for (int64_t p0 = 0; p0 < n; p0 += chunk) {
     const int64_t nc = std::min<int64_t>(chunk, n - p0);
     a.rowoff = rowoff + p0;
-    x3_sort_kernel<<<1, 1024, (size_t)(Tmax + 1) * sizeof(int), st>>>(a.rowoff, nc, Tmax, perm);
-    if (int rc = check_launch("tuner lstm length sort")) return rc;
+    if (int rc = sort_programs_by_length(a.rowoff, nc, Tmax, perm, st)) return rc;
     a.perm = perm;
     a.n = nc;
     const int grid = (int)std::min<int64_t>((nc + x3::kRows - 1) / x3::kRows, x3_grid_max(Tmax));
