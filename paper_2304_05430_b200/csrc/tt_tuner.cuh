@@ -641,6 +641,8 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
 // Counting sort of n programs by length (longest first) into perm
 // (tt_tuner_x3.cu); the tensor-core scorers fill their 128-program tiles in
 // this order.
-int sort_programs_by_length(const int64_t* rowoff, int64_t n, int Tmax, int32_t* perm, cudaStream_t st);
+int sort_programs_by_length(const int64_t* rowoff, int64_t n, int Tmax, int32_t* perm, void* scratch,
+                            cudaStream_t st);
+size_t sort_scratch_bytes(int Tmax);
 
 }  // namespace tt

@@ -713,7 +713,7 @@ static int64_t tc_chunk() { return 4 * (int64_t)sm_count() * sc::kRows; }
 
 size_t tuner_predict_tc_ws(int Tmax) {
   return align_up((size_t)sm_count() * 2 * sc::kRows * Tmax * sc::kD * sizeof(__half), 1024) + kScImageBytes +
-         align_up((size_t)tc_chunk() * sizeof(int32_t), 1024);
+         align_up((size_t)tc_chunk() * sizeof(int32_t), 1024) + align_up(sort_scratch_bytes(Tmax), 1024);
 }
 
 int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff, const float* ctx,
@@ -752,10 +752,11 @@ int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff
   // for about its own programs' length (the result of a row does not depend
   // on its tile)
   int32_t* perm = reinterpret_cast<int32_t*>(img + kScImageBytes);
+  void* sort_scr = reinterpret_cast<unsigned char*>(perm) + align_up((size_t)tc_chunk() * sizeof(int32_t), 1024);
   const int64_t chunk = tc_chunk();
   for (int64_t p0 = 0; p0 < n; p0 += chunk) {
     const int64_t nc = std::min<int64_t>(chunk, n - p0);
-    if (int rc = sort_programs_by_length(rowoff + p0, nc, Tmax, perm, st)) return rc;
+    if (int rc = sort_programs_by_length(rowoff + p0, nc, Tmax, perm, sort_scr, st)) return rc;
     a.rowoff = rowoff + p0;
     a.ctx = ctx + p0 * C;
     a.yhat = yhat + p0;

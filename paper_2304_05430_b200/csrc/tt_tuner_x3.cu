@@ -111,7 +111,7 @@ struct X3Args {
   float* S;        // [n][Tmax][64]
   float* scratch;  // per CTA [128][Tmax][64]
   const unsigned char* img;
-  const int32_t* perm;  // program of each tile slot (x3_sort_kernel)
+  const int32_t* perm;  // program of each tile slot (sort_programs_by_length)
 };
 
 struct __align__(8) X3Bars {
@@ -460,52 +460,61 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
   }
 }
 
-// Counting sort of a chunk's programs by length (one CTA): perm lists the
-// programs longest first.  Which tile a program lands in does not change its
-// arithmetic (every row is independent), only how many padded steps its
-// tile runs.
-__global__ void __launch_bounds__(1024) x3_sort_kernel(const int64_t* __restrict__ rowoff, int64_t n, int Tmax,
-                                                       int32_t* __restrict__ perm) {
+// Counting sort of a chunk's programs by length, longest first, in two
+// launches over kSortCtas CTAs: per-CTA bucket counts, then each CTA's
+// offsets (longer buckets first, then lower CTAs) and a scatter.  Which tile
+// a program lands in does not change its arithmetic (every row is
+// independent), only how many padded steps its tile runs.
+constexpr int kSortCtas = 64;
+
+__global__ void __launch_bounds__(512) x3_sort_count_kernel(const int64_t* __restrict__ rowoff, int64_t n, int Tmax,
+                                                            int* __restrict__ counts) {
   extern __shared__ int hist[];  // [Tmax + 1]
   for (int i = threadIdx.x; i <= Tmax; i += blockDim.x) hist[i] = 0;
   __syncthreads();
-  const int64_t stride = blockDim.x;
-  for (int64_t p0 = threadIdx.x; p0 < n; p0 += 4 * stride) {
-    int len[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t p = p0 + u * stride;
-      len[u] = p < n ? (int)(rowoff[p + 1] - rowoff[p]) : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (len[u] >= 0) atomicAdd(&hist[len[u]], 1);
-  }
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x, lo = blockIdx.x * per, hi = min(n, lo + per);
+  for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x) atomicAdd(&hist[(int)(rowoff[p + 1] - rowoff[p])], 1);
   __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive offsets, longest first
-    int run = 0;
-    for (int t = Tmax; t >= 0; --t) {
-      const int c = hist[t];
-      hist[t] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-  for (int64_t p0 = threadIdx.x; p0 < n; p0 += 4 * stride) {
-    int len[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t p = p0 + u * stride;
-      len[u] = p < n ? (int)(rowoff[p + 1] - rowoff[p]) : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (len[u] >= 0) perm[atomicAdd(&hist[len[u]], 1)] = (int32_t)(p0 + u * stride);
-  }
+  for (int i = threadIdx.x; i <= Tmax; i += blockDim.x) counts[(int64_t)blockIdx.x * (Tmax + 1) + i] = hist[i];
 }
 
-int sort_programs_by_length(const int64_t* rowoff, int64_t n, int Tmax, int32_t* perm, cudaStream_t st) {
-  x3_sort_kernel<<<1, 1024, (size_t)(Tmax + 1) * sizeof(int), st>>>(rowoff, n, Tmax, perm);
+__global__ void __launch_bounds__(512) x3_sort_scatter_kernel(const int64_t* __restrict__ rowoff, int64_t n,
+                                                              int Tmax, const int* __restrict__ counts,
+                                                              int32_t* __restrict__ perm) {
+  extern __shared__ int cur[];  // [2 (Tmax + 1)]: bucket totals, then this CTA's cursors
+  int* tot = cur + (Tmax + 1);
+  for (int t = threadIdx.x; t <= Tmax; t += blockDim.x) {
+    int all = 0, below = 0;
+    for (int b = 0; b < (int)gridDim.x; ++b) {
+      const int c = counts[(int64_t)b * (Tmax + 1) + t];
+      all += c;
+      if (b < (int)blockIdx.x) below += c;
+    }
+    tot[t] = all;
+    cur[t] = below;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive offsets, longest bucket first
+    int run = 0;
+    for (int t = Tmax; t >= 0; --t) {
+      cur[t] += run;
+      run += tot[t];
+    }
+  }
+  __syncthreads();
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x, lo = blockIdx.x * per, hi = min(n, lo + per);
+  for (int64_t p = lo + threadIdx.x; p < hi; p += blockDim.x)
+    perm[atomicAdd(&cur[(int)(rowoff[p + 1] - rowoff[p])], 1)] = (int32_t)p;
+}
+
+size_t sort_scratch_bytes(int Tmax) { return (size_t)kSortCtas * (Tmax + 1) * sizeof(int); }
+
+int sort_programs_by_length(const int64_t* rowoff, int64_t n, int Tmax, int32_t* perm, void* scratch,
+                            cudaStream_t st) {
+  int* counts = static_cast<int*>(scratch);
+  x3_sort_count_kernel<<<kSortCtas, 512, (size_t)(Tmax + 1) * sizeof(int), st>>>(rowoff, n, Tmax, counts);
+  x3_sort_scatter_kernel<<<kSortCtas, 512, 2 * (size_t)(Tmax + 1) * sizeof(int), st>>>(rowoff, n, Tmax, counts,
+                                                                                          perm);
   return check_launch("tuner length sort");
 }
 
@@ -951,6 +960,7 @@ size_t tuner_predict_x3_ws(int L, int H, int Tmax) {
   b += align_up((size_t)x3_grid_max(Tmax) * x3::kRows * rowb, 1024);     // layer scratch
   b += align_up((size_t)x3_image_off(L, 0), 1024);                      // B images
   b += align_up((size_t)x3_chunk(Tmax) * sizeof(int32_t), 1024);         // length order
+  b += align_up(sort_scratch_bytes(Tmax), 1024);
   return b;
 }
 
@@ -981,6 +991,8 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   w += align_up((size_t)x3_image_off(L, 0), 1024);
   int32_t* perm = reinterpret_cast<int32_t*>(w);
   w += align_up((size_t)chunk * sizeof(int32_t), 1024);
+  void* sort_scr = w;
+  w += align_up(sort_scratch_bytes(Tmax), 1024);
   a.img = img;
   tuner_x3_prepare_kernel<<<2 * L, 256, 0, st>>>(a.dm, prm, img);
   TT_CUDA(cudaFuncSetAttribute(tuner_lstm_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -988,7 +1000,7 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   for (int64_t p0 = 0; p0 < n; p0 += chunk) {
     const int64_t nc = std::min<int64_t>(chunk, n - p0);
     a.rowoff = rowoff + p0;
-    if (int rc = sort_programs_by_length(a.rowoff, nc, Tmax, perm, st)) return rc;
+    if (int rc = sort_programs_by_length(a.rowoff, nc, Tmax, perm, sort_scr, st)) return rc;
     a.perm = perm;
     a.n = nc;
     const int grid = (int)std::min<int64_t>((nc + x3::kRows - 1) / x3::kRows, x3_grid_max(Tmax));

@@ -70,7 +70,7 @@ def main():
                  "mma_h_ready", "mma_committed"]
         t0 = buf[0]
         print(json.dumps({f"s{2 + i // 9}_{names[i % 9]}": int(buf[i] - t0) for i in range(18) if i % 9 != 6}))
-    if "--fixed" in sys.argv:  # per-call time at uniform program lengths (TT_X3_VARIANT=4: LSTM only)
+    if "--fixed" in sys.argv:  # per-call time at uniform program lengths
         m = 4 * 148 * 128
         for T in (1, 2, 4, 7, 10):
             off = np.arange(0, (m + 1) * T, T, dtype=np.int64)
