@@ -126,13 +126,14 @@ int tt_tuner_predict_tf32(const float *d_params, const float *d_steps,
 
 /* fp32-accurate tensor-core scoring (csrc/tt_tuner_x3.cu): the biLSTM stack
  * as split-precision tcgen05 GEMMs (x.w = x_hi.w_hi + x_lo.w_hi + x_hi.w_lo,
- * fp32 accumulation, the Act<float> activations of tt_tuner_predict_f32),
- * then attention + head on the CUDA cores of tt_tuner_predict_f32.  Same
+ * fp32 accumulation; MUFU ex2/rcp activations), then attention + head in
+ * fp32 on the CUDA cores (K and V never formed, online softmax).  Same
  * signature and outputs as tt_tuner_predict_f32 (within its fp32 tolerance);
  * a program's score does not depend on the batch it is scored in.
  * tt_tuner_f32tc_eligible says whether the shapes are covered (hidden = 32,
- * step_width <= 32). */
-size_t tt_tuner_predict_f32tc_workspace_bytes(int32_t layers, int32_t hidden, int32_t max_steps);
+ * step_width <= 32).  The workspace depends on n (launches of up to 4 tiles of
+ * 128 programs per SM; small calls need little). */
+size_t tt_tuner_predict_f32tc_workspace_bytes(int32_t layers, int32_t hidden, int32_t max_steps, int64_t n);
 int tt_tuner_f32tc_eligible(int32_t layers, int32_t hidden, int32_t heads, int32_t step_width,
                             int32_t max_steps);
 int tt_tuner_predict_f32tc(const float *d_params, const float *d_steps,

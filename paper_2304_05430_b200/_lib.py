@@ -37,7 +37,7 @@ SIGNATURES: dict[str, tuple] = {
     "tt_tuner_predict_f64": (ctypes.c_int, [_P, _P, _P, _P, _I64] + [_I32] * 7 + [_P, _P, _SZ, _P]),
     "tt_tuner_predict_tf32_workspace_bytes": (_SZ, [_I32]),
     "tt_tuner_predict_tf32": (ctypes.c_int, [_P, _P, _P, _P, _I64] + [_I32] * 7 + [_P, _P, _SZ, _P]),
-    "tt_tuner_predict_f32tc_workspace_bytes": (_SZ, [_I32, _I32, _I32]),
+    "tt_tuner_predict_f32tc_workspace_bytes": (_SZ, [_I32, _I32, _I32, _I64]),
     "tt_tuner_f32tc_eligible": (ctypes.c_int, [_I32] * 5),
     "tt_tuner_predict_f32tc": (ctypes.c_int, [_P, _P, _P, _P, _I64] + [_I32] * 7 + [_P, _P, _SZ, _P]),
     "tt_tuner_train_workspace_bytes": (_SZ, [_I32] * 7),

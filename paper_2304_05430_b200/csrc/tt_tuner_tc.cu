@@ -114,7 +114,7 @@ struct __align__(8) ScBars {
 // K-major SW128 B^T tiles of N rows, at K offset kbase.  All threads.
 __device__ void sc_stage(unsigned char* dst, int N, int kbase, int Kcnt, const float* __restrict__ src,
                          int ld, int Kr) {
-  for (int i = threadIdx.x; i < Kcnt * N; i += blockDim.x) {
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < Kcnt * N; i += gridDim.y * blockDim.x) {
     const int n = i % N, k = i / N;
     const float v = k < Kr ? __ldg(src + (int64_t)k * ld + n) : 0.f;
     const int kk = kbase + k;
@@ -230,13 +230,13 @@ __device__ void sc_stage_attn(unsigned char* base, const TDims& dm, const float*
   sc_stage(bo_t, kD, 0, kD, prm + dm.Wo, kD, kD);
   sc_stage(b1_t, kD, 0, Zp, prm + dm.W1, kHeadHidden, Z);
   // Bk^T[h*64 + k][c] = Wk[k][c] for c in head h ; Bv^T[c][h*64 + k] = Wv[k][c] for c in head h
-  for (int i = threadIdx.x; i < NK * kD; i += blockDim.x) {
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < NK * kD; i += gridDim.y * blockDim.x) {
     const int nrow = i % NK, c = i / NK;
     const int h = nrow / kD, k = nrow % kD;
     const float v = (c / dh == h) ? __ldg(prm + dm.Wk + (int64_t)k * kD + c) : 0.f;
     *reinterpret_cast<float*>(bk_t + (c >> 5) * (NK * 128) + sw128_offset(nrow, c & 31)) = v;
   }
-  for (int i = threadIdx.x; i < kD * NK; i += blockDim.x) {
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < kD * NK; i += gridDim.y * blockDim.x) {
     const int c = i % kD, kk = i / kD;
     const int h = kk / kD, k = kk % kD;
     const float v = (c / dh == h) ? __ldg(prm + dm.Wv + (int64_t)k * kD + c) : 0.f;
@@ -745,7 +745,7 @@ int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff
   TT_REQUIRE(sc_attn_image_off(a.dm) + sc_attn_image_bytes(a.dm) <= (int64_t)kScImageBytes - 1024,
              "tuner tf32 scoring: weight images exceed the workspace");
   a.img = img;
-  tuner_tc_prepare_kernel<<<L + 1, 256, 0, st>>>(a.dm, prm, img);
+  tuner_tc_prepare_kernel<<<dim3(L + 1, 16), 256, 0, st>>>(a.dm, prm, img);
   TT_CUDA(cudaFuncSetAttribute(tuner_predict_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   // chunks of 4 tiles per SM, each ordered by program length so a tile runs

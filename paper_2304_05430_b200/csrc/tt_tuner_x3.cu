@@ -79,7 +79,9 @@ __global__ void __launch_bounds__(256) tuner_x3_prepare_kernel(TDims dm, const f
   unsigned char* base = img + x3_image_off(l, d);
   const float* Wx = prm + dm.wx[l][d];
   const float* Wh = prm + dm.wh[l][d];
-  for (int i = threadIdx.x; i < K * kN; i += blockDim.x) {
+  // blockIdx.y strides the elements: 16 CTAs per image keep this off the
+  // latency of small scoring calls
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < K * kN; i += gridDim.y * blockDim.x) {
     const int n = i % kN, k = i / kN, c = n & (kG - 1);
     float w = 0.f;
     if (k < kx) {
@@ -945,21 +947,25 @@ static int attn_rows(const AttnRowsArgs& a, cudaStream_t st) {
 
 // programs per (LSTM, attention) launch pair: up to 4 tiles per SM, fewer
 // when the padded rows of a chunk would pass kChunkBudget (long programs)
-static int64_t x3_chunk(int Tmax) {
+static int64_t x3_chunk(int Tmax, int64_t n) {
   const size_t tile = (size_t)x3::kRows * Tmax * x3::kD * sizeof(float);
   const int64_t tiles = std::max<int64_t>(1, std::min<int64_t>(x3::kMaxChunkTilesPerSm * sm_count(),
                                                                  (int64_t)(x3::kChunkBudget / tile)));
-  return tiles * x3::kRows;
+  // small calls (search-time scoring) size everything by their own programs
+  const int64_t need = std::max<int64_t>(1, (n + x3::kRows - 1) / x3::kRows);
+  return std::min(tiles, need) * x3::kRows;
 }
-static int x3_grid_max(int Tmax) { return (int)std::min<int64_t>(sm_count(), x3_chunk(Tmax) / x3::kRows); }
+static int x3_grid_max(int Tmax, int64_t n) {
+  return (int)std::min<int64_t>(sm_count(), x3_chunk(Tmax, n) / x3::kRows);
+}
 
-size_t tuner_predict_x3_ws(int L, int H, int Tmax) {
+size_t tuner_predict_x3_ws(int L, int H, int Tmax, int64_t n) {
   (void)H;
   const size_t rowb = (size_t)Tmax * x3::kD * sizeof(float);
-  size_t b = align_up((size_t)x3_chunk(Tmax) * rowb, 1024);              // S
-  b += align_up((size_t)x3_grid_max(Tmax) * x3::kRows * rowb, 1024);     // layer scratch
+  size_t b = align_up((size_t)x3_chunk(Tmax, n) * rowb, 1024);           // S
+  b += align_up((size_t)x3_grid_max(Tmax, n) * x3::kRows * rowb, 1024);  // layer scratch
   b += align_up((size_t)x3_image_off(L, 0), 1024);                      // B images
-  b += align_up((size_t)x3_chunk(Tmax) * sizeof(int32_t), 1024);         // length order
+  b += align_up((size_t)x3_chunk(Tmax, n) * sizeof(int32_t), 1024);      // length order
   b += align_up(sort_scratch_bytes(Tmax), 1024);
   return b;
 }
@@ -975,9 +981,9 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   TT_REQUIRE(Tmax >= 1 && Tmax <= 4096, "tuner fp32 tensor-core scoring: bad max steps");
   TT_REQUIRE(n >= 0, "tuner fp32 tensor-core scoring: negative n");
   if (n == 0) return TT_OK;
-  TT_REQUIRE(ws_bytes >= tuner_predict_x3_ws(L, H, Tmax), "tuner fp32 tensor-core scoring: workspace too small");
+  TT_REQUIRE(ws_bytes >= tuner_predict_x3_ws(L, H, Tmax, n), "tuner fp32 tensor-core scoring: workspace too small");
   const size_t rowb = (size_t)Tmax * x3::kD * sizeof(float);
-  const int64_t chunk = x3_chunk(Tmax);
+  const int64_t chunk = x3_chunk(Tmax, n);
   unsigned char* w = static_cast<unsigned char*>(ws);
   X3Args a{};
   a.dm = make_dims(L, H, heads, U, d0, C, Tmax);
@@ -986,7 +992,7 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   a.S = reinterpret_cast<float*>(w);
   w += align_up((size_t)chunk * rowb, 1024);
   a.scratch = reinterpret_cast<float*>(w);
-  w += align_up((size_t)x3_grid_max(Tmax) * x3::kRows * rowb, 1024);
+  w += align_up((size_t)x3_grid_max(Tmax, n) * x3::kRows * rowb, 1024);
   unsigned char* img = w;
   w += align_up((size_t)x3_image_off(L, 0), 1024);
   int32_t* perm = reinterpret_cast<int32_t*>(w);
@@ -994,7 +1000,7 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   void* sort_scr = w;
   w += align_up(sort_scratch_bytes(Tmax), 1024);
   a.img = img;
-  tuner_x3_prepare_kernel<<<2 * L, 256, 0, st>>>(a.dm, prm, img);
+  tuner_x3_prepare_kernel<<<dim3(2 * L, 16), 256, 0, st>>>(a.dm, prm, img);
   TT_CUDA(cudaFuncSetAttribute(tuner_lstm_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)x3::kSmem));
   for (int64_t p0 = 0; p0 < n; p0 += chunk) {
@@ -1003,7 +1009,7 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
     if (int rc = sort_programs_by_length(a.rowoff, nc, Tmax, perm, sort_scr, st)) return rc;
     a.perm = perm;
     a.n = nc;
-    const int grid = (int)std::min<int64_t>((nc + x3::kRows - 1) / x3::kRows, x3_grid_max(Tmax));
+    const int grid = (int)std::min<int64_t>((nc + x3::kRows - 1) / x3::kRows, x3_grid_max(Tmax, n));
     tuner_lstm_x3_kernel<<<grid, x3::kThreads, x3::kSmem, st>>>(a);
     if (int rc = check_launch("tuner lstm fp32 tensor-core")) return rc;
     AttnRowsArgs ar{a.dm, prm, rowoff + p0, ctx + p0 * C, nc, a.S, yhat + p0};
@@ -1022,8 +1028,8 @@ int tt_debug_x3_phase_times(int64_t* out, int32_t n) {
   return TT_OK;
 }
 
-size_t tt_tuner_predict_f32tc_workspace_bytes(int32_t L, int32_t H, int32_t max_steps) {
-  return tt::tuner_predict_x3_ws(L, H, max_steps);
+size_t tt_tuner_predict_f32tc_workspace_bytes(int32_t L, int32_t H, int32_t max_steps, int64_t n) {
+  return tt::tuner_predict_x3_ws(L, H, max_steps, n);
 }
 
 int tt_tuner_f32tc_eligible(int32_t L, int32_t H, int32_t heads, int32_t d0, int32_t max_steps) {

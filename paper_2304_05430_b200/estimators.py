@@ -302,7 +302,7 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
             # fp32 attention (csrc/tt_tuner_x3.cu); eligibility depends on the
             # model's shapes only, so a score never depends on its batch
             fn = "tt_tuner_predict_f32tc"
-            nbytes = lib.tt_tuner_predict_f32tc_workspace_bytes(dims["L"], dims["H"], max(prog.max_steps, 1))
+            nbytes = lib.tt_tuner_predict_f32tc_workspace_bytes(dims["L"], dims["H"], max(prog.max_steps, 1), prog.n)
         else:
             nbytes = lib.tt_tuner_predict_workspace_bytes(int(prec == "fp64"), dims["L"],
                                                           dims["H"], prog.max_steps)

@@ -26,8 +26,9 @@ python tools/ncu_summary.py list $OUT/${TAG}_launches.csv > $OUT/${TAG}_launches
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:tuner_train -s 3 -c 1 \
     -o $REP/train_full python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-extra > $OUT/${TAG}_prof_train_full.log 2>&1
 python tools/ncu_summary.py rep $REP/train_full.ncu-rep > $OUT/${TAG}_ncu_full_train.txt 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:'tuner_predict|lstm_x3|attn_rows|mlp_predict|pca_tile|gbdt' -c 16 \
-    -o $REP/scoring python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e > $OUT/${TAG}_prof_scoring.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on \
+    -k regex:'tuner_predict|lstm_x3|attn_rows|attn_warp|mlp_predict|pca_tile|rank_sort|gbdt_predict' -c 30 \
+    -o $REP/scoring python tools/scoring_profile_driver.py > $OUT/${TAG}_prof_scoring.log 2>&1
 python tools/ncu_summary.py rep $REP/scoring.ncu-rep > $OUT/${TAG}_ncu_full_scoring.txt 2>&1
 ls -la $REP
 fi

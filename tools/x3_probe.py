@@ -19,7 +19,7 @@ from paper_2304_05430_b200.layout import DevicePrograms, HostPrograms  # noqa: E
 
 def f32tc(est, prog, dims, flat):
     lib = _lib.load()
-    nbytes = lib.tt_tuner_predict_f32tc_workspace_bytes(dims["L"], dims["H"], prog.max_steps)
+    nbytes = lib.tt_tuner_predict_f32tc_workspace_bytes(dims["L"], dims["H"], prog.max_steps, prog.n)
     ws = _device.workspace(nbytes, "x3probe")
     out = torch.empty(prog.n, dtype=torch.float32, device="cuda")
     _lib.call("tt_tuner_predict_f32tc", flat.data_ptr(), prog.steps.data_ptr(), prog.offsets.data_ptr(),
