@@ -30,6 +30,9 @@
 // Layer outputs: the last layer lands in S = [n][Tmax][64] (fp32, padded
 // per program), which the attention kernel reads; the layers before it
 // alternate between the program's S rows and a per-CTA scratch tile.
+#include <mutex>
+#include <vector>
+
 #include "tt_sm100.cuh"
 #include "tt_tuner.cuh"
 
@@ -113,7 +116,7 @@ struct X3Args {
   float* S;        // [n][Tmax][64]
   float* scratch;  // per CTA [128][Tmax][64]
   const unsigned char* img;
-  const int32_t* perm;  // program of each tile slot (sort_programs_by_length)
+  const int32_t* perm;  // program of each tile slot (sort_programs_by_length), null: identity
 };
 
 struct __align__(8) X3Bars {
@@ -211,7 +214,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
     // tiles are filled in order of program length (a.perm): a tile runs for
     // its longest program, so mixing lengths would waste steps
     const int64_t slot = tile * kRows + row;
-    const int64_t p = slot < a.n ? (int64_t)a.perm[slot] : a.n;
+    const int64_t p = slot < a.n ? (a.perm ? (int64_t)a.perm[slot] : slot) : a.n;
     const bool live = rowt && p < a.n;
     int64_t r0 = 0;
     int T = 0;
@@ -900,13 +903,51 @@ __global__ void __launch_bounds__(32 * x3::kAttnWarps) tuner_attn_warp_kernel(At
   }
 }
 
+// cudaFuncSetAttribute + the occupancy query only when a (device, kernel)
+// needs more shared memory than it was opened up for, or a new (threads,
+// shared memory) pair: each costs microseconds of host time, which a
+// one-program scoring call (search) would pay every time.  The attribute is
+// only ever raised (lowering it would break a concurrent larger launch).
+static int resident_blocks(const void* kern, int threads, size_t smem, int* per_sm) {
+  struct Entry {
+    int dev;
+    const void* f;
+    int threads;     // -1: the kernel's shared-memory attribute entry
+    size_t smem;     // attribute: the largest value set so far
+    int per_sm;
+  };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  TT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  Entry* attr = nullptr;
+  for (Entry& e : cache) {
+    if (e.dev != dev || e.f != kern) continue;
+    if (e.threads == threads && e.smem == smem) {
+      *per_sm = e.per_sm;
+      return TT_OK;
+    }
+    if (e.threads == -1) attr = &e;
+  }
+  if (attr == nullptr || attr->smem < smem) {
+    TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (attr)
+      attr->smem = smem;
+    else
+      cache.push_back(Entry{dev, kern, -1, smem, 0});
+  }
+  TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem));
+  cache.push_back(Entry{dev, kern, threads, smem, *per_sm});
+  return TT_OK;
+}
+
 template <int HEADS>
 static int launch_attn_warp(const AttnRowsArgs& a, cudaStream_t st) {
   const size_t smem = x3_attn_warp_smem_floats(a.dm) * sizeof(float);
   auto kern = tuner_attn_warp_kernel<HEADS>;
-  TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * x3::kAttnWarps, smem));
+  if (int rc = resident_blocks((const void*)kern, 32 * x3::kAttnWarps, smem, &per_sm)) return rc;
   TT_REQUIRE(per_sm >= 1, "tuner attention: kernel cannot be resident (smem %zu)", smem);
   const int64_t blocks = (a.n + x3::kAttnWarps - 1) / x3::kAttnWarps;
   const int grid = (int)std::min<int64_t>(blocks, (int64_t)sm_count() * per_sm);
@@ -918,9 +959,8 @@ template <int HEADS>
 static int launch_attn_rows(const AttnRowsArgs& a, cudaStream_t st) {
   const size_t smem = x3_attn_smem_floats(a.dm) * sizeof(float);
   auto kern = tuner_attn_rows_kernel<HEADS>;
-  TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, x3::kAttnThreads, smem));
+  if (int rc = resident_blocks((const void*)kern, x3::kAttnThreads, smem, &per_sm)) return rc;
   TT_REQUIRE(per_sm >= 1, "tuner attention: kernel cannot be resident (smem %zu)", smem);
   const int64_t blocks = (a.n + x3::kAttnThreads - 1) / x3::kAttnThreads;
   const int grid = (int)std::min<int64_t>(blocks, (int64_t)sm_count() * per_sm);
@@ -1001,13 +1041,19 @@ int tuner_predict_x3(const float* prm, const float* steps, const int64_t* rowoff
   w += align_up(sort_scratch_bytes(Tmax), 1024);
   a.img = img;
   tuner_x3_prepare_kernel<<<dim3(2 * L, 16), 256, 0, st>>>(a.dm, prm, img);
-  TT_CUDA(cudaFuncSetAttribute(tuner_lstm_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)x3::kSmem));
+  {
+    int per_sm = 0;
+    if (int rc = resident_blocks((const void*)tuner_lstm_x3_kernel, x3::kThreads, x3::kSmem, &per_sm)) return rc;
+    TT_REQUIRE(per_sm == 1, "tuner lstm fp32 tensor-core: expected one CTA per SM, got %d", per_sm);
+  }
   for (int64_t p0 = 0; p0 < n; p0 += chunk) {
     const int64_t nc = std::min<int64_t>(chunk, n - p0);
     a.rowoff = rowoff + p0;
-    if (int rc = sort_programs_by_length(a.rowoff, nc, Tmax, perm, sort_scr, st)) return rc;
-    a.perm = perm;
+    a.perm = nullptr;  // one tile: its order does not matter
+    if (nc > x3::kRows) {
+      if (int rc = sort_programs_by_length(a.rowoff, nc, Tmax, perm, sort_scr, st)) return rc;
+      a.perm = perm;
+    }
     a.n = nc;
     const int grid = (int)std::min<int64_t>((nc + x3::kRows - 1) / x3::kRows, x3_grid_max(Tmax, n));
     tuner_lstm_x3_kernel<<<grid, x3::kThreads, x3::kSmem, st>>>(a);
