@@ -27,6 +27,14 @@ using namespace sm100;
 
 // tanh on the MUFU's native tanh.approx (one SFU op instead of ex2 + rcp):
 // max abs error ~5e-4, inside the tf32 mode's stated 1e-2 / 1e-3 tolerance
+// accurate tanh (see the split-precision kernel below): limits exact at +-inf
+__device__ __forceinline__ float tanh_acc(float x) {
+  float e, r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(2.8853900817779268f * x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.f));
+  return fmaf(-2.f, r, 1.f);
+}
+
 __device__ __forceinline__ float tanh_ftz(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -251,8 +259,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 //                16 columns of the atom each: Xlo -> TMEM slot
 //   warps 11..18 epilogue: h1 = tanh(acc1 + b1) -> (h1hi | h1lo) in place,
 //                then tanh(acc2 + b2) . W3 + b3 -> score.
-// Activations use the accurate exp-based tanh of the fp32 CUDA-core kernel
-// (Act<float>::tanh), not tanh.approx.
+// Activations use the accurate exp-based tanh, 1 - 2 / (e^{2x} + 1), of the
+// fp32 CUDA-core kernel (Act<float>::tanh) -- not tanh.approx -- with the
+// flush-to-zero MUFU forms (ex2.approx.ftz, rcp.approx.ftz): the same two
+// SFU ops without the denormal-range fix-ups (e^{2x} + 1 >= 1 never needs
+// them), a third fewer instructions in the epilogue.
 // TMEM (512 columns): 4 Xlo slots x 32 | 2 tile buffers x 128 (acc1a |
 // acc1b -> h1hi | h1lo in place) | 1 acc2a | acc2b x 128 (read out right
 // away by the epilogue).
@@ -467,7 +478,7 @@ __global__ void __launch_bounds__(kX3Threads, 1)
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float h = Act<float>::tanh((v[i] + lo[i]) + s_b1[c0 + i]);
+          const float h = tanh_acc((v[i] + lo[i]) + s_b1[c0 + i]);
           v[i] = trunc_tf32(h);
           lo[i] = h - v[i];
         }
@@ -490,7 +501,7 @@ __global__ void __launch_bounds__(kX3Threads, 1)
       float acc = 0.f;
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        acc = fmaf(Act<float>::tanh((a2[i] + b2[i]) + s_b2[hf * 32 + i]), s_w3[hf * 32 + i], acc);
+        acc = fmaf(tanh_acc((a2[i] + b2[i]) + s_b2[hf * 32 + i]), s_w3[hf * 32 + i], acc);
       const int pb = t & 1;
       s_part[pb][hf][row] = acc;
       named_barrier(1, 256);
