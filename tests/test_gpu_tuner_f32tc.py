@@ -118,3 +118,20 @@ def test_long_programs(cuda_ok):
     seqs = random_seqs(rng, [300, 1, 17, 250])
     m = make(epochs=0, seed=6).fit(seqs, rng.uniform(0.2, 0.8, size=4))
     np.testing.assert_allclose(m.predict(seqs), otuner.predict(otuner.init_params(6), seqs), rtol=0, atol=ATOL)
+
+
+def test_uncovered_shapes_use_the_cuda_core_kernel(cuda_ok):
+    """hidden != 32 (or heads = 8) scores on the CUDA-core fp32 kernel, at the same tolerance."""
+    from paper_2304_05430_b200 import _lib
+
+    rng = np.random.default_rng(31)
+    seqs = random_seqs(rng, rng.integers(1, 8, size=60))
+    for kw, p in (({"hidden_size": 8}, otuner.init_params(2, hidden=8)), ({"attention_heads": 8}, None)):
+        m = make(epochs=0, seed=2, **kw).fit(seqs, rng.uniform(0.1, 0.9, size=60))
+        before = _lib.CALLS["tt_tuner_predict_f32"], _lib.CALLS["tt_tuner_predict_f32tc"]
+        got = m.predict(seqs)
+        assert _lib.CALLS["tt_tuner_predict_f32"] == before[0] + 1
+        assert _lib.CALLS["tt_tuner_predict_f32tc"] == before[1]
+        want = otuner.predict(p if p is not None else {k: v.copy() for k, v in m.params_.items()}, seqs,
+                              heads=kw.get("attention_heads", 2))
+        np.testing.assert_allclose(got, want, rtol=0, atol=ATOL)
