@@ -2,6 +2,9 @@
 // logistic loss (mlp.py:25-35).
 #include <stdarg.h>
 
+#include <mutex>
+#include <vector>
+
 #include "tt_ops.cuh"
 
 namespace tt {
@@ -21,6 +24,51 @@ int check_launch(const char* what) {
     set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
     return TT_ECUDA;
   }
+  return TT_OK;
+}
+
+namespace {
+struct KernelEntry {
+  int dev;
+  const void* f;
+  int threads;  // -1: the shared-memory limit entry
+  size_t smem;  // limit entry: the largest value set so far
+  int per_sm;
+};
+std::mutex g_kernel_mu;
+std::vector<KernelEntry> g_kernels;
+}  // namespace
+
+int kernel_smem(const void* kern, size_t smem) {
+  if (smem <= 48 * 1024) return TT_OK;  // below the default limit
+  int dev = 0;
+  TT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(g_kernel_mu);
+  for (KernelEntry& e : g_kernels)
+    if (e.dev == dev && e.f == kern && e.threads == -1) {
+      if (e.smem < smem) {
+        TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        e.smem = smem;
+      }
+      return TT_OK;
+    }
+  TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  g_kernels.push_back(KernelEntry{dev, kern, -1, smem, 0});
+  return TT_OK;
+}
+
+int kernel_occupancy(const void* kern, int threads, size_t smem, int* per_sm) {
+  if (int rc = kernel_smem(kern, smem)) return rc;
+  int dev = 0;
+  TT_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(g_kernel_mu);
+  for (const KernelEntry& e : g_kernels)
+    if (e.dev == dev && e.f == kern && e.threads == threads && e.smem == smem) {
+      *per_sm = e.per_sm;
+      return TT_OK;
+    }
+  TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem));
+  g_kernels.push_back(KernelEntry{dev, kern, threads, smem, *per_sm});
   return TT_OK;
 }
 
@@ -89,9 +137,7 @@ static int rank_launch(const R* y, const R* s, const int64_t* off, int32_t n_seg
   if (n_segs == 0) return TT_OK;
   size_t smem = (3 * (size_t)max_seg + 256) * sizeof(R);
   TT_REQUIRE(smem <= 200 * 1024, "rank_loss: segment too large (%lld)", (long long)max_seg);
-  if (smem > 48 * 1024)
-    TT_CUDA(cudaFuncSetAttribute(rank_loss_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+  if (int rc = kernel_smem((const void*)rank_loss_kernel<R>, smem)) return rc;
   rank_loss_kernel<R><<<n_segs, 256, smem, as_stream(st)>>>(y, s, off, loss, grad);
   return check_launch("rank_loss");
 }

@@ -38,6 +38,15 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 int sm_count();
 
+// Raise a kernel's dynamic shared-memory limit to at least `smem` -- never
+// lower it: host threads scoring concurrently launch the same kernel with
+// different sizes, and a lowered limit fails the larger launch -- and report
+// its resident CTAs per SM for (threads, smem).  Both are cached per
+// (device, kernel): the CUDA calls cost microseconds of host time a
+// one-program scoring call would otherwise pay every time (tt_base.cu).
+int kernel_smem(const void* kern, size_t smem);
+int kernel_occupancy(const void* kern, int threads, size_t smem, int* per_sm);
+
 // ------------------------------------------------------------ arithmetic --
 // Activations.  float: ex2.approx-based exp + approximate reciprocal, error a
 // few ulp (well inside the 1e-5 score tolerance; tanh.approx's 5e-4 is not).

@@ -630,7 +630,7 @@ static int mlp_predict(const R* prm, const R* X, int64_t n, int F, R* out, tt_st
   if (n == 0) return TT_OK;
   const size_t smem = sizeof(MlpSmem<R>);
   auto kern = mlp_predict_kernel<R>;
-  TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int rc = kernel_smem((const void*)kern, smem)) return rc;
   const int64_t tiles = (n + kTile - 1) / kTile;
   const int grid = (int)std::min<int64_t>(tiles, (int64_t)sm_count() * 2);
   kern<<<grid, kMT, smem, as_stream(st)>>>(prm, X, n, F, out);
@@ -688,15 +688,14 @@ static int mlp_train(R* prm, R* m, R* v, const R* X, const R* y, int F, const in
     TT_CUDA(cudaGetDevice(&dev));
     TT_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     if (B <= kMB && sm2 + 1024 <= (size_t)optin) {
-      TT_CUDA(cudaFuncSetAttribute(mlp_train_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)sm2));
+      if (int rc = kernel_smem((const void*)mlp_train_smem_kernel, sm2)) return rc;
       mlp_train_smem_kernel<<<1, kMT2, sm2, as_stream(st)>>>(a);
       return check_launch("mlp train (smem)");
     }
   }
   const size_t smem = sizeof(MlpSmem<R>);
   auto kern = mlp_train_kernel<R>;
-  TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (int rc = kernel_smem((const void*)kern, smem)) return rc;
   kern<<<1, kMT, smem, as_stream(st)>>>(a);
   return check_launch("mlp train");
 }

@@ -564,8 +564,7 @@ int mlp_predict_tc(const float* prm, const float* X, int64_t n, int F, float* ou
   CUtensorMap map;
   if (int rc = make_x_map(X, n, F, &map)) return rc;
   MlpTcParams p{prm, out, n, F, kat};
-  TT_CUDA(cudaFuncSetAttribute(mlp_predict_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  if (int rc = kernel_smem((const void*)mlp_predict_tc_kernel, smem)) return rc;
   const int64_t tiles = (n + kTcRows - 1) / kTcRows;
   const int grid = (int)std::min<int64_t>(tiles, sm_count());
   mlp_predict_tc_kernel<<<grid, kTcThreads, smem, st>>>(map, p);
@@ -590,8 +589,7 @@ int mlp_predict_x3(const float* prm, const float* X, int64_t n, int F, float* ou
   CUtensorMap map;
   if (int rc = make_x_map(X, n, F, &map)) return rc;
   MlpTcParams p{prm, out, n, F, kat};
-  TT_CUDA(cudaFuncSetAttribute(mlp_predict_x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  if (int rc = kernel_smem((const void*)mlp_predict_x3_kernel, smem)) return rc;
   const int64_t tiles = (n + kTcRows - 1) / kTcRows;
   const int grid = (int)std::min<int64_t>(tiles, sm_count());
   mlp_predict_x3_kernel<<<grid, kX3Threads, smem, st>>>(map, p);

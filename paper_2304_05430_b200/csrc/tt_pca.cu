@@ -317,9 +317,7 @@ int tt_pca_counts(const double* d_y, const double* d_s, const int64_t* h_off, in
     const size_t smem = (size_t)np2 * (8 + 4 + 4);
     TT_CUDA(cudaMemcpyAsync(d_off, h_off, sizeof(int64_t) * (n_tasks + 1), cudaMemcpyHostToDevice,
                             st));
-    if (smem > 48 * 1024)
-      TT_CUDA(cudaFuncSetAttribute(rank_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    if (int rc = kernel_smem((const void*)rank_sort_kernel, smem)) return rc;
     dim3 grid((unsigned)sort_tasks.size(), 2);
     rank_sort_kernel<<<grid, 512, smem, st>>>(d_y, d_s, d_off, d_sort, ranks);
     if (int rc = check_launch("pca rank_sort")) return rc;

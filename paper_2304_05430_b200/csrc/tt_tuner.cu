@@ -369,9 +369,8 @@ struct Launch {
     const int64_t slot = (int64_t)3 * P * dm.Tmax * dm.D + (int64_t)2 * P * dm.Tmax * dm.G;
     const size_t smem = score_smem_bytes<R, P>(dm);
     auto kern = tuner_predict_kernel<R, H, P>;
-    TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    if (int rc = kernel_occupancy((const void*)kern, kThreads, smem, &per_sm)) return rc;
     TT_REQUIRE(per_sm >= 1, "tuner predict: kernel cannot be resident (smem %zu)", smem);
     int grid = (int)std::min<int64_t>((n + P - 1) / P, (int64_t)sm_count() * per_sm);
     const size_t need = (size_t)grid * slot * sizeof(R);
@@ -448,9 +447,8 @@ struct Launch {
       if (a.cache_smem) smem += cache;
     }
     auto kern = tuner_train_kernel<R, H>;
-    TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem));
+    if (int rc = kernel_occupancy((const void*)kern, kThreads, smem, &per_sm)) return rc;
     TT_REQUIRE(per_sm >= 1, "tuner train: kernel cannot be resident (smem %zu)", smem);
     void* args[] = {&a};
     TT_CUDA(cudaLaunchCooperativeKernel((void*)kern, grid, kThreads, args, smem, st));

@@ -2032,9 +2032,8 @@ inline int fast_launch(FastArgs a, const FastPlan& p, void* ws, cudaStream_t st)
   a.ctr = reinterpret_cast<unsigned int*>(w);
   TT_CUDA(cudaMemsetAsync(a.ctr, 0, 256, st));
   auto kern = tuner_train_fast_kernel;
-  TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem));
   int per_sm = 0;
-  TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, p.smem));
+  if (int rc = kernel_occupancy((const void*)kern, kThreads, p.smem, &per_sm)) return rc;
   TT_REQUIRE(per_sm >= 1, "tuner train (fast): kernel cannot be resident (smem %zu)", p.smem);
   const int grid = fast_grid();
   void* args[] = {&a};

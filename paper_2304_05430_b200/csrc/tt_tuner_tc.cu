@@ -746,8 +746,7 @@ int tuner_predict_tc(const float* prm, const float* steps, const int64_t* rowoff
              "tuner tf32 scoring: weight images exceed the workspace");
   a.img = img;
   tuner_tc_prepare_kernel<<<dim3(L + 1, 16), 256, 0, st>>>(a.dm, prm, img);
-  TT_CUDA(cudaFuncSetAttribute(tuner_predict_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  if (int rc = kernel_smem((const void*)tuner_predict_tc_kernel, smem)) return rc;
   // chunks of 4 tiles per SM, each ordered by program length so a tile runs
   // for about its own programs' length (the result of a row does not depend
   // on its tile)

@@ -30,9 +30,6 @@
 // Layer outputs: the last layer lands in S = [n][Tmax][64] (fp32, padded
 // per program), which the attention kernel reads; the layers before it
 // alternate between the program's S rows and a per-CTA scratch tile.
-#include <mutex>
-#include <vector>
-
 #include "tt_sm100.cuh"
 #include "tt_tuner.cuh"
 
@@ -903,43 +900,8 @@ __global__ void __launch_bounds__(32 * x3::kAttnWarps) tuner_attn_warp_kernel(At
   }
 }
 
-// cudaFuncSetAttribute + the occupancy query only when a (device, kernel)
-// needs more shared memory than it was opened up for, or a new (threads,
-// shared memory) pair: each costs microseconds of host time, which a
-// one-program scoring call (search) would pay every time.  The attribute is
-// only ever raised (lowering it would break a concurrent larger launch).
 static int resident_blocks(const void* kern, int threads, size_t smem, int* per_sm) {
-  struct Entry {
-    int dev;
-    const void* f;
-    int threads;     // -1: the kernel's shared-memory attribute entry
-    size_t smem;     // attribute: the largest value set so far
-    int per_sm;
-  };
-  static std::mutex mu;
-  static std::vector<Entry> cache;
-  int dev = 0;
-  TT_CUDA(cudaGetDevice(&dev));
-  std::lock_guard<std::mutex> g(mu);
-  Entry* attr = nullptr;
-  for (Entry& e : cache) {
-    if (e.dev != dev || e.f != kern) continue;
-    if (e.threads == threads && e.smem == smem) {
-      *per_sm = e.per_sm;
-      return TT_OK;
-    }
-    if (e.threads == -1) attr = &e;
-  }
-  if (attr == nullptr || attr->smem < smem) {
-    TT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    if (attr)
-      attr->smem = smem;
-    else
-      cache.push_back(Entry{dev, kern, -1, smem, 0});
-  }
-  TT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem));
-  cache.push_back(Entry{dev, kern, threads, smem, *per_sm});
-  return TT_OK;
+  return kernel_occupancy(kern, threads, smem, per_sm);
 }
 
 template <int HEADS>

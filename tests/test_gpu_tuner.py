@@ -218,11 +218,12 @@ def test_weight_round_trip_preserves_predictions(cuda_ok):
     assert np.array_equal(clone.predict(seqs), m.predict(seqs))
 
 
-@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("precision", ["fp32", "fp32_cuda", "tf32", "fp64"])
 def test_concurrent_predict_from_worker_threads(cuda_ok, precision):
     """search.tune(jobs>1) calls predict from ThreadPoolExecutor workers
     (search.py:563-567; SPEC.md:538 'safe for concurrent predict'): results
-    from 8 threads x mixed batch sizes equal the serial ones bit for bit."""
+    from 8 threads x mixed batch sizes (and longest programs, i.e. shared-memory
+    sizes of the same kernel) equal the serial ones bit for bit."""
     from concurrent.futures import ThreadPoolExecutor
 
     rng = np.random.default_rng(7)
