@@ -1,7 +1,8 @@
 // K5 at fp32 accuracy on the 5th-generation tensor cores: attention-tuner
 // scoring (tuner.py _forward :227-285, predict :468-476) with the biLSTM
-// stack as split-precision tcgen05 GEMMs, then attention + head on the CUDA
-// cores (tt_tuner.cu, the strict-fp32 code).
+// stack as split-precision tcgen05 GEMMs (tuner_lstm_x3_kernel), then
+// attention + head in fp32 on the CUDA cores (tuner_attn_rows_kernel /
+// tuner_attn_warp_kernel, below).
 //
 // kind::tf32 truncates fp32 operands to 10 mantissa bits
 // (tools/tf32_rounding_probe.py), so every product is split
@@ -9,8 +10,8 @@
 // with x_hi = x & ~0x1fff and x_lo = x - x_hi (exact in fp32).  The weight
 // side is pre-split into one stacked B image per (layer, direction):
 //   B^T rows [0,128) = W_hi^T, rows [128,256) = W_lo^T   (K-major SWIZZLE_128B)
-// so a time step is one N=256 MMA chain (A_hi . [W_hi | W_lo]) plus one
-// N=128 chain (A_lo . W_hi) accumulating into the first half.
+// and each operand part (x, h) is three N = 128 chains into the step's gate
+// buffer: A_hi W_hi, A_lo W_hi, A_hi W_lo.
 //
 // One persistent CTA per SM, 32 + 128 kParts threads, tiles of 128 programs:
 //   warp 0        TMEM allocator (512 columns) and the single MMA-issuing lane
@@ -18,17 +19,21 @@
 //                 part p owns hidden units 4p..4p+3 and 16+4p..16+4p+3
 //                 (16 row warps, 4 per SM sub-partition, hide the MUFU
 //                 latencies of the cell better than 8: 62.7 -> 65.8 M/s)
-// TMEM columns: G [0,256)  A_hi [256, 256+K)  A_lo [352, 352+K)  (K <= 96)
-// The two directions of a layer run one after the other (one direction's
-// G + A_hi + A_lo is 448 columns).  Per step the row threads read the gate
-// pre-activations (G[0:128) + G[128:256) + bias), apply the Act<float>
-// activations of the CUDA-core kernel, update c (registers) and h, write the
-// layer output row (fp32) and the next step's A = [x_t | h] split into hi/lo.
-// Programs shorter than the tile run past their end on zero inputs; those
-// steps write nothing (the valid steps of both directions are a prefix).
+// TMEM columns: G[s & 1] [0,256)  x_hi [256,320)  x_lo [320,384)
+//               h_hi [384,416)  h_lo [416,448)
+// The two directions of a layer run one after the other (448 columns per
+// direction).  Per step s the row threads load the gates G[s & 1] (+ bias),
+// write x_{s+1} (prefetched two steps ahead by cp.async) so the MMA lane can
+// issue the next step's x chains into G[(s+1) & 1] while they run the cell
+// (5 ex2 + 3 rcp per unit: two sigmoid pairs share a reciprocal), then write
+// h, whose three short chains close the step.  Programs are ordered by
+// length per launch chunk (sort_programs_by_length) so a tile runs ~its own
+// programs' steps; warps whose programs have ended skip their epilogue; a
+// shorter program's steps past its end write nothing (the valid steps of
+// both directions are a prefix).
 //
 // Layer outputs: the last layer lands in S = [n][Tmax][64] (fp32, padded
-// per program), which the attention kernel reads; the layers before it
+// per program), which the attention kernels read; the layers before it
 // alternate between the program's S rows and a per-CTA scratch tile.
 #include "tt_sm100.cuh"
 #include "tt_tuner.cuh"
