@@ -99,7 +99,8 @@ __global__ void __launch_bounds__(256) tuner_x3_prepare_kernel(TDims dm, const f
   }
 }
 
-// clock64 marks (debug aid, tt_debug_x3_phase_times): CTA 0, first tile,
+// clock64 marks (debug aid, tt_debug_x3_phase_times): CTA 0, first tile;
+// [18 + 2 (2l + d)] / [19 + ...]: (layer, direction) start / last MMA done;
 // layer 1, forward direction, steps 2 and 3 (9 marks each): row thread 0
 // [0] d_full [1] x_{s+1} arrived [2] gates loaded [3] activations done
 // [4] h arrived; MMA lane [5] x ready [6] (unused) [7] h ready [8] committed
@@ -247,6 +248,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
         mbar_wait(&bars->w_full, pw);
         pw ^= 1;
         __syncthreads();
+        X3_MARK(mk0 && threadIdx.x == 32 && 2 * l + d < 6, 18 + 2 * (2 * l + d));  // (l, d) starts
 
         if (rowt) {
           const uint32_t Xh = tmem + lane_off + kColXh, Xl = tmem + lane_off + kColXl;
@@ -442,6 +444,7 @@ __global__ void __launch_bounds__(x3::kThreads, 1) tuner_lstm_x3_kernel(X3Args a
           }
           // next (layer, direction)'s weights while the row threads finish
           if (Tt > 0) mbar_wait(&bars->d_full, pdm ^ 1);
+          X3_MARK(mk0 && 2 * l + d < 6, 19 + 2 * (2 * l + d));  // (l, d)'s last MMA done
           int nl = l, nd = d + 1;
           bool next = true;
           if (nd == 2) {

@@ -64,12 +64,14 @@ def main():
     if "--phases" in sys.argv:
         f32tc(est, prog, dims, flat)
         torch.cuda.synchronize()
-        buf = np.zeros(18, dtype=np.int64)
-        _lib.call("tt_debug_x3_phase_times", buf.ctypes.data, 18)
+        buf = np.zeros(30, dtype=np.int64)
+        _lib.call("tt_debug_x3_phase_times", buf.ctypes.data, 30)
         names = ["d_full", "x_arrived", "gates_loaded", "act_done", "h_arrived", "mma_x_ready", "-",
                  "mma_h_ready", "mma_committed"]
         t0 = buf[0]
         print(json.dumps({f"s{2 + i // 9}_{names[i % 9]}": int(buf[i] - t0) for i in range(18) if i % 9 != 6}))
+        ld = {f"ld{k // 2}_{'start' if k % 2 == 0 else 'mma_done'}": int(buf[18 + k] - buf[18]) for k in range(12)}
+        print(json.dumps(ld))
     if "--fixed" in sys.argv:  # per-call time at uniform program lengths
         m = 4 * 148 * 128
         for T in (1, 2, 4, 7, 10):
