@@ -500,6 +500,41 @@ def sharded_extra(world, rank, dist, l2, stream, est, dims, flat):
     return out
 
 
+def gbdt_fit_throughput(n=16384, F=164, trees=20, depth=6):
+    """GradientBoostedTrees.fit (bit-exact trees, csrc/tt_gbdt.cu)
+    on a synthetic TenSet-width matrix, wall clock through the estimator (the
+    host drives the level loop), against the unmodified reference's fit on
+    the same data for a bounded number of trees (per-tree cost is flat).
+    Trees per second, and identical trees / predictions checked."""
+    import refbench
+
+    from paper_2304_05430_b200 import GradientBoostedTrees
+
+    rng = np.random.default_rng(0)
+    X = rng.normal(size=(n, F))
+    y = np.tanh(X[:, 0] - 0.5 * X[:, 1] * X[:, 2]) + 0.05 * rng.normal(size=n)
+    GradientBoostedTrees(num_trees=2, max_depth=depth).fit(X[:1024], y[:1024])  # warm
+    t0 = time.perf_counter()
+    g = GradientBoostedTrees(num_trees=trees, max_depth=depth).fit(X, y)
+    t_gpu = time.perf_counter() - t0
+    out = {"gbdt_fit_rows": n, "gbdt_fit_features": F, "gbdt_fit_depth": depth,
+           "gbdt_fit_trees_per_s": trees / t_gpu}
+    if refbench.available():
+        refbench._import_ref()
+        from tensortune.estimators.gbdt import GradientBoostedTrees as RefGBDT
+
+        k = 2
+        t0 = time.perf_counter()
+        r = RefGBDT(num_trees=k, max_depth=depth).fit(X, y)
+        t_ref = time.perf_counter() - t0
+        g2 = GradientBoostedTrees(num_trees=k, max_depth=depth).fit(X, y)
+        out.update({"gbdt_fit_reference_trees_per_s": k / t_ref,
+                    "gbdt_fit_speedup_vs_reference": (trees / t_gpu) / (k / t_ref),
+                    "gbdt_fit_identical_predictions": bool(np.array_equal(g2.predict(X[:4096]),
+                                                                          r.predict(X[:4096])))})
+    return out
+
+
 def search_throughput(n_tasks=64, steps=128):
     """Search-time scoring (SURVEY §8 f2, config 3's real caller): the
     reference's tune (simulated annealing, one candidate per scorer call)
@@ -880,6 +915,7 @@ def run_b200(args, world, rank):
         extra.update(mlp_training())
         extra.update(dp_exchange_cost())
         extra.update(search_throughput())
+        extra.update(gbdt_fit_throughput())
 
     if rank == 0:
         cpu = None

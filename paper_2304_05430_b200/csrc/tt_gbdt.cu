@@ -127,25 +127,49 @@ __global__ void gbdt_split_scan_kernel(const double* __restrict__ Xc, const doub
   double best = -INFINITY;
   int bpos = -1;
   double bxa = 0.0, bxb = 0.0;
-  for (int i = 0; i < m - 1; ++i) {
-    const int r1 = o[i + 1];
-    const double xb = x[r1];
-    const double gb = g[r1];
-    const int nl = i + 1;
-    if (xa < xb && nl >= min_leaf && m - nl >= min_leaf) {
-      const double nld = (double)nl;
-      const double nrd = __dsub_rn(md, nld);
-      const double rc = __dsub_rn(G, c);
-      const double sc = __dadd_rn(__ddiv_rn(__dmul_rn(c, c), nld), __ddiv_rn(__dmul_rn(rc, rc), nrd));
-      if (bpos < 0 || sc > best) {  // first maximum wins (np.argmax)
-        best = sc;
-        bpos = i;
-        bxa = xa;
-        bxb = xb;
-      }
+  // The prefix sum c is the only loop-carried chain; the rows' (x, g) of the
+  // next kU positions are loaded one block ahead so the indirect loads
+  // (o -> x[r], g[r]) overlap the current block instead of stalling every
+  // position.  Same operations in the same order as the plain loop.
+  constexpr int kU = 8;
+  double xn[kU], gn[kU];
+  auto load_block = [&](int i0) {  // positions i0 + 1 .. i0 + kU
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int idx = i0 + 1 + u;
+      const int r = idx < m ? o[idx] : o[0];
+      xn[u] = x[r];
+      gn[u] = g[r];
     }
-    c = __dadd_rn(c, gb);
-    xa = xb;
+  };
+  load_block(0);
+  for (int i0 = 0; i0 < m - 1; i0 += kU) {
+    double xc[kU], gc[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xc[u] = xn[u], gc[u] = gn[u];
+    if (i0 + kU < m - 1) load_block(i0 + kU);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u;
+      if (i >= m - 1) break;
+      const double xb = xc[u];
+      const double gb = gc[u];
+      const int nl = i + 1;
+      if (xa < xb && nl >= min_leaf && m - nl >= min_leaf) {
+        const double nld = (double)nl;
+        const double nrd = __dsub_rn(md, nld);
+        const double rc = __dsub_rn(G, c);
+        const double sc = __dadd_rn(__ddiv_rn(__dmul_rn(c, c), nld), __ddiv_rn(__dmul_rn(rc, rc), nrd));
+        if (bpos < 0 || sc > best) {  // first maximum wins (np.argmax)
+          best = sc;
+          bpos = i;
+          bxa = xa;
+          bxb = xb;
+        }
+      }
+      c = __dadd_rn(c, gb);
+      xa = xb;
+    }
   }
   if (bpos < 0) return;
   found[t] = 1;

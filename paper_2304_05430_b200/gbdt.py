@@ -149,9 +149,13 @@ class GradientBoostedTrees(BaseEstimator, RegressorMixin):
         self.__dict__.pop("_dev_tree_cache", None)
         lr = float(self.learning_rate)
 
-        order = np.argsort(X, axis=0, kind="stable").astype(np.int32).T.copy()
-        d_order = _device.to_dev(order)
-        d_Xc = _device.to_dev(np.ascontiguousarray(X.T))
+        # per-feature stable argsort (gbdt.py:109) on the device: ties keep row
+        # order as numpy's stable sort does; + 0.0 maps -0.0 to 0.0, which
+        # numpy also treats as equal (a bit-pattern radix sort would not)
+        d_X = _device.to_dev(np.ascontiguousarray(X))
+        d_order = t.sort(d_X + 0.0, dim=0, stable=True).indices.to(t.int32).T.contiguous()
+        d_Xc = d_X.T.contiguous()
+        del d_X
         d_y = _device.to_dev(y)
         d_pred = _device.to_dev(np.full(n, self.base_prediction_))
         d_g = _device.empty(n, t.float64)

@@ -41,6 +41,8 @@ def test_gbdt_matches_oracle_on_random_data(cuda_ok, seed, n, F, md, ml):
     rng = np.random.default_rng(seed)
     X = rng.normal(size=(n, F))
     X[:, ::3] = np.round(X[:, ::3], 1)  # ties in a third of the columns
+    # signed zeros: numpy's stable argsort treats -0.0 == 0.0 (the device presort must too)
+    X[:, 1] = rng.choice([-0.0, 0.0, 0.5, -0.5], size=n)
     y = np.tanh(X[:, 0]) + 0.3 * X[:, 1] * X[:, 2 % F] + 0.05 * rng.normal(size=n)
     Xv = rng.normal(size=(257, F))
     m = _fit(X, y, Xv, y[:257], 6, md, 0.2, ml)
