@@ -95,14 +95,70 @@ __global__ void gbdt_init_kernel(int32_t* cnt, int32_t* list0, int32_t* nstart, 
   right[0] = -1;
 }
 
-__global__ void gbdt_node_total_kernel(const double* __restrict__ g, const int32_t* __restrict__ ord0,
-                                       const int32_t* __restrict__ list, const int32_t* __restrict__ cnt,
-                                       int par, const int32_t* nstart, const int32_t* nlen, double* gtot) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// The same sum with the leaves (the <= 128-term blocks of the pairwise
+// recursion) computed by the 32 lanes of a warp, then combined by lane 0 in
+// the recursion's order: the same additions in the same order, one warp per
+// node instead of one thread (the root's 16 k indirect loads no longer sit on
+// one thread).  Nodes of <= 128 rows or more than kMaxLeaves leaves: lane 0
+// alone, as before.
+constexpr int kMaxLeaves = 2048;
+
+__device__ double np_combine(const double* leaf, int64_t len, int& idx) {
+  if (len <= 128) return leaf[idx++];
+  int64_t n2 = len / 2;
+  n2 -= n2 % 8;
+  const double a = np_combine(leaf, n2, idx);
+  const double b = np_combine(leaf, len - n2, idx);
+  return __dadd_rn(a, b);
+}
+
+__global__ void __launch_bounds__(32) gbdt_node_total_warp_kernel(const double* __restrict__ g,
+                                                                  const int32_t* __restrict__ ord0,
+                                                                  const int32_t* list, const int32_t* cnt,
+                                                                  int par, const int32_t* nstart,
+                                                                  const int32_t* nlen, double* gtot) {
+  __shared__ int32_t leaf_lo[kMaxLeaves];
+  __shared__ int16_t leaf_len[kMaxLeaves];
+  __shared__ double leaf_sum[kMaxLeaves];
+  __shared__ int32_t st_lo[32], st_len[32];
+  __shared__ int n_leaves;
+  const int k = blockIdx.x, lane = threadIdx.x;
   if (k >= cnt[par]) return;
   const int node = list[k];
   const int32_t* o = ord0 + nstart[node];
-  gtot[node] = np_sum([&](int64_t i) { return g[o[i]]; }, nlen[node]);
+  const int64_t n = nlen[node];
+  auto v = [&](int64_t i) { return g[o[i]]; };
+  if (n <= 128 || n > (int64_t)kMaxLeaves * 64) {
+    if (lane == 0) gtot[node] = np_sum(v, n);
+    return;
+  }
+  if (lane == 0) {  // leaves in order: depth-first, left first (stack in shared memory:
+                    // the recursions below need the thread's small call stack)
+    int sp = 0, nl = 0;
+    st_lo[sp] = 0, st_len[sp] = (int32_t)n, ++sp;
+    while (sp > 0) {
+      --sp;
+      const int32_t a = st_lo[sp], l = st_len[sp];
+      if (l <= 128) {
+        leaf_lo[nl] = (int32_t)a;
+        leaf_len[nl] = (int16_t)l;
+        ++nl;
+        continue;
+      }
+      int32_t n2 = l / 2;
+      n2 -= n2 % 8;
+      st_lo[sp] = a + n2, st_len[sp] = l - n2, ++sp;  // right, popped second
+      st_lo[sp] = a, st_len[sp] = n2, ++sp;
+    }
+    n_leaves = nl;
+  }
+  __syncwarp();
+  for (int i = lane; i < n_leaves; i += 32) leaf_sum[i] = np_pairwise(v, leaf_lo[i], leaf_len[i]);
+  __syncwarp();
+  if (lane == 0) {
+    int idx = 0;
+    gtot[node] = __dadd_rn(0.0, np_combine(leaf_sum, n, idx));
+  }
 }
 
 __global__ void gbdt_split_scan_kernel(const double* __restrict__ Xc, const double* __restrict__ g,
@@ -439,8 +495,8 @@ int tt_gbdt_grow(const double* Xc, const double* g, const int32_t* root_order, i
   for (int d = 0; d <= max_depth; ++d) {
     const int par = d & 1;
     const int64_t pairs = width * F;
-    gbdt_node_total_kernel<<<(unsigned)((width + 127) / 128), 128, 0, s>>>(g, w.ord[cur], w.list[par], w.cnt,
-                                                                         par, w.nstart, w.nlen, w.gtot);
+    gbdt_node_total_warp_kernel<<<(unsigned)width, 32, 0, s>>>(g, w.ord[cur], w.list[par], w.cnt, par, w.nstart,
+                                                                w.nlen, w.gtot);
     gbdt_split_scan_kernel<<<(unsigned)((pairs + 127) / 128), 128, 0, s>>>(
         Xc, g, w.ord[cur], n, F, w.list[par], w.cnt, par, w.nstart, w.nlen, w.gtot, d, max_depth, min_leaf,
         w.found, w.gain, w.cutv);
