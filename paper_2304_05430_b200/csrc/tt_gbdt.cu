@@ -161,73 +161,89 @@ __global__ void __launch_bounds__(32) gbdt_node_total_warp_kernel(const double* 
   }
 }
 
-__global__ void gbdt_split_scan_kernel(const double* __restrict__ Xc, const double* __restrict__ g,
-                                       const int32_t* __restrict__ ord, int64_t n, int F,
-                                       const int32_t* __restrict__ list, const int32_t* __restrict__ cnt,
-                                       int par, const int32_t* nstart, const int32_t* nlen,
-                                       const double* gtot, int depth, int max_depth, int min_leaf,
-                                       int8_t* found, double* gain, double* cutv) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// The split search of one (node, feature) by a warp, 32 positions at a time:
+// every lane folds the chunk's 32 gradient terms in order onto the running
+// prefix (the same sequential additions as np.cumsum; lane j keeps the
+// prefix at its position), then the lanes score their positions in parallel
+// (the two divisions per position were the single thread's bottleneck) and
+// a warp reduction keeps the first maximum (larger score, then smaller
+// position; across chunks only a strictly larger score replaces the best).
+// The same results as one thread scanning the positions in order.
+__global__ void __launch_bounds__(128) gbdt_split_scan_warp_kernel(
+    const double* __restrict__ Xc, const double* __restrict__ g, const int32_t* __restrict__ ord, int64_t n, int F,
+    const int32_t* __restrict__ list, const int32_t* __restrict__ cnt, int par, const int32_t* nstart,
+    const int32_t* nlen, const double* gtot, int depth, int max_depth, int min_leaf, int8_t* found, double* gain,
+    double* cutv) {
+  __shared__ double sg[4][32];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // (slot, feature) pair
   const int slot = (int)(t / F), j = (int)(t % F);
-  if (slot >= cnt[par]) return;
+  if (slot >= cnt[par]) return;  // warp-uniform
   const int node = list[slot];
   const int m = nlen[node];
-  found[t] = 0;
+  if (lane == 0) found[t] = 0;
   if (depth >= max_depth || m < 2 * min_leaf) return;
   const int32_t* o = ord + (int64_t)j * n + nstart[node];
   const double* x = Xc + (int64_t)j * n;
   const double G = gtot[node];
   const double md = (double)m;
-  double c = g[o[0]];
-  double xa = x[o[0]];
-  double best = -INFINITY;
+  double c = g[o[0]];        // prefix through position i0 (all lanes)
+  double xprev = x[o[0]];    // x at position i0 (for lane 0's xa)
+  double best = -INFINITY, bxa = 0.0, bxb = 0.0;
   int bpos = -1;
-  double bxa = 0.0, bxb = 0.0;
-  // The prefix sum c is the only loop-carried chain; the rows' (x, g) of the
-  // next kU positions are loaded one block ahead so the indirect loads
-  // (o -> x[r], g[r]) overlap the current block instead of stalling every
-  // position.  Same operations in the same order as the plain loop.
-  constexpr int kU = 8;
-  double xn[kU], gn[kU];
-  auto load_block = [&](int i0) {  // positions i0 + 1 .. i0 + kU
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int idx = i0 + 1 + u;
-      const int r = idx < m ? o[idx] : o[0];
-      xn[u] = x[r];
-      gn[u] = g[r];
+  for (int i0 = 0; i0 < m - 1; i0 += 32) {
+    const int i = i0 + lane;  // this lane's boundary: rows [0, i] left of it
+    const bool in = i < m - 1;
+    double xb = 0.0, gb = 0.0;
+    if (in) {
+      const int r1 = o[i + 1];
+      xb = x[r1];
+      gb = g[r1];
     }
-  };
-  load_block(0);
-  for (int i0 = 0; i0 < m - 1; i0 += kU) {
-    double xc[kU], gc[kU];
+    double xa = __shfl_up_sync(0xffffffffu, xb, 1);
+    if (lane == 0) xa = xprev;
+    sg[wib][lane] = gb;
+    __syncwarp();
+    // sequential fold: my prefix (before adding my own gb) and the chunk total
+    double mine = c, run = c;
 #pragma unroll
-    for (int u = 0; u < kU; ++u) xc[u] = xn[u], gc[u] = gn[u];
-    if (i0 + kU < m - 1) load_block(i0 + kU);
+    for (int k = 0; k < 32; ++k) {
+      if (k == lane) mine = run;
+      run = __dadd_rn(run, sg[wib][k]);
+    }
+    __syncwarp();
+    const int nl = i + 1;
+    double sc = -INFINITY;
+    bool ok = in && xa < xb && nl >= min_leaf && m - nl >= min_leaf;
+    if (ok) {
+      const double nld = (double)nl;
+      const double nrd = __dsub_rn(md, nld);
+      const double rc = __dsub_rn(G, mine);
+      sc = __dadd_rn(__ddiv_rn(__dmul_rn(mine, mine), nld), __ddiv_rn(__dmul_rn(rc, rc), nrd));
+    }
+    // first maximum of the chunk: larger score, then smaller position
+    double rsc = sc;
+    int rpos = ok ? i : 0x7fffffff;
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int i = i0 + u;
-      if (i >= m - 1) break;
-      const double xb = xc[u];
-      const double gb = gc[u];
-      const int nl = i + 1;
-      if (xa < xb && nl >= min_leaf && m - nl >= min_leaf) {
-        const double nld = (double)nl;
-        const double nrd = __dsub_rn(md, nld);
-        const double rc = __dsub_rn(G, c);
-        const double sc = __dadd_rn(__ddiv_rn(__dmul_rn(c, c), nld), __ddiv_rn(__dmul_rn(rc, rc), nrd));
-        if (bpos < 0 || sc > best) {  // first maximum wins (np.argmax)
-          best = sc;
-          bpos = i;
-          bxa = xa;
-          bxb = xb;
-        }
+    for (int off = 16; off > 0; off >>= 1) {
+      const double osc = __shfl_xor_sync(0xffffffffu, rsc, off);
+      const int opos = __shfl_xor_sync(0xffffffffu, rpos, off);
+      if (opos != 0x7fffffff && (rpos == 0x7fffffff || osc > rsc || (osc == rsc && opos < rpos))) {
+        rsc = osc;
+        rpos = opos;
       }
-      c = __dadd_rn(c, gb);
-      xa = xb;
     }
+    if (rpos != 0x7fffffff && (bpos < 0 || rsc > best)) {
+      best = rsc;
+      bpos = rpos;
+      const int src = rpos - i0;
+      bxa = __shfl_sync(0xffffffffu, xa, src);
+      bxb = __shfl_sync(0xffffffffu, xb, src);
+    }
+    c = run;
+    xprev = __shfl_sync(0xffffffffu, xb, 31);
   }
-  if (bpos < 0) return;
+  if (lane != 0 || bpos < 0) return;
   found[t] = 1;
   gain[t] = best;
   cutv[t] = __ddiv_rn(__dadd_rn(bxa, bxb), 2.0);
@@ -497,7 +513,7 @@ int tt_gbdt_grow(const double* Xc, const double* g, const int32_t* root_order, i
     const int64_t pairs = width * F;
     gbdt_node_total_warp_kernel<<<(unsigned)width, 32, 0, s>>>(g, w.ord[cur], w.list[par], w.cnt, par, w.nstart,
                                                                 w.nlen, w.gtot);
-    gbdt_split_scan_kernel<<<(unsigned)((pairs + 127) / 128), 128, 0, s>>>(
+    gbdt_split_scan_warp_kernel<<<(unsigned)((pairs + 3) / 4), 128, 0, s>>>(
         Xc, g, w.ord[cur], n, F, w.list[par], w.cnt, par, w.nstart, w.nlen, w.gtot, d, max_depth, min_leaf,
         w.found, w.gain, w.cutv);
     gbdt_decide_kernel<<<1, 1024, 0, s>>>(F, w.list[par], w.list[par ^ 1], w.cnt, par, w.nstart, w.nlen,
