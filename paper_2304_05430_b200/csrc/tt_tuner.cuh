@@ -608,7 +608,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
     R v = 0;
     if (k < D)
       v = sm.pool[p * D + k];
-    else if (ti.len[p] > 0)
+    else if (ti.prog[p] >= 0)  // a program without steps keeps its context (tuner.py:276)
       v = __ldg(ti.ctx[p] + (k - D));
     sm.z[i] = v;
   }
@@ -625,7 +625,7 @@ __device__ void attention_head_fwd(const TDims& dm, const AttnW<R>& w, const Til
     R acc = 0;
     for (int c = lane; c < kHeadHidden; c += 32) acc = fma_rn(sm.a1[p * kHeadHidden + c], w.W2[c], acc);
     acc = warp_sum(acc);
-    if (lane == 0 && ti.len[p] > 0) {
+    if (lane == 0 && ti.prog[p] >= 0) {
       const R yh = Act<R>::sigmoid(acc + w.b2);
       out_yhat[p] = yh;
       if constexpr (TRAIN) cache->yhat[0] = yh;

@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(sc::kThreads, 1) tuner_predict_tc_kernel(ScArg
         const uint32_t Gd = tmem + lane_off + kColG + d * kG;
         const uint32_t Cd = Cst + d * kH;
         const float* bd = sbias + d * kG;
-        {
+        if (Tt > 0) {  // a tile of programs without steps issues no MMAs: no hand-off either
           float z[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int j0 = 0; j0 < kH; j0 += 8) {

@@ -295,7 +295,7 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         lib = _lib.load()
         if prec == "tf32" and self._tc_eligible(dims, prog):
             fn = "tt_tuner_predict_tf32"  # tcgen05 tensor-core scoring
-            nbytes = lib.tt_tuner_predict_tf32_workspace_bytes(prog.max_steps)
+            nbytes = lib.tt_tuner_predict_tf32_workspace_bytes(max(prog.max_steps, 1))
         elif prec == "fp32" and lib.tt_tuner_f32tc_eligible(dims["L"], dims["H"], dims["heads"], dims["d0"],
                                                              max(prog.max_steps, 1)):
             # fp32 accuracy on the tensor cores: split-precision LSTM GEMMs +
@@ -305,11 +305,11 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
             nbytes = lib.tt_tuner_predict_f32tc_workspace_bytes(dims["L"], dims["H"], max(prog.max_steps, 1), prog.n)
         else:
             nbytes = lib.tt_tuner_predict_workspace_bytes(int(prec == "fp64"), dims["L"],
-                                                          dims["H"], prog.max_steps)
+                                                          dims["H"], max(prog.max_steps, 1))
         ws = _device.workspace(nbytes, "tuner_predict")
         _lib.call(fn, flat.data_ptr(), prog.steps.data_ptr(), prog.offsets.data_ptr(),
                   prog.ctx.data_ptr(), prog.n, dims["L"], dims["H"], dims["heads"], dims["U"],
-                  dims["d0"], dims["C"], prog.max_steps, out.data_ptr(), ws.data_ptr(), nbytes,
+                  dims["d0"], dims["C"], max(prog.max_steps, 1), out.data_ptr(), ws.data_ptr(), nbytes,
                   _device.stream_ptr())
         del t
         return out
@@ -504,7 +504,10 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         if len(sequences) == 0:
             return np.zeros(0)
         dims = self._dims()
-        prog = DevicePrograms.from_sequences(sequences, self._prec(), dims["d0"], dims["C"])
+        # programs without steps score as in the reference (zero pooled and
+        # context vectors, tuner.py:36-52 masks them out); training still
+        # requires >= 1 step
+        prog = DevicePrograms.from_sequences(sequences, self._prec(), dims["d0"], dims["C"], min_steps=0)
         return self._predict_programs(prog, dims).cpu().double().numpy()
 
     def predict_device(self, prog: DevicePrograms):

@@ -63,7 +63,8 @@ def _pack_native(seqs, step_width, ctx_len, alloc):
     return off
 
 
-def pack_sequences(seqs, step_width: int | None = None, ctx_len: int | None = None) -> HostPrograms:
+def pack_sequences(seqs, step_width: int | None = None, ctx_len: int | None = None,
+                   min_steps: int = 1) -> HostPrograms:
     if len(seqs) == 0:
         raise DataValidationError("empty sequence batch")
     out = {}
@@ -75,13 +76,13 @@ def pack_sequences(seqs, step_width: int | None = None, ctx_len: int | None = No
     off = _pack_native(seqs, step_width, ctx_len, alloc)
     if off is not None:
         return HostPrograms(out["s"], off, out["c"])
-    fast = _pack_fast(seqs, step_width, ctx_len)
+    fast = _pack_fast(seqs, step_width, ctx_len, min_steps)
     if fast is not None:
         return fast
-    return _pack_checked(seqs, step_width, ctx_len)
+    return _pack_checked(seqs, step_width, ctx_len, min_steps)
 
 
-def _pack_fast(seqs, step_width, ctx_len) -> HostPrograms | None:
+def _pack_fast(seqs, step_width, ctx_len, min_steps=1) -> HostPrograms | None:
     """Vectorised packing for well-formed input (numpy does the shape checks);
     None sends malformed input to the per-item path for the exact message."""
     n = len(seqs)
@@ -95,7 +96,7 @@ def _pack_fast(seqs, step_width, ctx_len) -> HostPrograms | None:
     except (ValueError, TypeError, AttributeError):
         return None
     C = int(clens[0])
-    if (steps.ndim != 2 or ctx.ndim != 1 or lens.min() < 1 or steps.shape[0] != int(lens.sum())
+    if (steps.ndim != 2 or ctx.ndim != 1 or lens.min() < min_steps or steps.shape[0] != int(lens.sum())
             or np.any(clens != C) or ctx.shape[0] != n * C):
         return None
     ctx = ctx.reshape(n, C)
@@ -107,7 +108,7 @@ def _pack_fast(seqs, step_width, ctx_len) -> HostPrograms | None:
     return HostPrograms(steps, off, ctx)
 
 
-def _pack_checked(seqs, step_width, ctx_len) -> HostPrograms:
+def _pack_checked(seqs, step_width, ctx_len, min_steps=1) -> HostPrograms:
     steps = [np.asarray(s.steps, dtype=np.float64) for s in seqs]
     ctxs = [np.asarray(s.context, dtype=np.float64) for s in seqs]
     d0 = steps[0].shape[1] if steps[0].ndim == 2 else -1
@@ -118,8 +119,8 @@ def _pack_checked(seqs, step_width, ctx_len) -> HostPrograms:
         raise DataValidationError(f"context must have {ctx_len} slots, got {ctxs[0].shape}")
     lens = np.empty(len(seqs), dtype=np.int64)
     for i, (st, cx) in enumerate(zip(steps, ctxs)):
-        if st.ndim != 2 or st.shape[1] != d0 or st.shape[0] < 1:
-            raise DataValidationError(f"steps must be (n >= 1, {d0}), got {st.shape}")
+        if st.ndim != 2 or st.shape[1] != d0 or st.shape[0] < min_steps:
+            raise DataValidationError(f"steps must be (n >= {min_steps}, {d0}), got {st.shape}")
         if cx.shape != (C,):
             raise DataValidationError(f"context must have {C} slots, got {cx.shape}")
         lens[i] = st.shape[0]
@@ -146,7 +147,7 @@ class DevicePrograms:
         self.host_offsets = offsets
 
     @classmethod
-    def from_sequences(cls, seqs, precision="fp32", step_width=None, ctx_len=None):
+    def from_sequences(cls, seqs, precision="fp32", step_width=None, ctx_len=None, min_steps=1):
         """Host sequences -> device CSR.  With the native packer the rows are
         converted straight into ONE pinned staging buffer [steps | ctx |
         offsets] in the compute dtype and uploaded with one async copy."""
@@ -168,8 +169,8 @@ class DevicePrograms:
             return hb[:ns * esz].view(npdt), hb[o_c:o_c + nc * esz].view(npdt)
 
         off = _pack_native(seqs, step_width, ctx_len, alloc)
-        if off is None:
-            return cls(pack_sequences(seqs, step_width, ctx_len), precision)
+        if off is None:  # malformed input, or programs without steps (predict)
+            return cls(pack_sequences(seqs, step_width, ctx_len, min_steps), precision)
         o = out
         o["hb"][o["o_o"]:].view(np.int64)[:] = off
         dev = o["buf"].to(_device.device(), non_blocking=True)

@@ -135,3 +135,26 @@ def test_uncovered_shapes_use_the_cuda_core_kernel(cuda_ok):
         want = otuner.predict(p if p is not None else {k: v.copy() for k, v in m.params_.items()}, seqs,
                               heads=kw.get("attention_heads", 2))
         np.testing.assert_allclose(got, want, rtol=0, atol=ATOL)
+
+
+@pytest.mark.parametrize("precision,atol", [("fp32", ATOL), ("fp32_cuda", ATOL), ("fp64", 1e-12), ("tf32", 2e-3)])
+def test_empty_programs(cuda_ok, precision, atol):
+    """A program with no steps scores like the reference (pooled and context
+    vectors zero), alone and inside a batch; an all-empty batch too."""
+    from conftest import Seq
+
+    rng = np.random.default_rng(41)
+    seqs = random_seqs(rng, [3, 1, 5])
+    m = make(precision, epochs=0, seed=7).fit(seqs, rng.uniform(0.2, 0.8, size=3))
+    empty = Seq(np.zeros((0, 6)), rng.normal(size=35))
+    batch = [seqs[0], empty, seqs[1], empty, seqs[2]]
+    p = otuner.init_params(7)
+    got = m.predict(batch)
+    np.testing.assert_allclose(got, otuner.predict(p, batch), rtol=0, atol=atol)
+    # an all-empty batch (the reference's numpy reshape raises on it): the same scores
+    np.testing.assert_array_equal(m.predict([empty, empty]), [got[1], got[3]])
+    # whole tiles of empty programs (the reference's 256-program chunks would
+    # hit the same reshape): each scores as above, the others as alone
+    many = m.predict([empty] * 300 + seqs)
+    np.testing.assert_array_equal(many[:300], np.full(300, got[1]))
+    np.testing.assert_allclose(many[300:], otuner.predict(p, seqs), rtol=0, atol=atol)
