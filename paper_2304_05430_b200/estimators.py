@@ -372,7 +372,7 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         dims = self._dims()
         prec = self._prec()
         dt = _device.real_dtype(prec)
-        prog = DevicePrograms.from_sequences(sequences, prec, dims["d0"], dims["C"])
+        prog = DevicePrograms.from_sequences(sequences, prec, dims["d0"], dims["C"], min_steps=0)
         y = np.asarray(y, dtype=np.float64)
         n = prog.n
         if y.shape != (n,):
@@ -426,7 +426,7 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         dims = self._dims()
         prec = self._prec()
         dt = _device.real_dtype(prec)
-        prog = DevicePrograms.from_sequences(sequences, prec, dims["d0"], dims["C"])
+        prog = DevicePrograms.from_sequences(sequences, prec, dims["d0"], dims["C"], min_steps=0)
         y_dev = _device.to_dev(y, dt)
         flat = self._dev_params(dims).clone()
         NP = flat.numel()
@@ -444,7 +444,7 @@ class RecurrentAttentionTuner(_GpuParamsMixin, BaseEstimator, RegressorMixin):
         _warn_if_slow_path(dims, prec, prog.max_steps, B)
         ev = None
         if eval_set is not None:
-            eprog = DevicePrograms.from_sequences(eval_set[0], prec, dims["d0"], dims["C"])
+            eprog = DevicePrograms.from_sequences(eval_set[0], prec, dims["d0"], dims["C"], min_steps=0)
             ey = np.asarray(eval_set[1], dtype=np.float64)
             gperm = goff = None
             if eval_groups is not None:

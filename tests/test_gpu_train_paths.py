@@ -241,3 +241,29 @@ def test_long_programs_warn_about_the_generic_kernel(cuda_ok):
         RecurrentAttentionTuner(epochs=1, batch_size=8).fit(short, y)
     with pytest.warns(PerformanceWarning, match="generic kernel"):
         RecurrentAttentionTuner(epochs=1, batch_size=8).fit(long_, y)
+
+
+@pytest.mark.parametrize("precision,hidden,layers", [("fp64", 4, 1), ("fp32", 32, 3)])
+def test_training_with_programs_without_steps(cuda_ok, precision, hidden, layers):
+    """The reference trains on programs without steps (masked out, context
+    kept); so do the kernels -- generic (fp64) and latency path (fp32)."""
+    from conftest import Seq, random_seqs
+    from oracle import tuner as otuner
+    from paper_2304_05430_b200 import RecurrentAttentionTuner
+
+    rng = np.random.default_rng(51)
+    seqs = random_seqs(rng, rng.integers(1, 9, size=48))
+    for i in (5, 17, 30):
+        seqs[i] = Seq(np.zeros((0, 6)), seqs[i].context)
+    y = rng.uniform(0.1, 0.9, size=48)
+    m = RecurrentAttentionTuner(epochs=2, batch_size=8, hidden_size=hidden, recurrent_layers=layers,
+                                loss="ranking", seed=4)
+    m.precision = precision
+    m.fit(seqs, y)
+    p = otuner.init_params(4, layers=layers, hidden=hidden)
+    curve = otuner.train(p, seqs, y, epochs=2, lr=1e-3, batch_size=8, seed=4, loss="ranking")
+    rt = 1e-8 if precision == "fp64" else 1e-3
+    np.testing.assert_allclose([c[0] for c in m.train_curve_], [c[0] for c in curve], rtol=rt)
+    for k in p:
+        err = np.linalg.norm(m.params_[k] - p[k]) / max(np.linalg.norm(p[k]), 1e-12)
+        assert err <= (1e-8 if precision == "fp64" else 2e-3), (k, err)
