@@ -3,8 +3,9 @@
 
   tuner_train_fast_kernel (latency path, B = 16, and multi-round B = 300 on
   a reduced grid), the fused data-parallel kernel (2 ranks on one GPU), the
-  generic train kernel (hidden 4), tuner_predict (fp32 / fp64) and the
-  tcgen05 tf32 scorer, mlp predict (fp32 / tf32) and mlp train, PCA, top-k,
+  generic train kernel (hidden 4), tuner_predict (fp32 tensor-core
+  split-precision incl. its bulk path and programs without steps, fp32_cuda,
+  fp64) and the tcgen05 tf32 scorer, mlp predict (fp32 / tf32) and mlp train, PCA, top-k,
   pruning statistics and the GBDT kernels.
 """
 import sys
@@ -68,9 +69,16 @@ if step("dp"):
             rk.close()
 if step("predict"):
     m = RecurrentAttentionTuner(epochs=0, seed=1).fit(seqs, y)
-    for prec in ("fp32", "fp64", "tf32"):
+    for prec in ("fp32", "fp32_cuda", "fp64", "tf32"):
         m.precision = prec
         m.predict(seqs * 5)
+    # the fp32 tensor-core scorer's bulk path (length sort, thread-per-program
+    # attention) and programs without steps
+    from conftest import Seq  # noqa: E402
+
+    m.precision = "fp32"
+    m.predict(seqs * 320)
+    m.predict([Seq(np.zeros((0, 6)), seqs[0].context)] * 200 + seqs)
 if step("mlp"):
     X = rng.normal(size=(300, 164))
     mm = CostMLP(epochs=1, seed=0, loss="ranking").fit(X, rng.normal(size=300))
