@@ -62,6 +62,8 @@ def main():
                       "f32tc_mean_err": float(np.abs(otc - ref).mean()),
                       "fp32_cuda_per_s": prog.n / t32, "f32tc_per_s": prog.n / ttc}), flush=True)
     if "--phases" in sys.argv:
+        if "--n1" in sys.argv:  # one program: the latency of a single-tile call
+            prog = DevicePrograms(HostPrograms(st[: of[1]], of[:2], cx[:1]), "fp32")
         f32tc(est, prog, dims, flat)
         torch.cuda.synchronize()
         buf = np.zeros(30, dtype=np.int64)
