@@ -158,3 +158,17 @@ def test_empty_programs(cuda_ok, precision, atol):
     many = m.predict([empty] * 300 + seqs)
     np.testing.assert_array_equal(many[:300], np.full(300, got[1]))
     np.testing.assert_allclose(many[300:], otuner.predict(p, seqs), rtol=0, atol=atol)
+
+
+def test_saturated_activations(cuda_ok):
+    """Step values large enough to saturate every gate (the cell clamps its
+    exponent arguments at +-43 so the shared reciprocals stay finite): still
+    within the fp32 tolerance of the float64 oracle, no NaN."""
+    rng = np.random.default_rng(61)
+    seqs = random_seqs(rng, rng.integers(1, 11, size=200))
+    for s in seqs[::2]:
+        s.steps *= 300.0  # pre-activations in the hundreds
+    m = make(epochs=0, seed=8).fit(seqs, rng.uniform(0.1, 0.9, size=200))
+    got = m.predict(seqs)
+    assert np.all(np.isfinite(got))
+    np.testing.assert_allclose(got, otuner.predict(otuner.init_params(8), seqs), rtol=0, atol=ATOL)
