@@ -837,6 +837,20 @@ def run_b200(args, world, rank):
         extra["scoring_tflops"] = float(np.sum(134656.0 * lens + 45568.0)) / sc_t / 1e12
         extra["scoring_fp32_path"] = ("tt_tuner_predict_f32tc: split-precision tcgen05 biLSTM "
                                       "(x_hi.w_hi + x_lo.w_hi + x_hi.w_lo) + fp32 CUDA-core attention")
+        # where it sits (DESIGN 3.2b): the biLSTM's dense FLOPs run 3x on the
+        # tensor cores (three tf32 chains), its cell issues 8 MUFU ops per
+        # hidden unit and step; both against this box's peaks
+        lstm_flops = float(np.sum(2.0 * 58880.0 * lens))  # 3 layers x 2 dirs, x and h GEMVs
+        mufu_ops = float(np.sum(6.0 * 32 * 8 * lens))
+        tf32_peak = 0.5 * float(peaks.get("bf16_tflops_sustained", 1400.0))
+        extra["scoring_fp32_roofline"] = {
+            "bound": "latency of the per-step chain (gates -> x -> cell -> h MMAs)",
+            "tensor_tflops_tf32": 3.0 * lstm_flops / sc_t / 1e12,
+            "frac_of_tf32_peak": 3.0 * lstm_flops / sc_t / 1e12 / tf32_peak,
+            "mufu_ops_per_s": mufu_ops / sc_t,
+            "frac_of_mufu_peak": mufu_ops / sc_t / 4.62e12,
+            "peaks": f"tf32 = bf16_tflops_sustained / 2 = {tf32_peak:.0f} TFLOP/s (MEASURED_PEAKS.json); "
+                     "MUFU 4.62e12 ops/s (profiles/r2_issue_peaks.json)"}
         # the strict CUDA-core fp32 kernel ("fp32_cuda", the round-1 default)
         est.precision = "fp32_cuda"
         est._predict_programs(prog, dims, flat)
